@@ -1,0 +1,352 @@
+#!/usr/bin/env python
+"""bench.py -- decode tokens/s and achieved HBM GB/s (% of roofline) of the sparse
+mixed-precision FFN decode step (M2Cache, arXiv 2410.14740) on B200.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config S7|S13|S70|S70H|T]
+                  [--impl reference] [--no-cpu-baseline]
+
+A step = one decode token through the whole synthetic FFN stack (all L layers: predictor,
+top-k + tier split, cache lookup/fill, fused dequant-GEMV FFN, reduce/all-reduce, residual).
+N = 1 default workload: configs[1], the LLaMA-2-7B-shaped stack (32 x 4096 x 11008), whole
+model resident.  N > 1 (torchrun): configs[3], the 70B-shaped stack with d_ff sharded over
+the N ranks (one NCCL all-reduce per layer), total work fixed ("strong").
+Prints ONE JSON line (rank 0).  --impl reference times the CPU oracle instead (the tier's
+reference arm).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "decode tokens/s & achieved HBM GB/s (% of roofline), sparse MP FFN, 1/2/4/8 B200"
+WORKLOAD = {
+    "T": "configs[0]: single FFN layer 256x688, 10% active FP16/INT8/INT4 1:1:2, resident",
+    "S7": "configs[1]: LLaMA-2-7B-shaped FFN stack 32 x (4096 x 11008), 10% active 1:1:2, "
+          "whole model resident in HBM, batch-1 decode",
+    "S13": "configs[2]: LLaMA-2-13B-shaped FFN stack 40 x (5120 x 13824), 10% active 1:1:2, "
+           "HBM neuron cache capped at 25% of FFN FP16 bytes, LRU misses filled from pinned host",
+    "S70": "configs[3]: LLaMA-2-70B-shaped FFN stack 80 x (8192 x 28672), 10% active 1:1:2, "
+           "d_ff sharded over the ranks, NCCL all-reduce of down-projection partials",
+    "S70H": "configs[3] at 1 GPU: 40-layer half-depth 70B-shaped stack (all 80 layers x 3 tiers "
+            "= 199.9 GB exceed one B200)",
+}
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi-equivalent clock / throttle sampling (NVML) during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.02)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        s = sorted(self.samples)
+        return {"sm_mhz": s[len(s) // 2] if s else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(s)}
+
+
+def algorithmic_bytes(cfg, plan, P):
+    """per layer Σ_t k_t nb_t (active records) + r d (A) + F_r r (B) + 2d (x);
+    the per-launch FFN figure is Σ_t k_t nb_t + 2d."""
+    from paper_2410_14740_b200 import record_bytes
+    d, r = cfg.d_model, cfg.pred_rank
+    F_r = cfg.d_ff // P
+    rec = sum(k * record_bytes(b, d) for k, b in zip(plan.as_tuple()[1:], (16, 8, 4)))
+    return {"ffn_per_launch": rec + 2 * d, "layer": rec + r * d + F_r * r + 2 * d,
+            "token": cfg.n_layers * (rec + r * d + F_r * r + 2 * d)}
+
+
+def oracle_sample(cfg, P, layers, tokens, device_weights=None):
+    """Time the CPU oracle (as it stands, 1 thread) on a bounded sample: `tokens` tokens through
+    `layers` layers of the workload; returns seconds per (token, layer) and the sample string."""
+    import numpy as np
+    from oracle import oracle as orc
+    from synth import layer_weights, token_stream
+
+    plan = orc.tier_plan(cfg.d_ff // P, cfg.active_pct, cfg.a16, cfg.a8, cfg.den)
+    xs = token_stream(cfg, tokens).numpy()
+    total, n = 0.0, 0
+    for l in range(layers):
+        w = {k: v.numpy() for k, v in layer_weights(cfg, l, shard=(0, P)).items()}
+        # untimed: pack (offline in the method) the neurons this sample selects
+        ids = np.unique(np.concatenate([
+            orc.select(orc.predict(x, w["pred_A"], w["pred_B"])["s"], plan)["tier_ids"]
+            for x in xs]))
+        recs = {}
+        F_r, d = w["w_gate"].shape
+        for b in (16, 8, 4):
+            recs[b] = np.zeros((F_r, orc.record_bytes(b, d)), np.uint8)
+            for i in ids:
+                recs[b][i] = orc.pack(b, w["w_gate"], w["w_up"], w["w_down_t"], int(i), int(i) + 1)[0]
+        for x in xs:
+            t0 = time.perf_counter()
+            orc.layer_forward(w, recs, x, plan, act=0 if cfg.act == "silu" else 1)
+            total += time.perf_counter() - t0
+            n += 1
+    return total / n, f"{tokens} tokens x {layers} layers of the {cfg.name} workload (shard 0/{P}), " \
+                      f"1 thread, oracle pack untimed; scaled x{cfg.n_layers} layers per token"
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the tier's reference arm is the CPU oracle (it runs on host cores)."""
+    from synth import get_config
+    if rank != 0:
+        return
+    cfg = get_config(args.config or ("S7" if world == 1 else "S70"))
+    P = world if cfg.name == "S70" else 1
+    steps = max(1, min(args.steps, 64))
+    per, sample = oracle_sample(cfg, P, 1, max(1, min(args.warmup, 2)) + steps)
+    value = 1.0 / (per * cfg.n_layers)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s",
+            "n_gpus": world, "steps": steps, "warmup": args.warmup,
+            "ms_per_step": per * 1e3, "higher_is_better": True,
+            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded; SURVEY §8(d) recipe)",
+            "config": {"workload": WORKLOAD[cfg.name], "model": cfg.name},
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": 1, "kind": "oracle",
+                             "sample": sample + "; each step = one (token, layer)"},
+            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=256)
+    ap.add_argument("--warmup", type=int, default=16)
+    ap.add_argument("--config", default=None)
+    ap.add_argument("--impl", default="m2c", choices=["m2c", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--eager", action="store_true", help="no CUDA graph")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE={world}"
+    if args.impl == "reference":
+        return run_reference(args, world, rank)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2410_14740_b200 import (M2CContext, cache_cfg_capped, nccl_unique_id, plan_of)
+    from synth import get_config, layer_weights, token_stream
+
+    assert args.warmup >= 3, "timing rules: W >= 3"
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = get_config(args.config or ("S7" if world == 1 else "S70"))
+    P = world if world > 1 else 1
+    if cfg.name == "S70" and P == 1:
+        cfg = get_config("S70H")
+    plan = plan_of(cfg, P)
+    ctx = M2CContext(cfg.d_model, cfg.d_ff, cfg.n_layers, cfg.pred_rank, plan, shard=(rank, P),
+                     act=0 if cfg.act == "silu" else 1, device=local)
+    if P > 1:
+        uid = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        ctx.comm_init(P, rank, uid[0])
+    cc = None
+    if cfg.cache_mode != "resident":
+        cc = cache_cfg_capped(ctx.desc, plan, 1, 4, cfg.cache_mode)
+        ctx.reserve_host_tier(cfg.n_layers * ctx.layer_footprint(cc)[1])
+    t_load = time.time()
+    for l in range(cfg.n_layers):
+        w = layer_weights(cfg, l, device=dev, shard=(rank, P))
+        ctx.load_layer(l, w["w_gate"], w["w_up"], w["w_down_t"], w["pred_A"], w["pred_B"], cc)
+        del w
+    torch.cuda.synchronize()
+    t_load = time.time() - t_load
+    torch.cuda.empty_cache()
+    if args.eager:
+        ctx.set_graph(False)
+
+    W, K = args.warmup, args.steps
+    if cfg.cache_mode != "resident":
+        W = max(W, cfg.warmup_tokens)  # LRU warm-up
+    toks = token_stream(cfg, W + K, device=dev)
+    x = torch.empty(cfg.d_model, dtype=torch.float16, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    step = 1
+    for t in range(W):
+        x.copy_(toks[t])
+        ctx.decode_step(x, step)
+        step += 1
+    ctx.stats(reset=True)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- timed region: K tokens, inputs resident in HBM ----
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        e0.record(stream)
+        for t in range(W, W + K):
+            x.copy_(toks[t])
+            ctx.decode_step(x, step)
+            step += 1
+        e1.record(stream)
+        barrier()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        tmax = torch.tensor([ms], device=dev)
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        ms = float(tmax.item())
+    st = ctx.stats()
+    kpt = st["kernels_per_token"]
+    tok_s = K / (ms / 1e3)
+    ab = algorithmic_bytes(cfg, plan, P)
+    peak, peak_src = _peaks()
+    gbs = ab["token"] * K / (ms / 1e3) / 1e9 * P / P  # per-GPU bytes x tokens / time
+
+    # ---- phase breakdown + dominant-kernel roofline (events inside the graph) ----
+    ctx.profile(True)
+    prof = [[0.0] * 4 for _ in range(cfg.n_layers)]
+    nprof = min(K, 32)
+    for t in range(nprof):
+        x.copy_(toks[W + t % K])
+        ctx.decode_step(x, step)
+        step += 1
+        p, n_ffn = ctx.profile_read()
+        for l in range(cfg.n_layers):
+            for i in range(4):
+                prof[l][i] += p[l][i] / nprof
+    ctx.profile(False)
+    phase_ms = [sum(prof[l][i] for l in range(cfg.n_layers)) for i in range(4)]
+    ffn_launch_ms = phase_ms[2] / (cfg.n_layers * n_ffn)
+    ffn_bytes_launch = ab["ffn_per_launch"] / n_ffn
+    achieved = ffn_bytes_launch / (ffn_launch_ms / 1e3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ffn_traffic.json")) as f:
+            traffic = json.load(f).get(cfg.name)
+    except Exception:
+        pass
+
+    # ---- end to end through the public API: pinned host in, host out, every step ----
+    e2e = None
+    if not args.no_e2e:
+        xh = toks[W:W + K].cpu().pin_memory()
+        yh = torch.empty(cfg.d_model, dtype=torch.float16).pin_memory()
+        barrier()
+        t0 = time.perf_counter()
+        for t in range(K):
+            x.copy_(xh[t], non_blocking=True)
+            ctx.decode_step(x, step)
+            step += 1
+            yh.copy_(x, non_blocking=True)
+            stream.synchronize()
+        barrier()
+        el = time.perf_counter() - t0
+        if world > 1:
+            te = torch.tensor([el], device=dev)
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+            el = float(te.item())
+        e2e = {"value": K / el, "unit": "tokens/s", "h2d_bytes_per_step": 2 * cfg.d_model,
+               "d2h_bytes_per_step": 2 * cfg.d_model}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        per, sample = oracle_sample(cfg, P, 1, 12)
+        cpu = {"value": 1.0 / (per * cfg.n_layers), "unit": "tokens/s", "cores": 1,
+               "kind": "oracle", "sample": sample}
+
+    if rank == 0:
+        hits, miss = st["hits"], st["misses"]
+        line = {
+            "metric": METRIC, "value": tok_s, "unit": "tokens/s", "n_gpus": world, "steps": K,
+            "warmup": W, "ms_per_step": ms / K, "higher_is_better": True,
+            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f16",
+            "data": "synthetic (seeded random-init weights/tokens, SURVEY §8(d) recipe)",
+            "config": {"workload": WORKLOAD[cfg.name], "model": cfg.name,
+                       "layers": cfg.n_layers, "d_model": cfg.d_model, "d_ff": cfg.d_ff,
+                       "active_pct": cfg.active_pct, "tier_plan": list(plan.as_tuple()),
+                       "cache": cfg.cache_mode, "global_batch": 1, "seq_len": 1,
+                       "parallelism": f"dff-shard{P}" if P > 1 else "single",
+                       "l2": "inputs larger than L2 (%.0f MB touched per token)" % (ab["token"] / 1e6),
+                       "graph": not args.eager},
+            "hbm_gbs": gbs, "hbm_frac": gbs / peak,
+            "roofline": {"kernel": "k_ffn (fused dequant-GEMV + SiLU*mul + down)", "bound": "hbm",
+                         "achieved": achieved, "peak": peak, "peak_src": peak_src,
+                         "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                         "bytes_per_launch": ffn_bytes_launch, "ms_per_launch": ffn_launch_ms},
+            "phase_ms_per_token": dict(zip(["predict", "select", "cache+ffn", "reduce"], phase_ms)),
+            "gpu_launches": kpt * K,
+            "kernels_per_token": kpt,
+            "clocks": clk.summary(),
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "load_s": t_load,
+        }
+        if cfg.cache_mode != "resident":
+            line["cache"] = {"hits": hits, "misses": miss,
+                             "hit_ratio": [h / max(1, h + m) for h, m in zip(hits, miss)]}
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,202 @@
+/*
+ * m2c.h -- C ABI of libm2c: the B200-native (sm_100a) dynamic sparse mixed-precision FFN
+ * decode step of M2Cache (arXiv 2410.14740).
+ *
+ * Citations: P:L = PAPER.md line L (section); DESIGN.md R# = the reading taken where the
+ * paper is silent.  The calls follow the paper's statement of the problem
+ * (P:73): 1) Active Neuron Identification (m2c_predict_rank), 2) Selective Loading into GPU
+ * (m2c_cache_lookup_fill), 3) Active Score-based Quantization (m2c_quant_pack /
+ * m2c_load_layer), then the sparse FFN over the mixed-precision active neurons
+ * (m2c_sparse_ffn_forward) and the whole-token driver (m2c_decode_step).
+ *
+ * Conventions (all calls):
+ *   - Pointers named *_dev / device buffers are CUDA device pointers; "device or pinned"
+ *     pointers may also be page-locked host memory (UVA-mapped).  Pageable host memory is
+ *     never accepted except where stated (host-side structs).
+ *   - All large memory is CALLER-OWNED (PyTorch allocates it); the library never frees caller
+ *     memory.  The context owns only a small workspace (see m2c_create).
+ *   - fp16 tensors are IEEE binary16, passed as void* (no CUDA types in the ABI).
+ *   - Asynchronous calls are enqueued on the context's compute stream (borrowed from the
+ *     caller, who keeps it alive); CUDA errors of enqueued kernels surface as M2C_ERR_CUDA on
+ *     the next synchronising call.  Host-side validation happens before any launch; on error
+ *     nothing is enqueued.  m2c_last_error() returns a thread-local message.
+ *   - F_r = d_ff / shard_count is the rank-local neuron count; neuron ids in every list are
+ *     rank-local (global id = shard_index * F_r + local id).
+ */
+#ifndef M2C_H
+#define M2C_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define M2C_ABI_VERSION 1
+
+typedef struct m2c_ctx m2c_ctx;
+typedef struct CUstream_st *m2c_stream_t; /* == cudaStream_t, borrowed */
+typedef struct CUevent_st *m2c_event_t;   /* == cudaEvent_t, borrowed */
+
+typedef enum {
+    M2C_OK = 0,
+    M2C_ERR_INVALID_ARG = 1, /* null / misaligned pointer, bad bits, bad range */
+    M2C_ERR_CONFIG = 2,      /* inconsistent model / plan (e.g. tiers do not sum to k) */
+    M2C_ERR_CAPACITY = 3,    /* cache capacity < k_tau, or > the per-pool limit */
+    M2C_ERR_CUDA = 4,        /* a CUDA runtime call or kernel failed */
+    M2C_ERR_NCCL = 5,        /* NCCL missing or an NCCL call failed */
+    M2C_ERR_STATE = 6        /* call order violated (e.g. step not increasing, layer not loaded) */
+} m2c_status;
+
+/* Model shape of one rank.  d_model % 256 == 0 and <= 8192 (128-element quantisation groups,
+ * R4, and 8-element chunks per thread in the FFN kernel); group == 128; d_ff % shard_count == 0;
+ * pred_rank = 16 * 2^j <= 512; act 0 = SiLU, 1 = ReLU (R6).  Violations: M2C_ERR_CONFIG. */
+typedef struct {
+    int32_t d_model, d_ff, n_layers, pred_rank, group;
+    int32_t shard_index, shard_count;
+    int32_t act;
+} m2c_model_desc;
+
+/* Active set size and its split into FP16 / INT8 / INT4 tiers (R3). */
+typedef struct {
+    int32_t k, k_fp16, k_int8, k_int4;
+} m2c_tier_plan;
+
+/* HBM neuron cache of one layer: mode 0 = resident (all F_r neurons of all tiers in HBM,
+ * identity slots), 1 = LRU (R7), 2 = ATU (LRU with cap_slots[t] == k_t).
+ * cap_slots[t] = slots of the tier-t pool (t: 0 FP16, 1 INT8, 2 INT4); ignored if resident. */
+typedef struct {
+    int32_t mode;
+    int32_t cap_slots[3];
+} m2c_cache_cfg;
+
+/* ---- helpers (pure host functions, no CUDA) -------------------------------------------- */
+const char *m2c_last_error(void);
+int32_t m2c_abi_version(void);
+
+/* Bytes of one packed neuron record of a tier (R1, R4): FP16 6d; INT8 3d + 9d/128;
+ * INT4 3d/2 + 9d/128; each padded to 16 B.  Returns -1 for bad arguments. */
+int64_t m2c_record_bytes(int32_t tier_bits, int32_t d_model);
+
+/* R3: k = floor(active_pct * F_r / 100); k16 = floor(k*a16/den); k8 = floor(k*a8/den);
+ * k4 = k - k16 - k8.  (25, 25, 100) is the paper's 25/25/50 mix. */
+m2c_status m2c_tier_plan_make(int32_t F_r, int32_t active_pct, int32_t a16, int32_t a8,
+                              int32_t den, m2c_tier_plan *out);
+
+/* R8: capped LRU sizing.  budget = budget_num/budget_den x FP16 bytes of the layer FFN (6 d F_r);
+ * cap_slots[t] = floor(M k_t), M = budget / sum_t k_t nb_t (computed in double). */
+m2c_status m2c_cache_cfg_capped(const m2c_model_desc *desc, const m2c_tier_plan *plan,
+                                int32_t budget_num, int32_t budget_den, int32_t mode,
+                                m2c_cache_cfg *out);
+
+/* Sizes of the caller-owned regions m2c_load_layer needs for one layer: hbm_bytes (device:
+ * predictor + tier pools + cache metadata), host_pinned_bytes (pinned host tier: all three
+ * tiers packed, LRU/ATU only; 0 if resident).  Each region must be 256-B aligned. */
+m2c_status m2c_layer_footprint(const m2c_model_desc *desc, const m2c_cache_cfg *cfg,
+                               size_t *hbm_bytes, size_t *host_pinned_bytes);
+
+/* ---- context --------------------------------------------------------------------------- */
+/* Creates a context on `device` with borrowed streams `compute` and `copy` (copy carries the
+ * miss fills, "dedicated CUDA streams").  `decode_plan` is the plan m2c_decode_step
+ * uses.  The context allocates a small device workspace (O(F_r + k + 148 d) bytes). */
+m2c_status m2c_create(const m2c_model_desc *desc, int32_t device, m2c_stream_t compute,
+                      m2c_stream_t copy, const m2c_tier_plan *decode_plan, m2c_ctx **out);
+m2c_status m2c_destroy(m2c_ctx *ctx);
+
+/* ---- a0: pack (P:73 step 3; R1, R4) -------------------------------------- */
+/* Packs neurons [n_begin, n_end) of one tier (16, 8 or 4 bits) into `records_out`
+ * (n_end - n_begin records of m2c_record_bytes(tier_bits, d) bytes, record i = neuron
+ * n_begin + i).  Inputs are neuron-major fp16 [n][d]: W_gate rows, W_up rows, W_down
+ * columns (= rows of W_down^T).  Pointers: device or pinned, 16-B aligned.  Bit-exact
+ * contract (tests compare every byte with the oracle).  Asynchronous on `stream`. */
+m2c_status m2c_quant_pack(int32_t d_model, int32_t tier_bits, const void *w_gate,
+                          const void *w_up, const void *w_down_t, int64_t n_begin, int64_t n_end,
+                          void *records_out, m2c_stream_t stream);
+
+/* ---- layer load ------------------------------------------------------------------------ */
+/* Copies the predictor (pred_A int8 [r][d], pred_B int8 [F_r][r], rank-local rows) into
+ * hbm_region, packs the rank's F_r neurons in all three tiers, places them in the HBM pools
+ * (resident) or in host_region (LRU/ATU: pinned host tier, "loaded in lower precision
+ * from DRAM"; R10), and initialises the cache metadata (identity / cold).  Synchronous: the
+ * master weights may be freed when it returns.  Errors: M2C_ERR_CAPACITY if an LRU pool is
+ * smaller than the decode plan's k_t or larger than 8192 slots. */
+m2c_status m2c_load_layer(m2c_ctx *ctx, int32_t layer, const void *w_gate, const void *w_up,
+                          const void *w_down_t, const int8_t *pred_A, const int8_t *pred_B,
+                          const m2c_cache_cfg *cfg, void *hbm_region, void *host_region);
+
+/* ---- a1-a3: predictor, top-k, tier split (P:70, P:73 step 1; R2, R3) ---------
+ * x: fp16 [d] device.  Outputs (device, any may be NULL except tier_ids):
+ *   rank_list int32 [k]   : active ids in rank order (score desc, id asc)
+ *   tier_of   int8  [F_r] : -1 inactive, 0 FP16, 1 INT8, 2 INT4
+ *   tier_ids  int32 [k]   : three segments [k16 | k8 | k4], ids ascending in each
+ *   scores    int32 [F_r] : predictor scores s = B hq
+ * Plan must satisfy k16 + k8 + k4 == k <= F_r (else M2C_ERR_CONFIG, host-checked). */
+m2c_status m2c_predict_rank(m2c_ctx *ctx, int32_t layer, const void *x,
+                            const m2c_tier_plan *plan, int32_t *rank_list, int8_t *tier_of,
+                            int32_t *tier_ids, int32_t *scores);
+
+/* ---- a4-a5: cache lookup + asynchronous miss fill (R7, R9) ---
+ * Looks the plan's tier segments of tier_ids up in the layer's per-tier pools at timestamp
+ * `step` (must strictly increase per layer, else M2C_ERR_STATE).  Outputs (device):
+ *   slots      int32 [k]          : pool slot of tier_ids[i]
+ *   hit_bitmap uint32 [ceil(k/32)]: bit i set iff tier_ids[i] hit
+ *   miss_log   int32 [k][2] or NULL: (id, slot) of misses; tier t's misses start at the
+ *                                    segment offset of t (0, k16, k16+k8)
+ *   evict_log  int32 [k][2] or NULL: (evicted id, slot), same offsets
+ *   counts     int32 [6]  or NULL : misses per tier (3), evictions per tier (3)
+ * The lookup runs on the compute stream; the fills run on the copy stream and `fill_done`
+ * (caller-created event, may be NULL) is recorded there.  Resident mode: identity slots,
+ * every bit set, no fills. */
+m2c_status m2c_cache_lookup_fill(m2c_ctx *ctx, int32_t layer, int64_t step,
+                                 const int32_t *tier_ids, const m2c_tier_plan *plan,
+                                 int32_t *slots, uint32_t *hit_bitmap, int32_t *miss_log,
+                                 int32_t *evict_log, int32_t *counts, m2c_event_t fill_done);
+
+/* ---- a6-a7: fused dequant-GEMV + SiLU.mul + sparse down-projection --
+ * Computes, for the plan's active neurons, y = sum_n act(g_n) u_n W_down[:, n] reading the
+ * records in place in the cache pools ("directly used for inference computation").
+ * slots: from m2c_cache_lookup_fill, or NULL in resident mode (slot = id).  hit_bitmap: NULL
+ * = everything resident; else hits are computed first, then the compute stream waits on
+ * fill_done (if non-NULL) and the misses are computed (R11).  Outputs (device, either may be
+ * NULL): y_partial fp32 [d] = this rank's sum before any all-reduce; y fp16 [d] = the
+ * all-reduced (if the context has a communicator with >1 rank) sum rounded to fp16. */
+m2c_status m2c_sparse_ffn_forward(m2c_ctx *ctx, int32_t layer, const void *x,
+                                  const int32_t *tier_ids, const int32_t *slots,
+                                  const uint32_t *hit_bitmap, const m2c_tier_plan *plan,
+                                  m2c_event_t fill_done, float *y_partial, void *y);
+
+/* ---- multi-GPU (d_ff sharding, R13) ----------------------------------------------------
+ * nccl_unique_id: 128 bytes from m2c_nccl_unique_id on rank 0, broadcast by the caller (the
+ * torch process group is used for bootstrap only).  nccl_lib: path of libnccl.so.2 (dlopen'd;
+ * NULL = default search).  Afterwards every layer all-reduces the fp32 partial sums once. */
+m2c_status m2c_nccl_unique_id(const char *nccl_lib, void *id_out_128);
+m2c_status m2c_comm_init(m2c_ctx *ctx, int32_t nranks, int32_t rank, const void *nccl_unique_id,
+                         const char *nccl_lib);
+
+/* ---- whole token (all layers), CUDA-graph captured ------------------------------------
+ * x_inout: fp16 [d] device; on return (asynchronously) holds x_L where
+ * x_{l+1} = fp16(x_l + fp16(y_l)) (R14).  step: strictly increasing (LRU timestamps). */
+m2c_status m2c_decode_step(m2c_ctx *ctx, void *x_inout, int64_t step);
+
+/* Disables (0) or enables (1, default) CUDA-graph capture of m2c_decode_step. */
+m2c_status m2c_set_graph(m2c_ctx *ctx, int32_t enable);
+
+/* Phase timing (CUDA events recorded inside the decode graph, on the compute stream):
+ * m2c_profile(ctx, 1) instruments every layer of m2c_decode_step with 5 timing events
+ * (before predict | after predict | after select | after cache+FFN | after reduce); the graph
+ * is re-captured.  m2c_profile_read synchronises the compute stream and writes, for the last
+ * decode step, ms[l*4 + {0,1,2,3}] = predictor, select, cache lookup + FFN (all launches),
+ * reduce/all-reduce/residual of layer l.  ffn_launches_out = FFN kernel launches per layer. */
+m2c_status m2c_profile(m2c_ctx *ctx, int32_t enable);
+m2c_status m2c_profile_read(m2c_ctx *ctx, float *ms, int32_t *ffn_launches_out);
+
+/* Kernels launched by the last m2c_decode_step (per token), and cumulative cache counters
+ * (hits, misses per tier) since the last reset (device counters; synchronises). */
+m2c_status m2c_stats(m2c_ctx *ctx, int64_t *kernels_per_token, int64_t hits[3], int64_t misses[3],
+                     int32_t reset);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* M2C_H */

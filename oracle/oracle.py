@@ -207,6 +207,20 @@ def layer_records(w, tiers=(16, 8, 4)):
     return {b: pack(b, w["w_gate"], w["w_up"], w["w_down_t"]) for b in tiers}
 
 
+def records_for(w, tier_ids, plan):
+    """Oracle-packed records of only the neurons ``tier_ids`` selects, each in its own tier
+    (rows of other neurons are left zero): the O0 pack applied lazily, for large layers."""
+    F, d = w["w_gate"].shape
+    seg = [0, int(plan[1]), int(plan[1]) + int(plan[2]), int(plan[0])]
+    out = {}
+    for t, b in enumerate((16, 8, 4)):
+        rec = np.zeros((F, record_bytes(b, d)), np.uint8)
+        for n in np.asarray(tier_ids)[seg[t]:seg[t + 1]]:
+            rec[n] = pack(b, w["w_gate"], w["w_up"], w["w_down_t"], int(n), int(n) + 1)[0]
+        out[b] = rec
+    return out
+
+
 def layer_forward(w, recs, x, plan, act=0):
     """One (token, layer) of the method, O1..O6: returns every intermediate."""
     pr = predict(x, w["pred_A"], w["pred_B"])

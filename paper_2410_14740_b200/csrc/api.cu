@@ -1,0 +1,701 @@
+// api.cu -- the C ABI of libm2c (include/m2c.h): validation, memory layout, stream/event
+// orchestration, CUDA-graph capture of the decode step, NCCL (dlopen) for d_ff sharding.
+#include <dlfcn.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "m2c_internal.cuh"
+
+namespace m2c {
+
+static thread_local std::string g_err;
+
+void set_error(const std::string &msg) { g_err = msg; }
+m2c_status fail(m2c_status st, const std::string &msg) {
+    g_err = msg;
+    return st;
+}
+m2c_status cuda_fail(cudaError_t e, const char *what) {
+    g_err = std::string(what) + ": " + cudaGetErrorString(e);
+    return M2C_ERR_CUDA;
+}
+
+size_t select_smem_bytes(int F_r, int P2);
+size_t select_smem_limit();
+size_t lru_smem_bytes(int P2, int maxcnt);
+int ffn_nch(int d);
+
+// ---- NCCL, loaded at run time (no link-time dependency) ----
+typedef int ncclResult_t;
+typedef void *ncclComm_t;
+typedef struct {
+    char internal[128];
+} ncclUniqueId;
+struct NcclApi {
+    void *h = nullptr;
+    ncclResult_t (*getUniqueId)(ncclUniqueId *) = nullptr;
+    ncclResult_t (*commInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*allReduce)(const void *, void *, size_t, int, int, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+    const char *(*errStr)(ncclResult_t) = nullptr;
+};
+
+static NcclApi *load_nccl(const char *path) {
+    static NcclApi api;
+    if (api.h) return &api;
+    const char *cands[] = {path, "libnccl.so.2", "libnccl.so"};
+    for (const char *p : cands) {
+        if (!p) continue;
+        api.h = dlopen(p, RTLD_NOW | RTLD_GLOBAL);
+        if (api.h) break;
+    }
+    if (!api.h) return nullptr;
+    api.getUniqueId = (decltype(api.getUniqueId))dlsym(api.h, "ncclGetUniqueId");
+    api.commInitRank = (decltype(api.commInitRank))dlsym(api.h, "ncclCommInitRank");
+    api.allReduce = (decltype(api.allReduce))dlsym(api.h, "ncclAllReduce");
+    api.commDestroy = (decltype(api.commDestroy))dlsym(api.h, "ncclCommDestroy");
+    api.errStr = (decltype(api.errStr))dlsym(api.h, "ncclGetErrorString");
+    if (!api.getUniqueId || !api.commInitRank || !api.allReduce || !api.commDestroy) {
+        dlclose(api.h);
+        api.h = nullptr;
+        return nullptr;
+    }
+    return &api;
+}
+
+// ---- per-layer memory layout (hbm_region / host_region) ----
+struct Layout {
+    size_t A = 0, B = 0, pool[3] = {0, 0, 0}, occ[3] = {0, 0, 0}, last[3] = {0, 0, 0},
+           slot_of[3] = {0, 0, 0}, hbm = 0;
+    size_t host_rec[3] = {0, 0, 0}, host = 0;
+};
+static size_t a256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+static Layout layout_of(const m2c_model_desc &d, const m2c_cache_cfg &cfg) {
+    Layout L;
+    const int64_t F_r = d.d_ff / d.shard_count;
+    const int bits[3] = {16, 8, 4};
+    size_t off = 0;
+    L.A = off;
+    off += a256((size_t)d.pred_rank * d.d_model);
+    L.B = off;
+    off += a256((size_t)F_r * d.pred_rank);
+    for (int t = 0; t < 3; t++) {
+        const int64_t cap = cfg.mode == 0 ? F_r : cfg.cap_slots[t];
+        L.pool[t] = off;
+        off += a256((size_t)cap * m2c_record_bytes(bits[t], d.d_model));
+    }
+    if (cfg.mode != 0) {
+        for (int t = 0; t < 3; t++) {
+            L.occ[t] = off;
+            off += a256(4 * (size_t)cfg.cap_slots[t]);
+            L.last[t] = off;
+            off += a256(4 * (size_t)cfg.cap_slots[t]);
+            L.slot_of[t] = off;
+            off += a256(4 * (size_t)F_r);
+        }
+        size_t h = 0;
+        for (int t = 0; t < 3; t++) {
+            L.host_rec[t] = h;
+            h += a256((size_t)F_r * m2c_record_bytes(bits[t], d.d_model));
+        }
+        L.host = h;
+    }
+    L.hbm = off;
+    return L;
+}
+
+static m2c_status check_desc(const m2c_model_desc *d) {
+    if (!d) return fail(M2C_ERR_INVALID_ARG, "null model desc");
+    if (d->d_model <= 0 || d->d_model % 256 || d->d_model > 8192)
+        return fail(M2C_ERR_CONFIG, "d_model must be a positive multiple of 256, <= 8192");
+    if (d->group != 128) return fail(M2C_ERR_CONFIG, "group must be 128 (R4)");
+    if (d->pred_rank < 16 || d->pred_rank % 16 || d->pred_rank > 512 ||
+        ((d->pred_rank / 16) & (d->pred_rank / 16 - 1)))
+        return fail(M2C_ERR_CONFIG, "pred_rank must be 16 * 2^j <= 512");
+    if (d->shard_count < 1 || d->shard_index < 0 || d->shard_index >= d->shard_count ||
+        d->d_ff <= 0 || d->d_ff % d->shard_count)
+        return fail(M2C_ERR_CONFIG, "bad d_ff / shard");
+    if (d->d_ff / d->shard_count > (1 << 20)) return fail(M2C_ERR_CONFIG, "F_r too large");
+    if (d->n_layers < 1) return fail(M2C_ERR_CONFIG, "n_layers < 1");
+    if (d->act != 0 && d->act != 1) return fail(M2C_ERR_CONFIG, "act must be 0 (SiLU) or 1 (ReLU)");
+    return M2C_OK;
+}
+
+static m2c_status check_plan(const m2c_tier_plan *p, int F_r) {
+    if (!p) return fail(M2C_ERR_INVALID_ARG, "null plan");
+    if (p->k < 0 || p->k > F_r || p->k_fp16 < 0 || p->k_int8 < 0 || p->k_int4 < 0 ||
+        (int64_t)p->k_fp16 + p->k_int8 + p->k_int4 != p->k)
+        return fail(M2C_ERR_CONFIG, "tier plan: need k16 + k8 + k4 == k <= F_r");
+    return M2C_OK;
+}
+
+static bool al16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+static int32_t *step_ptr(m2c_ctx *c) { return c->ws.counts + 15; }
+
+// ---- the token: all layers on the compute stream (+ copy stream for LRU fills) ----
+static cudaError_t mark(m2c_ctx *c, int l, int i) {
+    if (c->prof_ev.empty()) return cudaSuccess;
+    return cudaEventRecordWithFlags(c->prof_ev[5 * l + i], c->compute, cudaEventRecordExternal);
+}
+
+static cudaError_t enqueue_layer(m2c_ctx *c, int l, __half *x) {
+    LayerState &L = c->layers[l];
+    const m2c_tier_plan &p = c->plan;
+    cudaStream_t st = c->compute;
+    cudaError_t e;
+    if ((e = mark(c, l, 0))) return e;
+    if ((e = launch_predict(c, L, x, c->ws.s, st))) return e;
+    if ((e = mark(c, l, 1))) return e;
+    if ((e = launch_select(c, c->ws.s, p, nullptr, nullptr, c->ws.tier_ids, st))) return e;
+    if ((e = mark(c, l, 2))) return e;
+    int np = c->G;
+    if (L.mode == 0) {
+        e = launch_ffn(c, L, x, c->ws.tier_ids, c->ws.counts, p, c->ws.partial, st);
+        if (e) return e;
+    } else {
+        e = launch_lru(c, L, step_ptr(c), c->ws.tier_ids, p, c->ws.slots, c->ws.hit_bits, nullptr, nullptr, st);
+        if (e) return e;
+        if ((e = cudaEventRecord(c->ev_lookup, st))) return e;
+        if ((e = cudaStreamWaitEvent(c->copy, c->ev_lookup, 0))) return e;
+        if ((e = launch_fill(c, L, p, c->copy))) return e;
+        if ((e = cudaEventRecord(c->ev_fill, c->copy))) return e;
+        e = launch_ffn(c, L, x, c->ws.hit_items, c->ws.counts + 4, p, c->ws.partial, st);
+        if (e) return e;
+        if ((e = cudaStreamWaitEvent(st, c->ev_fill, 0))) return e;
+        e = launch_ffn(c, L, x, c->ws.miss_items, c->ws.counts + 8, p,
+                       c->ws.partial + (size_t)c->G * c->desc.d_model, st);
+        if (e) return e;
+        np = 2 * c->G;
+    }
+    if ((e = mark(c, l, 3))) return e;
+    if (c->nranks > 1) {
+        if ((e = launch_reduce(c, np, c->ws.partial, x, c->ws.y32, nullptr, nullptr, st))) return e;
+        int r = c->nccl->allReduce(c->ws.y32, c->ws.y32, (size_t)c->desc.d_model, 7 /*f32*/,
+                                   0 /*sum*/, c->comm, st);
+        if (r != 0) return cudaErrorUnknown;
+        if ((e = launch_finalize(c, c->ws.y32, x, nullptr, x, st))) return e;
+    } else {
+        if ((e = launch_reduce(c, np, c->ws.partial, x, nullptr, nullptr, x, st))) return e;
+    }
+    return mark(c, l, 4);
+}
+
+static cudaError_t enqueue_token(m2c_ctx *c, __half *x) {
+    const m2c_tier_plan &p = c->plan;
+    cudaError_t e = launch_set_counts(c->ws.counts, p.k_fp16, p.k_int8, p.k_int4, c->compute);
+    c->launch_counter++;
+    if (e) return e;
+    for (int l = 0; l < c->desc.n_layers; l++)
+        if ((e = enqueue_layer(c, l, x))) return e;
+    return cudaSuccess;
+}
+
+}  // namespace m2c
+
+using namespace m2c;
+
+extern "C" {
+
+const char *m2c_last_error(void) { return g_err.c_str(); }
+int32_t m2c_abi_version(void) { return M2C_ABI_VERSION; }
+
+int64_t m2c_record_bytes(int32_t bits, int32_t d) {
+    if (d <= 0 || d % 128) return -1;
+    const int64_t G = d / 128;
+    int64_t raw;
+    if (bits == 16) raw = 6LL * d;
+    else if (bits == 8) raw = 3LL * d + 9 * G;
+    else if (bits == 4) raw = 3LL * d / 2 + 9 * G;
+    else return -1;
+    return (raw + 15) / 16 * 16;
+}
+
+m2c_status m2c_tier_plan_make(int32_t F_r, int32_t pct, int32_t a16, int32_t a8, int32_t den,
+                              m2c_tier_plan *out) {
+    if (!out || F_r < 0 || pct < 0 || pct > 100 || den <= 0 || a16 < 0 || a8 < 0 || a16 + a8 > den)
+        return fail(M2C_ERR_INVALID_ARG, "tier_plan_make: bad arguments");
+    const int64_t k = (int64_t)F_r * pct / 100;
+    const int64_t k16 = k * a16 / den, k8 = k * a8 / den;
+    out->k = (int32_t)k;
+    out->k_fp16 = (int32_t)k16;
+    out->k_int8 = (int32_t)k8;
+    out->k_int4 = (int32_t)(k - k16 - k8);
+    return M2C_OK;
+}
+
+m2c_status m2c_cache_cfg_capped(const m2c_model_desc *desc, const m2c_tier_plan *plan,
+                                int32_t num, int32_t den, int32_t mode, m2c_cache_cfg *out) {
+    m2c_status st = check_desc(desc);
+    if (st) return st;
+    const int F_r = desc->d_ff / desc->shard_count;
+    if ((st = check_plan(plan, F_r))) return st;
+    if (!out || num <= 0 || den <= 0 || (mode != 1 && mode != 2))
+        return fail(M2C_ERR_INVALID_ARG, "cache_cfg_capped: bad arguments");
+    const int kt[3] = {plan->k_fp16, plan->k_int8, plan->k_int4};
+    const int bits[3] = {16, 8, 4};
+    out->mode = mode;
+    if (mode == 2) {  // ATU: exactly the active set
+        for (int t = 0; t < 3; t++) out->cap_slots[t] = kt[t];
+        return M2C_OK;
+    }
+    double act_bytes = 0;
+    for (int t = 0; t < 3; t++) act_bytes += (double)kt[t] * m2c_record_bytes(bits[t], desc->d_model);
+    const double budget = (double)num / den * 6.0 * desc->d_model * F_r;
+    const double M = act_bytes > 0 ? budget / act_bytes : 0;
+    for (int t = 0; t < 3; t++) {
+        double c = std::floor(M * kt[t]);
+        if (c > F_r) c = F_r;
+        out->cap_slots[t] = (int32_t)c;
+    }
+    return M2C_OK;
+}
+
+m2c_status m2c_layer_footprint(const m2c_model_desc *desc, const m2c_cache_cfg *cfg,
+                               size_t *hbm, size_t *host) {
+    m2c_status st = check_desc(desc);
+    if (st) return st;
+    if (!cfg || cfg->mode < 0 || cfg->mode > 2) return fail(M2C_ERR_INVALID_ARG, "bad cache cfg");
+    const Layout L = layout_of(*desc, *cfg);
+    if (hbm) *hbm = L.hbm;
+    if (host) *host = L.host;
+    return M2C_OK;
+}
+
+m2c_status m2c_create(const m2c_model_desc *desc, int32_t device, m2c_stream_t compute,
+                      m2c_stream_t copy, const m2c_tier_plan *plan, m2c_ctx **out) {
+    m2c_status st = check_desc(desc);
+    if (st) return st;
+    const int F_r = desc->d_ff / desc->shard_count;
+    if ((st = check_plan(plan, F_r))) return st;
+    if (!out) return fail(M2C_ERR_INVALID_ARG, "null out");
+    int ndev = 0;
+    M2C_CUDA(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return fail(M2C_ERR_INVALID_ARG, "bad device");
+    M2C_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    M2C_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) return fail(M2C_ERR_CONFIG, "libm2c is built for sm_100a (B200) only");
+    m2c_ctx *c = new m2c_ctx();
+    c->desc = *desc;
+    c->F_r = F_r;
+    c->device = device;
+    c->num_sms = prop.multiProcessorCount;
+    c->G = prop.multiProcessorCount;
+    c->compute = reinterpret_cast<cudaStream_t>(compute);
+    c->copy = reinterpret_cast<cudaStream_t>(copy);
+    c->plan = *plan;
+    const int bits[3] = {16, 8, 4};
+    for (int t = 0; t < 3; t++) c->nb[t] = m2c_record_bytes(bits[t], desc->d_model);
+    c->layers.resize(desc->n_layers);
+    // workspace
+    const int d = desc->d_model, r = desc->pred_rank;
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        size_t o = off;
+        off += a256(bytes);
+        return o;
+    };
+    const size_t o_h = take(4 * (size_t)r), o_s = take(4 * (size_t)F_r),
+                 o_ids = take(4 * (size_t)F_r), o_tof = take((size_t)F_r),
+                 o_slots = take(4 * (size_t)F_r), o_bits = take(4 * ((size_t)F_r / 32 + 2)),
+                 o_hit = take(4 * (size_t)F_r), o_miss = take(4 * (size_t)F_r),
+                 o_mid = take(4 * (size_t)F_r), o_cnt = take(4 * 16),
+                 o_part = take(4 * (size_t)2 * c->G * d), o_y = take(4 * (size_t)d),
+                 o_x = take(2 * (size_t)d), o_stats = take(8 * 6), o_err = take(4);
+    cudaError_t e = cudaMalloc(&c->ws_mem, off);
+    if (e != cudaSuccess) {
+        delete c;
+        return cuda_fail(e, "cudaMalloc(workspace)");
+    }
+    c->ws_bytes = off;
+    uint8_t *b = static_cast<uint8_t *>(c->ws_mem);
+    c->ws.h = (int32_t *)(b + o_h);
+    c->ws.s = (int32_t *)(b + o_s);
+    c->ws.tier_ids = (int32_t *)(b + o_ids);
+    c->ws.tier_of = (int8_t *)(b + o_tof);
+    c->ws.slots = (int32_t *)(b + o_slots);
+    c->ws.hit_bits = (uint32_t *)(b + o_bits);
+    c->ws.hit_items = (int32_t *)(b + o_hit);
+    c->ws.miss_items = (int32_t *)(b + o_miss);
+    c->ws.miss_ids = (int32_t *)(b + o_mid);
+    c->ws.counts = (int32_t *)(b + o_cnt);
+    c->ws.partial = (float *)(b + o_part);
+    c->ws.y32 = (float *)(b + o_y);
+    c->ws.xbuf = (__half *)(b + o_x);
+    c->ws.stats = (unsigned long long *)(b + o_stats);
+    c->ws.err = (uint32_t *)(b + o_err);
+    e = cudaMemset(c->ws_mem, 0, off);
+    static bool attrs_done = false;
+    if (e == cudaSuccess && !attrs_done) {
+        e = init_select_attrs();
+        if (e == cudaSuccess) e = init_cache_attrs();
+        if (e == cudaSuccess) e = init_ffn_attrs();
+        attrs_done = e == cudaSuccess;
+    }
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_lookup, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_fill, cudaEventDisableTiming);
+    if (e != cudaSuccess) {
+        m2c_destroy(c);
+        return cuda_fail(e, "m2c_create");
+    }
+    *out = c;
+    return M2C_OK;
+}
+
+m2c_status m2c_destroy(m2c_ctx *c) {
+    if (!c) return M2C_OK;
+    if (c->graph) cudaGraphExecDestroy(c->graph);
+    for (cudaEvent_t e : c->prof_ev) cudaEventDestroy(e);
+    if (c->comm && c->nccl) c->nccl->commDestroy(c->comm);
+    if (c->ev_lookup) cudaEventDestroy(c->ev_lookup);
+    if (c->ev_fill) cudaEventDestroy(c->ev_fill);
+    if (c->ws_mem) cudaFree(c->ws_mem);
+    delete c;
+    return M2C_OK;
+}
+
+m2c_status m2c_quant_pack(int32_t d, int32_t bits, const void *g, const void *u, const void *dn,
+                          int64_t n0, int64_t n1, void *out, m2c_stream_t stream) {
+    if (d <= 0 || d % 128) return fail(M2C_ERR_INVALID_ARG, "quant_pack: d % 128 != 0");
+    if (bits != 16 && bits != 8 && bits != 4) return fail(M2C_ERR_INVALID_ARG, "quant_pack: bits");
+    if (!g || !u || !dn || !out || n0 < 0 || n1 < n0)
+        return fail(M2C_ERR_INVALID_ARG, "quant_pack: null pointer or bad range");
+    if (!al16(g) || !al16(u) || !al16(dn) || !al16(out))
+        return fail(M2C_ERR_INVALID_ARG, "quant_pack: pointers must be 16-B aligned");
+    M2C_CUDA(launch_pack(d, bits, (const __half *)g, (const __half *)u, (const __half *)dn, n0, n1,
+                         (uint8_t *)out, reinterpret_cast<cudaStream_t>(stream)));
+    return M2C_OK;
+}
+
+m2c_status m2c_load_layer(m2c_ctx *c, int32_t layer, const void *g, const void *u, const void *dn,
+                          const int8_t *A, const int8_t *B, const m2c_cache_cfg *cfg,
+                          void *hbm_region, void *host_region) {
+    if (!c || !cfg || !g || !u || !dn || !A || !B || !hbm_region)
+        return fail(M2C_ERR_INVALID_ARG, "load_layer: null argument");
+    if (layer < 0 || layer >= c->desc.n_layers) return fail(M2C_ERR_INVALID_ARG, "bad layer");
+    if (cfg->mode < 0 || cfg->mode > 2) return fail(M2C_ERR_INVALID_ARG, "bad cache mode");
+    if ((reinterpret_cast<uintptr_t>(hbm_region) & 255) ||
+        (host_region && (reinterpret_cast<uintptr_t>(host_region) & 255)))
+        return fail(M2C_ERR_INVALID_ARG, "regions must be 256-B aligned");
+    if (!al16(g) || !al16(u) || !al16(dn)) return fail(M2C_ERR_INVALID_ARG, "masters not 16-B aligned");
+    const int kt[3] = {c->plan.k_fp16, c->plan.k_int8, c->plan.k_int4};
+    if (cfg->mode != 0) {
+        if (!host_region) return fail(M2C_ERR_INVALID_ARG, "LRU/ATU needs a pinned host region");
+        for (int t = 0; t < 3; t++)
+            if (cfg->cap_slots[t] < kt[t] || cfg->cap_slots[t] > kMaxPoolSlots ||
+                cfg->cap_slots[t] > c->F_r)
+                return fail(M2C_ERR_CAPACITY, "pool capacity must be in [k_t, min(F_r, 8192)]");
+    }
+    const Layout Lo = layout_of(c->desc, *cfg);
+    cudaStream_t st = c->compute;
+    const int d = c->desc.d_model, r = c->desc.pred_rank, F_r = c->F_r;
+    uint8_t *hb = static_cast<uint8_t *>(hbm_region);
+    uint8_t *hh = static_cast<uint8_t *>(host_region);
+    LayerState &L = c->layers[layer];
+    L = LayerState();
+    L.mode = cfg->mode;
+    L.A = (const int8_t *)(hb + Lo.A);
+    L.B = (const int8_t *)(hb + Lo.B);
+    M2C_CUDA(cudaMemcpyAsync(hb + Lo.A, A, (size_t)r * d, cudaMemcpyDefault, st));
+    M2C_CUDA(cudaMemcpyAsync(hb + Lo.B, B, (size_t)F_r * r, cudaMemcpyDefault, st));
+    const int bits[3] = {16, 8, 4};
+    const __half *G = (const __half *)g, *U = (const __half *)u, *D = (const __half *)dn;
+    for (int t = 0; t < 3; t++) {
+        L.pool[t] = hb + Lo.pool[t];
+        L.cap[t] = cfg->mode == 0 ? F_r : cfg->cap_slots[t];
+        if (cfg->mode == 0) {
+            M2C_CUDA(launch_pack(d, bits[t], G, U, D, 0, F_r, L.pool[t], st));
+        } else {
+            // pack chunk-wise into the (cold) pool memory as scratch, then copy to the host tier
+            uint8_t *dst = hh + Lo.host_rec[t];
+            const int64_t chunk = L.cap[t];
+            for (int64_t n0 = 0; n0 < F_r; n0 += chunk) {
+                const int64_t n1 = n0 + chunk < F_r ? n0 + chunk : F_r;
+                M2C_CUDA(launch_pack(d, bits[t], G, U, D, n0, n1, L.pool[t], st));
+                M2C_CUDA(cudaMemcpyAsync(dst + n0 * c->nb[t], L.pool[t], (n1 - n0) * c->nb[t],
+                                         cudaMemcpyDefault, st));
+            }
+            L.host_rec[t] = dst;
+            L.occupant[t] = (int32_t *)(hb + Lo.occ[t]);
+            L.last[t] = (int32_t *)(hb + Lo.last[t]);
+            L.slot_of[t] = (int32_t *)(hb + Lo.slot_of[t]);
+            M2C_CUDA(launch_fill_i32(L.occupant[t], -1, L.cap[t], st));
+            M2C_CUDA(launch_fill_i32(L.last[t], -1, L.cap[t], st));
+            M2C_CUDA(launch_fill_i32(L.slot_of[t], -1, F_r, st));
+        }
+    }
+    M2C_CUDA(cudaStreamSynchronize(st));
+    L.loaded = true;
+    if (c->graph) {  // topology may have changed
+        cudaGraphExecDestroy(c->graph);
+        c->graph = nullptr;
+    }
+    return M2C_OK;
+}
+
+m2c_status m2c_predict_rank(m2c_ctx *c, int32_t layer, const void *x, const m2c_tier_plan *plan,
+                            int32_t *rank_list, int8_t *tier_of, int32_t *tier_ids,
+                            int32_t *scores) {
+    if (!c || !x || !plan || (!tier_ids && plan->k > 0))
+        return fail(M2C_ERR_INVALID_ARG, "predict_rank: null argument");
+    if (layer < 0 || layer >= c->desc.n_layers || !c->layers[layer].loaded)
+        return fail(M2C_ERR_STATE, "predict_rank: layer not loaded");
+    m2c_status st = check_plan(plan, c->F_r);
+    if (st) return st;
+    if (!al16(x)) return fail(M2C_ERR_INVALID_ARG, "x must be 16-B aligned");
+    if (rank_list && plan->k > 0) {
+        int P2 = 2;
+        while (P2 < plan->k) P2 <<= 1;
+        if (select_smem_bytes(c->F_r, P2) > select_smem_limit())
+            return fail(M2C_ERR_CAPACITY, "rank_list: k too large for the on-chip sort");
+    } else if (select_smem_bytes(c->F_r, 0) > select_smem_limit()) {
+        return fail(M2C_ERR_CAPACITY, "F_r too large for the single-CTA select");
+    }
+    int32_t *s = scores ? scores : c->ws.s;
+    M2C_CUDA(launch_predict(c, c->layers[layer], (const __half *)x, s, c->compute));
+    M2C_CUDA(launch_select(c, s, *plan, rank_list, tier_of, tier_ids, c->compute));
+    return M2C_OK;
+}
+
+m2c_status m2c_cache_lookup_fill(m2c_ctx *c, int32_t layer, int64_t step, const int32_t *tier_ids,
+                                 const m2c_tier_plan *plan, int32_t *slots, uint32_t *hit_bitmap,
+                                 int32_t *miss_log, int32_t *evict_log, int32_t *counts,
+                                 m2c_event_t fill_done) {
+    if (!c || !plan || !hit_bitmap || ((!tier_ids || !slots) && plan->k > 0))
+        return fail(M2C_ERR_INVALID_ARG, "cache_lookup_fill: null argument");
+    if (layer < 0 || layer >= c->desc.n_layers || !c->layers[layer].loaded)
+        return fail(M2C_ERR_STATE, "cache_lookup_fill: layer not loaded");
+    m2c_status st = check_plan(plan, c->F_r);
+    if (st) return st;
+    LayerState &L = c->layers[layer];
+    if (step <= L.last_step || step > INT32_MAX - 2 || step < 0)
+        return fail(M2C_ERR_STATE, "cache_lookup_fill: step must strictly increase (0..2^31-3)");
+    cudaStream_t cs = c->compute;
+    const size_t nbits = sizeof(uint32_t) * ((plan->k + 31) / 32 + 1);
+    if (L.mode == 0) {  // resident: identity, all hits
+        M2C_CUDA(cudaMemcpyAsync(slots, tier_ids, 4 * (size_t)plan->k, cudaMemcpyDeviceToDevice, cs));
+        M2C_CUDA(cudaMemsetAsync(hit_bitmap, 0, nbits, cs));
+        if (plan->k) M2C_CUDA(cudaMemsetAsync(hit_bitmap, 0xff, 4 * (size_t)(plan->k / 32), cs));
+        if (plan->k % 32) {
+            const uint32_t tail = (1u << (plan->k % 32)) - 1;
+            M2C_CUDA(cudaMemcpyAsync(hit_bitmap + plan->k / 32, &tail, 4, cudaMemcpyHostToDevice, cs));
+        }
+        if (counts) M2C_CUDA(cudaMemsetAsync(counts, 0, 6 * sizeof(int32_t), cs));
+        M2C_CUDA(launch_set_counts(c->ws.counts + 4, plan->k_fp16, plan->k_int8, plan->k_int4, cs));
+        M2C_CUDA(launch_set_counts(c->ws.counts + 8, 0, 0, 0, cs));
+        M2C_CUDA(cudaMemcpyAsync(c->ws.hit_items, tier_ids, 4 * (size_t)plan->k, cudaMemcpyDeviceToDevice, cs));
+        if (fill_done) M2C_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(fill_done), cs));
+    } else {
+        for (int t = 0; t < 3; t++) {
+            const int kt = t == 0 ? plan->k_fp16 : (t == 1 ? plan->k_int8 : plan->k_int4);
+            if (kt > L.cap[t]) return fail(M2C_ERR_CAPACITY, "k_t exceeds the pool capacity");
+        }
+        const int32_t st32 = (int32_t)step;
+        M2C_CUDA(cudaMemcpyAsync(step_ptr(c), &st32, 4, cudaMemcpyHostToDevice, cs));
+        M2C_CUDA(launch_lru(c, L, step_ptr(c), tier_ids, *plan, slots, hit_bitmap, miss_log, evict_log, cs));
+        if (counts) {
+            M2C_CUDA(cudaMemcpyAsync(counts, c->ws.counts + 8, 12, cudaMemcpyDeviceToDevice, cs));
+            M2C_CUDA(cudaMemcpyAsync(counts + 3, c->ws.counts + 12, 12, cudaMemcpyDeviceToDevice, cs));
+        }
+        M2C_CUDA(cudaEventRecord(c->ev_lookup, cs));
+        M2C_CUDA(cudaStreamWaitEvent(c->copy, c->ev_lookup, 0));
+        M2C_CUDA(launch_fill(c, L, *plan, c->copy));
+        if (fill_done) M2C_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(fill_done), c->copy));
+    }
+    L.last_step = step;
+    return M2C_OK;
+}
+
+m2c_status m2c_sparse_ffn_forward(m2c_ctx *c, int32_t layer, const void *x, const int32_t *tier_ids,
+                                  const int32_t *slots, const uint32_t *hit_bitmap,
+                                  const m2c_tier_plan *plan, m2c_event_t fill_done,
+                                  float *y_partial, void *y) {
+    if (!c || !x || !plan || (!tier_ids && plan->k > 0))
+        return fail(M2C_ERR_INVALID_ARG, "sparse_ffn_forward: null argument");
+    if (layer < 0 || layer >= c->desc.n_layers || !c->layers[layer].loaded)
+        return fail(M2C_ERR_STATE, "sparse_ffn_forward: layer not loaded");
+    m2c_status st = check_plan(plan, c->F_r);
+    if (st) return st;
+    if (!al16(x)) return fail(M2C_ERR_INVALID_ARG, "x must be 16-B aligned");
+    LayerState &L = c->layers[layer];
+    if (L.mode != 0 && !hit_bitmap)
+        return fail(M2C_ERR_STATE, "LRU/ATU layer: pass the lookup's slots and hit_bitmap");
+    cudaStream_t cs = c->compute;
+    const __half *xh = (const __half *)x;
+    const int d = c->desc.d_model;
+    int np = c->G;
+    M2C_CUDA(launch_set_counts(c->ws.counts, plan->k_fp16, plan->k_int8, plan->k_int4, cs));
+    if (!hit_bitmap) {
+        M2C_CUDA(launch_ffn(c, L, xh, slots ? slots : tier_ids, c->ws.counts, *plan, c->ws.partial, cs));
+    } else {
+        // hits first, then wait for the fills, then the misses (R11)
+        M2C_CUDA(launch_ffn(c, L, xh, c->ws.hit_items, c->ws.counts + 4, *plan, c->ws.partial, cs));
+        if (fill_done) M2C_CUDA(cudaStreamWaitEvent(cs, reinterpret_cast<cudaEvent_t>(fill_done), 0));
+        M2C_CUDA(launch_ffn(c, L, xh, c->ws.miss_items, c->ws.counts + 8, *plan,
+                            c->ws.partial + (size_t)c->G * d, cs));
+        np = 2 * c->G;
+    }
+    if (c->nranks > 1) {
+        M2C_CUDA(launch_reduce(c, np, c->ws.partial, xh, c->ws.y32, nullptr, nullptr, cs));
+        if (y_partial)
+            M2C_CUDA(cudaMemcpyAsync(y_partial, c->ws.y32, 4 * (size_t)d, cudaMemcpyDeviceToDevice, cs));
+        if (y) {
+            int r = c->nccl->allReduce(c->ws.y32, c->ws.y32, (size_t)d, 7, 0, c->comm, cs);
+            if (r) return fail(M2C_ERR_NCCL, c->nccl->errStr ? c->nccl->errStr(r) : "ncclAllReduce");
+            M2C_CUDA(launch_finalize(c, c->ws.y32, xh, (__half *)y, nullptr, cs));
+        }
+    } else {
+        M2C_CUDA(launch_reduce(c, np, c->ws.partial, xh, y_partial, (__half *)y, nullptr, cs));
+    }
+    return M2C_OK;
+}
+
+m2c_status m2c_nccl_unique_id(const char *lib, void *id_out) {
+    if (!id_out) return fail(M2C_ERR_INVALID_ARG, "null id");
+    NcclApi *api = load_nccl(lib);
+    if (!api) return fail(M2C_ERR_NCCL, "cannot dlopen libnccl.so.2");
+    ncclUniqueId id;
+    int r = api->getUniqueId(&id);
+    if (r) return fail(M2C_ERR_NCCL, api->errStr ? api->errStr(r) : "ncclGetUniqueId");
+    memcpy(id_out, &id, sizeof(id));
+    return M2C_OK;
+}
+
+m2c_status m2c_comm_init(m2c_ctx *c, int32_t nranks, int32_t rank, const void *uid, const char *lib) {
+    if (!c || !uid) return fail(M2C_ERR_INVALID_ARG, "comm_init: null argument");
+    if (nranks != c->desc.shard_count || rank != c->desc.shard_index)
+        return fail(M2C_ERR_CONFIG, "comm_init: nranks/rank must equal shard_count/shard_index");
+    if (nranks == 1) return M2C_OK;
+    NcclApi *api = load_nccl(lib);
+    if (!api) return fail(M2C_ERR_NCCL, "cannot dlopen libnccl.so.2");
+    ncclUniqueId id;
+    memcpy(&id, uid, sizeof(id));
+    M2C_CUDA(cudaSetDevice(c->device));
+    ncclComm_t comm = nullptr;
+    int r = api->commInitRank(&comm, nranks, id, rank);
+    if (r) return fail(M2C_ERR_NCCL, api->errStr ? api->errStr(r) : "ncclCommInitRank");
+    c->nccl = api;
+    c->comm = comm;
+    c->nranks = nranks;
+    c->rank = rank;
+    if (c->graph) {
+        cudaGraphExecDestroy(c->graph);
+        c->graph = nullptr;
+    }
+    return M2C_OK;
+}
+
+m2c_status m2c_set_graph(m2c_ctx *c, int32_t enable) {
+    if (!c) return fail(M2C_ERR_INVALID_ARG, "null ctx");
+    c->use_graph = enable != 0;
+    return M2C_OK;
+}
+
+m2c_status m2c_decode_step(m2c_ctx *c, void *x_inout, int64_t step) {
+    if (!c || !x_inout) return fail(M2C_ERR_INVALID_ARG, "decode_step: null argument");
+    if (!al16(x_inout)) return fail(M2C_ERR_INVALID_ARG, "x must be 16-B aligned");
+    bool any_lru = false;
+    for (int l = 0; l < c->desc.n_layers; l++) {
+        LayerState &L = c->layers[l];
+        if (!L.loaded) return fail(M2C_ERR_STATE, "decode_step: a layer is not loaded");
+        if (L.mode != 0) {
+            any_lru = true;
+            if (step <= L.last_step || step < 0 || step > INT32_MAX - 2)
+                return fail(M2C_ERR_STATE, "decode_step: step must strictly increase");
+        }
+    }
+    if (select_smem_bytes(c->F_r, 0) > select_smem_limit())
+        return fail(M2C_ERR_CAPACITY, "F_r too large for the single-CTA select");
+    cudaStream_t cs = c->compute;
+    if (any_lru) {
+        const int32_t st32 = (int32_t)step;  // pageable source: staged before return
+        M2C_CUDA(cudaMemcpyAsync(step_ptr(c), &st32, 4, cudaMemcpyHostToDevice, cs));
+    }
+    __half *x = static_cast<__half *>(x_inout);
+    if (c->use_graph) {
+        if (c->graph && c->graph_x != x_inout) {
+            cudaGraphExecDestroy(c->graph);
+            c->graph = nullptr;
+        }
+        if (!c->graph) {
+            const int64_t before = c->launch_counter;
+            cudaGraph_t g = nullptr;
+            M2C_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+            cudaError_t e = enqueue_token(c, x);
+            cudaError_t e2 = cudaStreamEndCapture(cs, &g);
+            if (e != cudaSuccess) {
+                if (g) cudaGraphDestroy(g);
+                return cuda_fail(e, "decode_step capture");
+            }
+            if (e2 != cudaSuccess) return cuda_fail(e2, "cudaStreamEndCapture");
+            e = cudaGraphInstantiate(&c->graph, g, 0);
+            cudaGraphDestroy(g);
+            if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate");
+            c->graph_x = x_inout;
+            c->kernels_per_token = c->launch_counter - before;
+        }
+        M2C_CUDA(cudaGraphLaunch(c->graph, cs));
+    } else {
+        const int64_t before = c->launch_counter;
+        M2C_CUDA(enqueue_token(c, x));
+        c->kernels_per_token = c->launch_counter - before;
+    }
+    for (int l = 0; l < c->desc.n_layers; l++)
+        if (c->layers[l].mode != 0) c->layers[l].last_step = step;
+    return M2C_OK;
+}
+
+m2c_status m2c_profile(m2c_ctx *c, int32_t enable) {
+    if (!c) return fail(M2C_ERR_INVALID_ARG, "null ctx");
+    M2C_CUDA(cudaStreamSynchronize(c->compute));
+    for (cudaEvent_t e : c->prof_ev) cudaEventDestroy(e);
+    c->prof_ev.clear();
+    if (enable) {
+        c->prof_ev.resize(5 * (size_t)c->desc.n_layers);
+        for (auto &e : c->prof_ev) M2C_CUDA(cudaEventCreate(&e));
+    }
+    if (c->graph) {
+        cudaGraphExecDestroy(c->graph);
+        c->graph = nullptr;
+    }
+    return M2C_OK;
+}
+
+m2c_status m2c_profile_read(m2c_ctx *c, float *ms, int32_t *ffn_launches) {
+    if (!c || !ms) return fail(M2C_ERR_INVALID_ARG, "null argument");
+    if (c->prof_ev.empty()) return fail(M2C_ERR_STATE, "profiling not enabled");
+    M2C_CUDA(cudaStreamSynchronize(c->compute));
+    for (int l = 0; l < c->desc.n_layers; l++)
+        for (int i = 0; i < 4; i++)
+            M2C_CUDA(cudaEventElapsedTime(&ms[4 * l + i], c->prof_ev[5 * l + i], c->prof_ev[5 * l + i + 1]));
+    if (ffn_launches) *ffn_launches = c->layers[0].mode == 0 ? 1 : 2;
+    return M2C_OK;
+}
+
+m2c_status m2c_stats(m2c_ctx *c, int64_t *kpt, int64_t hits[3], int64_t misses[3], int32_t reset) {
+    if (!c) return fail(M2C_ERR_INVALID_ARG, "null ctx");
+    if (kpt) *kpt = c->kernels_per_token;
+    unsigned long long h[6] = {0, 0, 0, 0, 0, 0};
+    M2C_CUDA(cudaStreamSynchronize(c->compute));
+    M2C_CUDA(cudaMemcpy(h, c->ws.stats, sizeof(h), cudaMemcpyDeviceToHost));
+    uint32_t err = 0;
+    M2C_CUDA(cudaMemcpy(&err, c->ws.err, 4, cudaMemcpyDeviceToHost));
+    for (int t = 0; t < 3; t++) {
+        if (hits) hits[t] = (int64_t)h[t];
+        if (misses) misses[t] = (int64_t)h[3 + t];
+    }
+    if (reset) M2C_CUDA(cudaMemset(c->ws.stats, 0, sizeof(h)));
+    if (err) {
+        cudaMemset(c->ws.err, 0, 4);
+        return fail(M2C_ERR_STATE, "device flagged a non-finite input x");
+    }
+    return M2C_OK;
+}
+
+}  // extern "C"

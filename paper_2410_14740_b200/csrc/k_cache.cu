@@ -1,0 +1,254 @@
+// k_cache.cu -- a4/a5: the per-(layer, tier) neuron cache in HBM and the miss fills.
+//
+// Paper: one isolated, contiguous cache unit per layer whose memory is used in place by the
+// computation; "a neuron-level mixed-precision LRU cache in HBM";
+// misses loaded "asynchronously from DRAM to HBM to overlap the HBM cache miss with the GPU
+// computation" on "dedicated CUDA streams".  The paper keeps the bookkeeping on
+// the host; we keep it on the device because host-driven cache management costs a
+// device->host round trip per layer ("GPU kernels are launched by CPUs").
+// Policy details (the paper is silent): DESIGN.md R7 -- step-granular timestamps, victims =
+// smallest (last_use, slot) with last_use < t, misses in ascending id paired with victims in
+// that order; a tier change is a miss in the new tier's pool (R9).
+#include "m2c_internal.cuh"
+
+namespace m2c {
+namespace {
+
+constexpr int NT = 1024;
+constexpr int NW = NT / 32;
+
+struct LruArgs {
+    int32_t *occ[3];
+    int32_t *last[3];
+    int32_t *slot_of[3];
+    int cap[3];
+    int seg[3];
+    int cnt[3];
+};
+
+// exclusive block scan of one int per thread
+__device__ __forceinline__ int block_scan1(int v, int *tot, int *sm) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) sm[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        int w = (lane < NW) ? sm[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += y;
+        }
+        if (lane < NW) sm[lane] = w;
+    }
+    __syncthreads();
+    const int r = (warp ? sm[warp - 1] : 0) + x - v;
+    *tot = sm[NW - 1];
+    __syncthreads();
+    return r;
+}
+
+__global__ void __launch_bounds__(NT, 1)
+    k_lru(LruArgs a, const int32_t *__restrict__ step_ptr, const int32_t *__restrict__ tier_ids, int32_t *__restrict__ slots,
+          uint32_t *__restrict__ hit_bits, int32_t *__restrict__ hit_items,
+          int32_t *__restrict__ miss_items, int32_t *__restrict__ miss_ids,
+          int32_t *__restrict__ miss_log, int32_t *__restrict__ evict_log,
+          int32_t *__restrict__ counts, unsigned long long *__restrict__ stats, int P2) {
+    extern __shared__ __align__(16) uint8_t smraw[];
+    unsigned long long *ck = reinterpret_cast<unsigned long long *>(smraw);  // [P2]
+    int32_t *mpos = reinterpret_cast<int32_t *>(smraw + 8 * (size_t)P2);     // [cnt]
+    __shared__ int scan_sm[NW];
+    griddep_wait();
+    const int t = *step_ptr;
+    const int tau = blockIdx.x;
+    const int n = a.cnt[tau], seg = a.seg[tau], C = a.cap[tau];
+    int32_t *occ = a.occ[tau], *last = a.last[tau], *slot_of = a.slot_of[tau];
+    const int32_t *R = tier_ids + seg;
+
+    // 1. hits: refresh their timestamp (a hit never moves slot)
+    const int CH = (n + NT - 1) / NT;
+    const int i0 = min(n, (int)threadIdx.x * CH), i1 = min(n, i0 + CH);
+    int nh = 0;
+    for (int i = i0; i < i1; i++) {
+        const int sl = slot_of[R[i]];
+        if (sl >= 0) {
+            last[sl] = t;
+            slots[seg + i] = sl;
+            atomicOr(&hit_bits[(seg + i) >> 5], 1u << ((seg + i) & 31));
+            nh++;
+        }
+    }
+    int tot_h;
+    int hpos = block_scan1(nh, &tot_h, scan_sm);  // also a barrier: last[] writes visible
+    int mp = (i0 - (hpos)) ;  // misses before this chunk = i0 - hits before it
+    for (int i = i0; i < i1; i++) {
+        const int sl = slot_of[R[i]];
+        if (sl >= 0) hit_items[seg + hpos++] = sl;
+        else mpos[mp++] = i;
+    }
+    const int nm = n - tot_h;
+    // 3. victims: the nm smallest (last_use, slot) among slots with last_use < t
+    for (int sl = threadIdx.x; sl < P2; sl += NT) {
+        unsigned long long key = ~0ull;
+        if (sl < C) {
+            const int lu = last[sl];
+            if (lu < t) key = ((unsigned long long)(uint32_t)(lu + 1) << 32) | (uint32_t)sl;
+        }
+        ck[sl] = key;
+    }
+    __syncthreads();
+    for (int size = 2; size <= P2; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int i = threadIdx.x; i < P2 / 2; i += NT) {
+                const int lo = 2 * i - (i & (stride - 1));
+                const int hi = lo + stride;
+                const bool asc = ((lo & size) == 0);
+                const unsigned long long x = ck[lo], y = ck[hi];
+                if ((x > y) == asc) {
+                    ck[lo] = y;
+                    ck[hi] = x;
+                }
+            }
+            __syncthreads();
+        }
+    }
+    // 4. install misses[m] in victim[m]; evictions compacted in miss order
+    const int MC = (nm + NT - 1) / NT;
+    const int m0 = min(nm, (int)threadIdx.x * MC), m1 = min(nm, m0 + MC);
+    int ne = 0;
+    for (int m = m0; m < m1; m++) ne += occ[(uint32_t)ck[m]] >= 0;
+    int tot_e;
+    int epos = block_scan1(ne, &tot_e, scan_sm);
+    for (int m = m0; m < m1; m++) {
+        const int i = mpos[m];
+        const int id = R[i];
+        const int sl = (int)(uint32_t)ck[m];
+        const int old = occ[sl];
+        if (old >= 0) {
+            slot_of[old] = -1;
+            if (evict_log) {
+                evict_log[2 * (seg + epos)] = old;
+                evict_log[2 * (seg + epos) + 1] = sl;
+            }
+            epos++;
+        }
+        occ[sl] = id;
+        slot_of[id] = sl;
+        last[sl] = t;
+        slots[seg + i] = sl;
+        miss_items[seg + m] = sl;
+        miss_ids[seg + m] = id;
+        if (miss_log) {
+            miss_log[2 * (seg + m)] = id;
+            miss_log[2 * (seg + m) + 1] = sl;
+        }
+    }
+    if (threadIdx.x == 0) {
+        counts[4 + tau] = tot_h;
+        counts[8 + tau] = nm;
+        counts[12 + tau] = tot_e;
+        atomicAdd(&stats[tau], (unsigned long long)tot_h);
+        atomicAdd(&stats[3 + tau], (unsigned long long)nm);
+    }
+}
+
+struct FillArgs {
+    const uint8_t *host[3];
+    uint8_t *pool[3];
+    int64_t nb[3];
+    int seg[3];
+};
+
+// a5: SM-driven gather of the missed records from the pinned host tier (UVA-mapped) into
+// their victim slots.  One warp per record, 8 x 16 B loads in flight per lane.
+__global__ void __launch_bounds__(256) k_fill(FillArgs a, const int32_t *__restrict__ counts,
+                                              const int32_t *__restrict__ miss_ids,
+                                              const int32_t *__restrict__ miss_items) {
+    griddep_wait();
+    const int c0 = counts[8], c1 = counts[9], c2 = counts[10];
+    const int total = c0 + c1 + c2;
+    const int lane = threadIdx.x & 31;
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nwarps = (gridDim.x * blockDim.x) >> 5;
+    for (int w = gw; w < total; w += nwarps) {
+        const int tau = w < c0 ? 0 : (w < c0 + c1 ? 1 : 2);
+        const int m = w - (tau == 0 ? 0 : (tau == 1 ? c0 : c0 + c1));
+        const int id = miss_ids[a.seg[tau] + m];
+        const int sl = miss_items[a.seg[tau] + m];
+        const int64_t nv = a.nb[tau] / 16;
+        const uint4 *src = reinterpret_cast<const uint4 *>(a.host[tau] + (int64_t)id * a.nb[tau]);
+        uint4 *dst = reinterpret_cast<uint4 *>(a.pool[tau] + (int64_t)sl * a.nb[tau]);
+        for (int64_t base = 0; base < nv; base += 32 * 8) {
+            uint4 v[8];
+#pragma unroll
+            for (int j = 0; j < 8; j++) {
+                const int64_t c = base + lane + 32 * j;
+                if (c < nv) v[j] = src[c];
+            }
+#pragma unroll
+            for (int j = 0; j < 8; j++) {
+                const int64_t c = base + lane + 32 * j;
+                if (c < nv) dst[c] = v[j];
+            }
+        }
+    }
+}
+
+}  // namespace
+
+size_t lru_smem_bytes(int P2, int maxcnt) { return 8 * (size_t)P2 + 4 * (size_t)maxcnt; }
+
+cudaError_t init_cache_attrs() {
+    return cudaFuncSetAttribute(k_lru, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)lru_smem_bytes(kMaxPoolSlots, kMaxPoolSlots));
+}
+
+cudaError_t launch_lru(m2c_ctx *c, LayerState &L, const int32_t *step_dev, const int32_t *tier_ids,
+                       const m2c_tier_plan &p, int32_t *slots, uint32_t *hit_bits,
+                       int32_t *miss_log, int32_t *evict_log, cudaStream_t st) {
+    LruArgs a;
+    const int cnt[3] = {p.k_fp16, p.k_int8, p.k_int4};
+    const int seg[3] = {0, p.k_fp16, p.k_fp16 + p.k_int8};
+    int P2 = 2, maxcnt = 1;
+    for (int t = 0; t < 3; t++) {
+        a.occ[t] = L.occupant[t];
+        a.last[t] = L.last[t];
+        a.slot_of[t] = L.slot_of[t];
+        a.cap[t] = L.cap[t];
+        a.seg[t] = seg[t];
+        a.cnt[t] = cnt[t];
+        while (P2 < L.cap[t]) P2 <<= 1;
+        maxcnt = cnt[t] > maxcnt ? cnt[t] : maxcnt;
+    }
+    cudaError_t e = cudaMemsetAsync(hit_bits, 0, sizeof(uint32_t) * ((p.k + 31) / 32 + 1), st);
+    if (e != cudaSuccess) return e;
+    const size_t smem = lru_smem_bytes(P2, maxcnt);
+    e = launch_k(k_lru, dim3(3), dim3(NT), smem, st, a, step_dev, tier_ids, slots, hit_bits,
+                 c->ws.hit_items, c->ws.miss_items, c->ws.miss_ids, miss_log, evict_log,
+                 c->ws.counts, c->ws.stats, P2);
+    c->launch_counter++;
+    return e;
+}
+
+cudaError_t launch_fill(m2c_ctx *c, const LayerState &L, const m2c_tier_plan &p,
+                        cudaStream_t st) {
+    FillArgs a;
+    const int seg[3] = {0, p.k_fp16, p.k_fp16 + p.k_int8};
+    for (int t = 0; t < 3; t++) {
+        a.host[t] = L.host_rec[t];
+        a.pool[t] = L.pool[t];
+        a.nb[t] = c->nb[t];
+        a.seg[t] = seg[t];
+    }
+    cudaError_t e = launch_k(k_fill, dim3(64), dim3(256), 0, st, a, c->ws.counts, c->ws.miss_ids,
+                             c->ws.miss_items);
+    c->launch_counter++;
+    return e;
+}
+
+}  // namespace m2c

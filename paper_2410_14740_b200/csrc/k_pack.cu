@@ -1,0 +1,129 @@
+// k_pack.cu -- a0: offline packing of neuron records in the three precision tiers.
+//
+// Paper: neuron = row of the first FFN matrices + column of the next; active
+// neurons are "quantized to a smaller number of bits" by score (P:73 step 3) and
+// dequantised "back to FP16" for compute; tiers FP16 / INT8 / INT4.
+// Scheme (the paper is silent): DESIGN.md R4 -- asymmetric min/max per 128-group over the
+// range extended to include 0, fp16 scale, u8 zero-point, IEEE fp32 RNE single ops.
+// The IEEE intrinsics (__fsub_rn, __fdiv_rn, __float2int_rn) are never contracted or
+// approximated, so the bytes are reproducible bit for bit.
+#include "m2c_internal.cuh"
+
+namespace m2c {
+namespace {
+
+// One warp per 128-group; blockIdx.y = matrix (0 gate, 1 up, 2 down), blockIdx.x = neuron.
+template <int BITS>
+__global__ void __launch_bounds__(128) k_pack_q(int d, const __half *__restrict__ g,
+                                                const __half *__restrict__ u,
+                                                const __half *__restrict__ dn, int64_t n0,
+                                                int64_t nb, uint8_t *__restrict__ out) {
+    griddep_wait();
+    constexpr int maxq = (1 << BITS) - 1;
+    const int m = blockIdx.y;
+    const int64_t n = n0 + blockIdx.x;
+    const int G = d / 128;
+    const __half *w = (m == 0 ? g : (m == 1 ? u : dn)) + n * (int64_t)d;
+    uint8_t *rec = out + (int64_t)blockIdx.x * nb;
+    const int64_t data_bytes = (BITS == 8) ? 3LL * d : 3LL * d / 2;
+    uint8_t *scales = rec + data_bytes;
+    uint8_t *zeros = scales + 6 * G;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int gi = warp; gi < G; gi += blockDim.x / 32) {
+        const uint2 raw = *reinterpret_cast<const uint2 *>(w + gi * 128 + lane * 4);
+        float v[4];
+        {
+            __half2 a = *reinterpret_cast<const __half2 *>(&raw.x);
+            __half2 b = *reinterpret_cast<const __half2 *>(&raw.y);
+            v[0] = __low2float(a);
+            v[1] = __high2float(a);
+            v[2] = __low2float(b);
+            v[3] = __high2float(b);
+        }
+        float lo = 0.f, hi = 0.f;  // range extended to include 0
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            lo = fminf(lo, v[j]);
+            hi = fmaxf(hi, v[j]);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+            hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        }
+        unsigned short s16;
+        if (lo == hi) {
+            s16 = 0x3c00;  // 1.0
+        } else {
+            const float s32 = __fdiv_rn(__fsub_rn(hi, lo), (float)maxq);
+            s16 = __half_as_ushort(__float2half_rn(s32));
+            if ((s16 & 0x7fff) == 0) s16 = 0x0001;  // underflow -> 2^-24
+        }
+        const float s = __half2float(__ushort_as_half(s16));
+        int z = __float2int_rn(__fdiv_rn(-lo, s));
+        z = min(max(z, 0), maxq);
+        int q[4];
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            int qi = __float2int_rn(__fdiv_rn(v[j], s)) + z;
+            q[j] = min(max(qi, 0), maxq);
+        }
+        if (BITS == 8) {
+            uint32_t word = (uint32_t)q[0] | ((uint32_t)q[1] << 8) | ((uint32_t)q[2] << 16) |
+                            ((uint32_t)q[3] << 24);
+            *reinterpret_cast<uint32_t *>(rec + (int64_t)m * d + gi * 128 + lane * 4) = word;
+        } else {
+            uint16_t hw = (uint16_t)(q[0] | (q[1] << 4) | (q[2] << 8) | (q[3] << 12));
+            *reinterpret_cast<uint16_t *>(rec + (int64_t)m * (d / 2) + gi * 64 + lane * 2) = hw;
+        }
+        if (lane == 0) {
+            *reinterpret_cast<unsigned short *>(scales + 2 * (m * G + gi)) = s16;
+            zeros[m * G + gi] = (uint8_t)z;
+        }
+    }
+    if (m == 2 && threadIdx.x == 0) {  // zero the 16-B padding tail
+        for (int64_t b = data_bytes + 9 * G; b < nb; b++) rec[b] = 0;
+    }
+}
+
+// FP16 tier: the record is the raw concatenation gate[d] | up[d] | down[d].
+__global__ void __launch_bounds__(256) k_pack_f16(int d, const __half *__restrict__ g,
+                                                  const __half *__restrict__ u,
+                                                  const __half *__restrict__ dn, int64_t n0,
+                                                  uint8_t *__restrict__ out) {
+    griddep_wait();
+    const int64_t n = n0 + blockIdx.x;
+    const int vec = d / 8;  // uint4 per row
+    uint4 *rec = reinterpret_cast<uint4 *>(out + (int64_t)blockIdx.x * 6 * d);
+    for (int i = threadIdx.x; i < 3 * vec; i += blockDim.x) {
+        const int m = i / vec, j = i % vec;
+        const __half *w = (m == 0 ? g : (m == 1 ? u : dn)) + n * (int64_t)d;
+        rec[i] = reinterpret_cast<const uint4 *>(w)[j];
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_pack(int d, int bits, const __half *g, const __half *u, const __half *dn,
+                        int64_t n0, int64_t n1, uint8_t *out, cudaStream_t st) {
+    int64_t n = n1 - n0;
+    if (n <= 0) return cudaSuccess;
+    const int64_t nb = m2c_record_bytes(bits, d);
+    for (int64_t off = 0; off < n; off += 65535) {  // grid.x limit for the y-dimensioned launch
+        const int64_t cnt = (n - off < 65535) ? n - off : 65535;
+        cudaError_t e;
+        if (bits == 16)
+            e = launch_k(k_pack_f16, dim3((unsigned)cnt), dim3(256), 0, st, d, g, u, dn, n0 + off,
+                         out + off * nb);
+        else if (bits == 8)
+            e = launch_k(k_pack_q<8>, dim3((unsigned)cnt, 3), dim3(128), 0, st, d, g, u, dn,
+                         n0 + off, nb, out + off * nb);
+        else
+            e = launch_k(k_pack_q<4>, dim3((unsigned)cnt, 3), dim3(128), 0, st, d, g, u, dn,
+                         n0 + off, nb, out + off * nb);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
+}  // namespace m2c

@@ -1,0 +1,105 @@
+// k_reduce.cu -- a7: deterministic reduction of the per-CTA partial sums, fp16 output and the
+// stack residual x_{l+1} = fp16(x_l + fp16(y_l)) (R14), plus small helpers.
+// The reduction order is fixed (partial rows in ascending order within each of 8 warp lanes,
+// then the 8 lanes in order), so y is bit-reproducible run to run.
+#include "m2c_internal.cuh"
+
+namespace m2c {
+namespace {
+
+// grid d/32 CTAs x 256 threads: lane = element of a 32-element slice, warp w sums rows w::8
+__global__ void __launch_bounds__(256) k_reduce(int d, int np, const float *__restrict__ partial,
+                                                const __half *__restrict__ x,
+                                                float *__restrict__ y32, __half *__restrict__ y16,
+                                                __half *__restrict__ x_next) {
+    __shared__ float sm[8][33];
+    griddep_wait();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int e = blockIdx.x * 32 + lane;
+    float acc = 0.f;
+    for (int r = warp; r < np; r += 8) acc += partial[(int64_t)r * d + e];
+    sm[warp][lane] = acc;
+    __syncthreads();
+    if (warp == 0) {
+        float y = 0.f;
+#pragma unroll
+        for (int w = 0; w < 8; w++) y += sm[w][lane];
+        if (y32) y32[e] = y;
+        const __half yh = __float2half_rn(y);
+        if (y16) y16[e] = yh;
+        if (x_next) x_next[e] = __hadd(x[e], yh);
+    }
+    griddep_launch();
+}
+
+__global__ void k_finalize(int d, const float *__restrict__ y32, const __half *__restrict__ x,
+                           __half *__restrict__ y16, __half *__restrict__ x_next) {
+    griddep_wait();
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < d) {
+        const __half yh = __float2half_rn(y32[e]);
+        if (y16) y16[e] = yh;
+        if (x_next) x_next[e] = __hadd(x[e], yh);
+    }
+}
+
+__global__ void k_fill_i32(int32_t *p, int32_t v, int64_t n) {
+    griddep_wait();
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = v;
+}
+
+__global__ void k_iota(int32_t *p, int64_t n) {
+    griddep_wait();
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = (int32_t)i;
+}
+
+__global__ void k_set_counts(int32_t *dst, int32_t a, int32_t b, int32_t c) {
+    griddep_wait();
+    dst[0] = a;
+    dst[1] = b;
+    dst[2] = c;
+}
+
+}  // namespace
+
+cudaError_t launch_reduce(m2c_ctx *c, int n_partials, const float *partial, const __half *x,
+                          float *y32, __half *y16, __half *x_next, cudaStream_t st) {
+    const int d = c->desc.d_model;
+    cudaError_t e = launch_k(k_reduce, dim3(d / 32), dim3(256), 0, st, d, n_partials, partial, x,
+                             y32, y16, x_next);
+    c->launch_counter++;
+    return e;
+}
+
+cudaError_t launch_finalize(m2c_ctx *c, const float *y32, const __half *x, __half *y16,
+                            __half *x_next, cudaStream_t st) {
+    const int d = c->desc.d_model;
+    cudaError_t e = launch_k(k_finalize, dim3((d + 255) / 256), dim3(256), 0, st, d, y32, x, y16,
+                             x_next);
+    c->launch_counter++;
+    return e;
+}
+
+cudaError_t launch_fill_i32(int32_t *p, int32_t v, int64_t n, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    int64_t blocks = (n + 255) / 256;
+    if (blocks > 4096) blocks = 4096;
+    return launch_k(k_fill_i32, dim3((unsigned)blocks), dim3(256), 0, st, p, v, n);
+}
+
+cudaError_t launch_iota(int32_t *p, int64_t n, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    int64_t blocks = (n + 255) / 256;
+    if (blocks > 4096) blocks = 4096;
+    return launch_k(k_iota, dim3((unsigned)blocks), dim3(256), 0, st, p, n);
+}
+
+cudaError_t launch_set_counts(int32_t *dst, int32_t a, int32_t b, int32_t c, cudaStream_t st) {
+    return launch_k(k_set_counts, dim3(1), dim3(1), 0, st, dst, a, b, c);
+}
+
+}  // namespace m2c

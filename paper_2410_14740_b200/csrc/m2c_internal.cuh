@@ -1,0 +1,228 @@
+// m2c_internal.cuh -- shared internals of libm2c (context, PTX wrappers, launch helpers).
+// Part of the PRODUCT path.  Shares nothing with oracle/ (see DESIGN.md §3).
+#pragma once
+
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/m2c.h"
+
+namespace m2c {
+
+// ----------------------------------------------------------------------------------------
+// error plumbing
+// ----------------------------------------------------------------------------------------
+void set_error(const std::string &msg);
+m2c_status fail(m2c_status st, const std::string &msg);
+m2c_status cuda_fail(cudaError_t e, const char *what);
+
+#define M2C_CUDA(call)                                                   \
+    do {                                                                 \
+        cudaError_t _e = (call);                                         \
+        if (_e != cudaSuccess) return ::m2c::cuda_fail(_e, #call);      \
+    } while (0)
+
+constexpr int kMaxPoolSlots = 8192;  // LRU / ATU pool limit (single-CTA bitonic victim sort)
+constexpr int kSelectThreads = 1024;
+
+// ----------------------------------------------------------------------------------------
+// context
+// ----------------------------------------------------------------------------------------
+struct LayerState {
+    bool loaded = false;
+    int mode = 0;  // 0 resident, 1 lru, 2 atu
+    int cap[3] = {0, 0, 0};
+    const int8_t *A = nullptr;  // [r][d]
+    const int8_t *B = nullptr;  // [F_r][r]
+    uint8_t *pool[3] = {nullptr, nullptr, nullptr};
+    int32_t *occupant[3] = {nullptr, nullptr, nullptr};
+    int32_t *last[3] = {nullptr, nullptr, nullptr};
+    int32_t *slot_of[3] = {nullptr, nullptr, nullptr};
+    const uint8_t *host_rec[3] = {nullptr, nullptr, nullptr};
+    int64_t last_step = INT64_MIN;
+};
+
+struct NcclApi;  // dlopen'd NCCL entry points
+
+struct Workspace {
+    int32_t *h = nullptr;          // [r]
+    int32_t *s = nullptr;          // [F_r]
+    int32_t *tier_ids = nullptr;   // [F_r]
+    int8_t *tier_of = nullptr;     // [F_r]
+    int32_t *slots = nullptr;      // [F_r]
+    uint32_t *hit_bits = nullptr;  // [F_r/32 + 1]
+    int32_t *hit_items = nullptr;  // [F_r]  compacted hit slots, tier segments
+    int32_t *miss_items = nullptr; // [F_r]  compacted miss slots, tier segments
+    int32_t *miss_ids = nullptr;   // [F_r]  compacted miss ids (fill source), tier segments
+    int32_t *counts = nullptr;     // [16]: 0..2 plan counts, 4..6 hits, 8..10 misses, 12..14 evictions
+    float *partial = nullptr;      // [2][G][d]
+    float *y32 = nullptr;          // [d]
+    __half *xbuf = nullptr;        // [d]
+    unsigned long long *stats = nullptr;  // [6] hits[3], misses[3] cumulative
+    uint32_t *err = nullptr;       // device error flag
+};
+
+}  // namespace m2c
+
+struct m2c_ctx {
+    m2c_model_desc desc{};
+    int F_r = 0;
+    int device = 0;
+    int num_sms = 148;
+    cudaStream_t compute = nullptr, copy = nullptr;
+    m2c_tier_plan plan{};
+    int64_t nb[3] = {0, 0, 0};
+    std::vector<m2c::LayerState> layers;
+    void *ws_mem = nullptr;
+    size_t ws_bytes = 0;
+    m2c::Workspace ws;
+    int G = 148;              // FFN grid (persistent CTAs)
+    cudaEvent_t ev_lookup = nullptr, ev_fill = nullptr;
+    // decode graph
+    bool use_graph = true;
+    cudaGraphExec_t graph = nullptr;
+    void *graph_x = nullptr;
+    int64_t kernels_per_token = 0;
+    int64_t launch_counter = 0;
+    // phase timing events (m2c_profile): 5 per layer
+    std::vector<cudaEvent_t> prof_ev;
+    // multi-GPU
+    m2c::NcclApi *nccl = nullptr;
+    void *comm = nullptr;
+    int nranks = 1, rank = 0;
+};
+
+namespace m2c {
+
+// ----------------------------------------------------------------------------------------
+// launchers (defined in the kernel .cu files); all enqueue on `st`, PDL-enabled
+// ----------------------------------------------------------------------------------------
+cudaError_t launch_pack(int d, int bits, const __half *g, const __half *u, const __half *dn,
+                        int64_t n0, int64_t n1, uint8_t *out, cudaStream_t st);
+cudaError_t launch_predict(m2c_ctx *c, const LayerState &L, const __half *x, int32_t *scores,
+                           cudaStream_t st);
+cudaError_t launch_select(m2c_ctx *c, const int32_t *scores, const m2c_tier_plan &p,
+                          int32_t *rank_list, int8_t *tier_of, int32_t *tier_ids, cudaStream_t st);
+cudaError_t launch_lru(m2c_ctx *c, LayerState &L, const int32_t *step_dev, const int32_t *tier_ids,
+                       const m2c_tier_plan &p, int32_t *slots, uint32_t *hit_bits,
+                       int32_t *miss_log, int32_t *evict_log, cudaStream_t st);
+cudaError_t launch_fill(m2c_ctx *c, const LayerState &L, const m2c_tier_plan &p, cudaStream_t st);
+cudaError_t launch_ffn(m2c_ctx *c, const LayerState &L, const __half *x, const int32_t *items,
+                       const int32_t *counts, const m2c_tier_plan &p, float *partial,
+                       cudaStream_t st);
+cudaError_t launch_reduce(m2c_ctx *c, int n_partials, const float *partial, const __half *x,
+                          float *y32, __half *y16, __half *x_next, cudaStream_t st);
+cudaError_t launch_finalize(m2c_ctx *c, const float *y32, const __half *x, __half *y16,
+                            __half *x_next, cudaStream_t st);
+cudaError_t init_select_attrs();
+cudaError_t init_cache_attrs();
+cudaError_t init_ffn_attrs();
+cudaError_t launch_fill_i32(int32_t *p, int32_t v, int64_t n, cudaStream_t st);
+cudaError_t launch_set_counts(int32_t *dst, int32_t a, int32_t b, int32_t c, cudaStream_t st);
+cudaError_t launch_iota(int32_t *p, int64_t n, cudaStream_t st);
+
+// PDL-enabled launch (programmatic stream serialization): the dependent kernel calls
+// griddep_wait() before touching its predecessor's outputs.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                     cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
+// ----------------------------------------------------------------------------------------
+// device helpers
+// ----------------------------------------------------------------------------------------
+__device__ __forceinline__ void griddep_wait() {
+#if defined(__CUDA_ARCH__) && __CUDA_ARCH__ >= 900
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+__device__ __forceinline__ void griddep_launch() {
+#if defined(__CUDA_ARCH__) && __CUDA_ARCH__ >= 900
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+                 : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// 1-D bulk copy global -> shared (TMA engine; SASS UBLKCP), completion on an mbarrier.
+// EVICT_FIRST L2 policy: the neuron records are streamed once per token.
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes,
+                                         uint64_t *bar, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+        "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+
+__device__ __forceinline__ int warp_sum_i(int v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ float warp_sum_f(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// exact sgn(v) * floor((254|v| + M) / (2M)) for |v| <= M < 2^45 (R2); double division is
+// correctly rounded and num, den < 2^53 are exact, so the floor is off by at most one and
+// the two integer checks fix it.
+__device__ __forceinline__ int quant127(long long v, long long M) {
+    if (M == 0) return 0;
+    long long a = v < 0 ? -v : v;
+    long long num = 254 * a + M, den = 2 * M;
+    long long q = (long long)floor((double)num / (double)den);
+    if (q * den > num) q -= 1;
+    if ((q + 1) * den <= num) q += 1;
+    return (int)(v < 0 ? -q : q);
+}
+
+}  // namespace m2c
