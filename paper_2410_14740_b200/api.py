@@ -215,6 +215,9 @@ class M2CContext:
     def set_graph(self, enable: bool):
         check(lib().m2c_set_graph(self._h, 1 if enable else 0))
 
+    def set_fused(self, enable: bool):
+        check(lib().m2c_set_fused(self._h, 1 if enable else 0))
+
     def profile(self, enable: bool):
         check(lib().m2c_profile(self._h, 1 if enable else 0))
 

@@ -26,7 +26,6 @@ m2c_status cuda_fail(cudaError_t e, const char *what) {
 size_t select_smem_bytes(int F_r, int P2);
 size_t select_smem_limit();
 size_t lru_smem_bytes(int P2, int maxcnt);
-int ffn_nch(int d);
 
 // ---- NCCL, loaded at run time (no link-time dependency) ----
 typedef int ncclResult_t;
@@ -149,13 +148,19 @@ static cudaError_t enqueue_layer(m2c_ctx *c, int l, __half *x) {
     const m2c_tier_plan &p = c->plan;
     cudaStream_t st = c->compute;
     cudaError_t e;
+    // resident layers: predictor (+ score histogram) -> fused select+FFN -> reduce (4 kernels)
+    const bool fused = L.mode == 0 && c->use_fused && ffn_sel_supported(c, p);
+    int32_t *lists = c->prev_ids + (size_t)l * (p.k > 0 ? p.k : 1);
     if ((e = mark(c, l, 0))) return e;
-    if ((e = launch_predict(c, L, x, c->ws.s, st))) return e;
+    if ((e = launch_predict(c, L, x, c->ws.s, fused ? c->ghist : nullptr, st))) return e;
     if ((e = mark(c, l, 1))) return e;
-    if ((e = launch_select(c, c->ws.s, p, nullptr, nullptr, c->ws.tier_ids, st))) return e;
+    if (!fused && (e = launch_select(c, c->ws.s, p, nullptr, nullptr, c->ws.tier_ids, st))) return e;
     if ((e = mark(c, l, 2))) return e;
     int np = c->G;
-    if (L.mode == 0) {
+    if (fused) {
+        e = launch_ffn_sel(c, L, x, c->ws.s, c->ghist, lists, lists, p, c->ws.partial, st);
+        if (e) return e;
+    } else if (L.mode == 0) {
         e = launch_ffn(c, L, x, c->ws.tier_ids, c->ws.counts, p, c->ws.partial, st);
         if (e) return e;
     } else {
@@ -175,13 +180,17 @@ static cudaError_t enqueue_layer(m2c_ctx *c, int l, __half *x) {
     }
     if ((e = mark(c, l, 3))) return e;
     if (c->nranks > 1) {
-        if ((e = launch_reduce(c, np, c->ws.partial, x, c->ws.y32, nullptr, nullptr, st))) return e;
+        if ((e = launch_reduce(c, np, c->ws.partial, x, c->ws.y32, nullptr, nullptr,
+                               fused ? c->ghist : nullptr, st)))
+            return e;
         int r = c->nccl->allReduce(c->ws.y32, c->ws.y32, (size_t)c->desc.d_model, 7 /*f32*/,
                                    0 /*sum*/, c->comm, st);
         if (r != 0) return cudaErrorUnknown;
         if ((e = launch_finalize(c, c->ws.y32, x, nullptr, x, st))) return e;
     } else {
-        if ((e = launch_reduce(c, np, c->ws.partial, x, nullptr, nullptr, x, st))) return e;
+        if ((e = launch_reduce(c, np, c->ws.partial, x, nullptr, nullptr, x,
+                               fused ? c->ghist : nullptr, st)))
+            return e;
     }
     return mark(c, l, 4);
 }
@@ -307,7 +316,16 @@ m2c_status m2c_create(const m2c_model_desc *desc, int32_t device, m2c_stream_t c
                  o_hit = take(4 * (size_t)F_r), o_miss = take(4 * (size_t)F_r),
                  o_mid = take(4 * (size_t)F_r), o_cnt = take(4 * 16),
                  o_part = take(4 * (size_t)2 * c->G * d), o_y = take(4 * (size_t)d),
-                 o_x = take(2 * (size_t)d), o_stats = take(8 * 6), o_err = take(4);
+                 o_x = take(2 * (size_t)d), o_stats = take(8 * 6), o_err = take(4),
+                 o_hist = take(4 * 4096),
+                 o_prev = take(4 * (size_t)desc->n_layers * (plan->k > 0 ? plan->k : 1));
+    // score histogram geometry: |s| <= 127^2 r, bins of 2^sh over [0, 2 smax] (4096 bins)
+    c->sel_smax = 16129 * desc->pred_rank;
+    {
+        int bits = 0;
+        while ((1LL << bits) <= 2LL * c->sel_smax) bits++;
+        c->sel_sh = bits > 12 ? bits - 12 : 0;
+    }
     cudaError_t e = cudaMalloc(&c->ws_mem, off);
     if (e != cudaSuccess) {
         delete c;
@@ -330,7 +348,11 @@ m2c_status m2c_create(const m2c_model_desc *desc, int32_t device, m2c_stream_t c
     c->ws.xbuf = (__half *)(b + o_x);
     c->ws.stats = (unsigned long long *)(b + o_stats);
     c->ws.err = (uint32_t *)(b + o_err);
+    c->ghist = (int *)(b + o_hist);
+    c->prev_ids = (int32_t *)(b + o_prev);
     e = cudaMemset(c->ws_mem, 0, off);
+    if (e == cudaSuccess)  // no previous selection yet: -1 disables the prefetch hint
+        e = cudaMemset(c->prev_ids, 0xff, 4 * (size_t)desc->n_layers * (plan->k > 0 ? plan->k : 1));
     static bool attrs_done = false;
     if (e == cudaSuccess && !attrs_done) {
         e = init_select_attrs();
@@ -458,7 +480,7 @@ m2c_status m2c_predict_rank(m2c_ctx *c, int32_t layer, const void *x, const m2c_
         return fail(M2C_ERR_CAPACITY, "F_r too large for the single-CTA select");
     }
     int32_t *s = scores ? scores : c->ws.s;
-    M2C_CUDA(launch_predict(c, c->layers[layer], (const __half *)x, s, c->compute));
+    M2C_CUDA(launch_predict(c, c->layers[layer], (const __half *)x, s, nullptr, c->compute));
     M2C_CUDA(launch_select(c, s, *plan, rank_list, tier_of, tier_ids, c->compute));
     return M2C_OK;
 }
@@ -542,7 +564,7 @@ m2c_status m2c_sparse_ffn_forward(m2c_ctx *c, int32_t layer, const void *x, cons
         np = 2 * c->G;
     }
     if (c->nranks > 1) {
-        M2C_CUDA(launch_reduce(c, np, c->ws.partial, xh, c->ws.y32, nullptr, nullptr, cs));
+        M2C_CUDA(launch_reduce(c, np, c->ws.partial, xh, c->ws.y32, nullptr, nullptr, nullptr, cs));
         if (y_partial)
             M2C_CUDA(cudaMemcpyAsync(y_partial, c->ws.y32, 4 * (size_t)d, cudaMemcpyDeviceToDevice, cs));
         if (y) {
@@ -551,7 +573,7 @@ m2c_status m2c_sparse_ffn_forward(m2c_ctx *c, int32_t layer, const void *x, cons
             M2C_CUDA(launch_finalize(c, c->ws.y32, xh, (__half *)y, nullptr, cs));
         }
     } else {
-        M2C_CUDA(launch_reduce(c, np, c->ws.partial, xh, y_partial, (__half *)y, nullptr, cs));
+        M2C_CUDA(launch_reduce(c, np, c->ws.partial, xh, y_partial, (__half *)y, nullptr, nullptr, cs));
     }
     return M2C_OK;
 }
@@ -594,6 +616,16 @@ m2c_status m2c_comm_init(m2c_ctx *c, int32_t nranks, int32_t rank, const void *u
 m2c_status m2c_set_graph(m2c_ctx *c, int32_t enable) {
     if (!c) return fail(M2C_ERR_INVALID_ARG, "null ctx");
     c->use_graph = enable != 0;
+    return M2C_OK;
+}
+
+m2c_status m2c_set_fused(m2c_ctx *c, int32_t enable) {
+    if (!c) return fail(M2C_ERR_INVALID_ARG, "null ctx");
+    if (c->use_fused != (enable != 0) && c->graph) {
+        cudaGraphExecDestroy(c->graph);
+        c->graph = nullptr;
+    }
+    c->use_fused = enable != 0;
     return M2C_OK;
 }
 

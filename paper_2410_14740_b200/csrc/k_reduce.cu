@@ -7,29 +7,43 @@
 namespace m2c {
 namespace {
 
-// grid d/32 CTAs x 256 threads: lane = element of a 32-element slice, warp w sums rows w::8
-__global__ void __launch_bounds__(256) k_reduce(int d, int np, const float *__restrict__ partial,
-                                                const __half *__restrict__ x,
-                                                float *__restrict__ y32, __half *__restrict__ y16,
-                                                __half *__restrict__ x_next) {
-    __shared__ float sm[8][33];
+// grid d/32 CTAs x 1024 threads: lane = element of a 32-element slice, warp w sums rows w::32
+// (<= 10 independent loads in flight per thread), then warp 0 sums the 32 warp totals.
+__global__ void __launch_bounds__(1024) k_reduce(int d, int np, const float *__restrict__ partial,
+                                                 const __half *__restrict__ x,
+                                                 float *__restrict__ y32, __half *__restrict__ y16,
+                                                 __half *__restrict__ x_next,
+                                                 int *__restrict__ hist_zero) {
+    __shared__ float sm[32][33];
+    griddep_launch();
     griddep_wait();
+    // the FFN that read the score histogram is complete: clear it for the next layer
+    if (hist_zero)
+        for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 4096; i += gridDim.x * blockDim.x)
+            hist_zero[i] = 0;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int e = blockIdx.x * 32 + lane;
+    float v[10];
+#pragma unroll
+    for (int i = 0; i < 10; i++) {
+        const int r = warp + 32 * i;
+        v[i] = r < np ? partial[(int64_t)r * d + e] : 0.f;
+    }
     float acc = 0.f;
-    for (int r = warp; r < np; r += 8) acc += partial[(int64_t)r * d + e];
+#pragma unroll
+    for (int i = 0; i < 10; i++) acc += v[i];
+    for (int r = warp + 320; r < np; r += 32) acc += partial[(int64_t)r * d + e];
     sm[warp][lane] = acc;
     __syncthreads();
     if (warp == 0) {
         float y = 0.f;
 #pragma unroll
-        for (int w = 0; w < 8; w++) y += sm[w][lane];
+        for (int w = 0; w < 32; w++) y += sm[w][lane];
         if (y32) y32[e] = y;
         const __half yh = __float2half_rn(y);
         if (y16) y16[e] = yh;
         if (x_next) x_next[e] = __hadd(x[e], yh);
     }
-    griddep_launch();
 }
 
 __global__ void k_finalize(int d, const float *__restrict__ y32, const __half *__restrict__ x,
@@ -67,10 +81,11 @@ __global__ void k_set_counts(int32_t *dst, int32_t a, int32_t b, int32_t c) {
 }  // namespace
 
 cudaError_t launch_reduce(m2c_ctx *c, int n_partials, const float *partial, const __half *x,
-                          float *y32, __half *y16, __half *x_next, cudaStream_t st) {
+                          float *y32, __half *y16, __half *x_next, int *hist_zero,
+                          cudaStream_t st) {
     const int d = c->desc.d_model;
-    cudaError_t e = launch_k(k_reduce, dim3(d / 32), dim3(256), 0, st, d, n_partials, partial, x,
-                             y32, y16, x_next);
+    cudaError_t e = launch_k(k_reduce, dim3(d / 32), dim3(1024), 0, st, d, n_partials, partial, x,
+                             y32, y16, x_next, hist_zero);
     c->launch_counter++;
     return e;
 }

@@ -90,6 +90,12 @@ struct m2c_ctx {
     int64_t launch_counter = 0;
     // phase timing events (m2c_profile): 5 per layer
     std::vector<cudaEvent_t> prof_ev;
+    // fused decode-path select: score histogram (s + sel_smax) >> sel_sh into 4096 bins,
+    // and the previous token's tier lists per layer (L2 prefetch hint)
+    int sel_smax = 0, sel_sh = 0;
+    int *ghist = nullptr;       // [4096]
+    int32_t *prev_ids = nullptr;  // [n_layers][k]
+    bool use_fused = true;
     // multi-GPU
     m2c::NcclApi *nccl = nullptr;
     void *comm = nullptr;
@@ -104,7 +110,11 @@ namespace m2c {
 cudaError_t launch_pack(int d, int bits, const __half *g, const __half *u, const __half *dn,
                         int64_t n0, int64_t n1, uint8_t *out, cudaStream_t st);
 cudaError_t launch_predict(m2c_ctx *c, const LayerState &L, const __half *x, int32_t *scores,
-                           cudaStream_t st);
+                           int *hist, cudaStream_t st);
+cudaError_t launch_ffn_sel(m2c_ctx *c, const LayerState &L, const __half *x, const int32_t *scores,
+                           const int32_t *hist, int32_t *out_ids, const int32_t *prev_ids,
+                           const m2c_tier_plan &p, float *partial, cudaStream_t st);
+bool ffn_sel_supported(m2c_ctx *c, const m2c_tier_plan &p);
 cudaError_t launch_select(m2c_ctx *c, const int32_t *scores, const m2c_tier_plan &p,
                           int32_t *rank_list, int8_t *tier_of, int32_t *tier_ids, cudaStream_t st);
 cudaError_t launch_lru(m2c_ctx *c, LayerState &L, const int32_t *step_dev, const int32_t *tier_ids,
@@ -115,7 +125,7 @@ cudaError_t launch_ffn(m2c_ctx *c, const LayerState &L, const __half *x, const i
                        const int32_t *counts, const m2c_tier_plan &p, float *partial,
                        cudaStream_t st);
 cudaError_t launch_reduce(m2c_ctx *c, int n_partials, const float *partial, const __half *x,
-                          float *y32, __half *y16, __half *x_next, cudaStream_t st);
+                          float *y32, __half *y16, __half *x_next, int *hist_zero, cudaStream_t st);
 cudaError_t launch_finalize(m2c_ctx *c, const float *y32, const __half *x, __half *y16,
                             __half *x_next, cudaStream_t st);
 cudaError_t init_select_attrs();
@@ -195,6 +205,10 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
         "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
         : "memory");
 }
+// bulk L2 prefetch (no smem destination); size multiple of 16, address 16-B aligned
+__device__ __forceinline__ void prefetch_l2(const void *p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes & ~15u) : "memory");
+}
 __device__ __forceinline__ uint64_t policy_evict_first() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -215,6 +229,18 @@ __device__ __forceinline__ float warp_sum_f(float v) {
 // exact sgn(v) * floor((254|v| + M) / (2M)) for |v| <= M < 2^45 (R2); double division is
 // correctly rounded and num, den < 2^53 are exact, so the floor is off by at most one and
 // the two integer checks fix it.
+// Same exact result from an fp32 estimate est ~= 127 |v| / M + 0.5 (|error| << 1): the floor
+// of the estimate is within one of the exact value and two int64 checks pin it.
+__device__ __forceinline__ int quant127_est(long long v, long long M, float est) {
+    if (M == 0) return 0;
+    const long long a = v < 0 ? -v : v;
+    const long long num = 254 * a + M, den = 2 * M;
+    long long q = (long long)__float2int_rd(est);
+    if (q * den > num) q -= 1;
+    else if ((q + 1) * den <= num) q += 1;
+    return (int)(v < 0 ? -q : q);
+}
+
 __device__ __forceinline__ int quant127(long long v, long long M) {
     if (M == 0) return 0;
     long long a = v < 0 ? -v : v;

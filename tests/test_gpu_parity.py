@@ -347,6 +347,34 @@ def test_decode_step_equals_api_chain_and_layer0_oracle(m2c):
     ctx.close()
 
 
+@pytest.mark.parametrize("name,layers", [("T", 3), ("S7", 2), ("S70", 1)])
+def test_decode_fused_select_equals_unfused(m2c, name, layers):
+    """The decode path's fused select+FFN kernel (histogram thresholds, L2 prefetch of the
+    previous selection) gives bit-identical tokens to predict_rank's separate select."""
+    cfg = get_config(name)
+    shard = (0, 8) if name == "S70" else (0, 1)
+    plan = m2c.plan_of(cfg, shard[1])
+    ctxs = []
+    for fused in (True, False):
+        ctx = _ctx(m2c, cfg, plan, n_layers=layers, shard=shard)
+        for l in range(layers):
+            w = layer_weights(cfg, l, device="cuda", shard=shard)
+            ctx.load_layer(l, w["w_gate"], w["w_up"], w["w_down_t"], w["pred_A"], w["pred_B"])
+        ctx.set_fused(fused)
+        ctxs.append(ctx)
+    xs = token_stream(cfg, 6, device="cuda")
+    for t in range(6):
+        outs = []
+        for ctx in ctxs:
+            x = xs[t].contiguous().clone()
+            ctx.decode_step(x, t + 1)
+            outs.append(x)
+        torch.cuda.synchronize()
+        assert torch.equal(outs[0], outs[1]), t
+    for ctx in ctxs:
+        ctx.close()
+
+
 def test_decode_step_lru_matches_api_chain(m2c):
     cfg = get_config("T")
     L = 2
