@@ -174,6 +174,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--eager", action="store_true", help="no CUDA graph")
+    ap.add_argument("--unfused", action="store_true", help="separate select kernel")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -186,6 +187,7 @@ def main():
     import torch.distributed as dist
 
     from paper_2410_14740_b200 import (M2CContext, cache_cfg_capped, nccl_unique_id, plan_of)
+    from paper_2410_14740_b200 import dist as m2c_dist
     from synth import get_config, layer_weights, token_stream
 
     assert args.warmup >= 3, "timing rules: W >= 3"
@@ -201,9 +203,7 @@ def main():
     ctx = M2CContext(cfg.d_model, cfg.d_ff, cfg.n_layers, cfg.pred_rank, plan, shard=(rank, P),
                      act=0 if cfg.act == "silu" else 1, device=local)
     if P > 1:
-        uid = [nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        ctx.comm_init(P, rank, uid[0])
+        m2c_dist.comm_init(ctx, make_id=nccl_unique_id)
     cc = None
     if cfg.cache_mode != "resident":
         cc = cache_cfg_capped(ctx.desc, plan, 1, 4, cfg.cache_mode)
@@ -218,6 +218,8 @@ def main():
     torch.cuda.empty_cache()
     if args.eager:
         ctx.set_graph(False)
+    if args.unfused:
+        ctx.set_fused(False)
 
     W, K = args.warmup, args.steps
     if cfg.cache_mode != "resident":
@@ -249,10 +251,7 @@ def main():
         e1.record(stream)
         barrier()
     ms = e0.elapsed_time(e1)
-    if world > 1:
-        tmax = torch.tensor([ms], device=dev)
-        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
-        ms = float(tmax.item())
+    ms = m2c_dist.max_over_ranks(ms, device=dev)
     st = ctx.stats()
     kpt = st["kernels_per_token"]
     tok_s = K / (ms / 1e3)
@@ -299,10 +298,7 @@ def main():
             stream.synchronize()
         barrier()
         el = time.perf_counter() - t0
-        if world > 1:
-            te = torch.tensor([el], device=dev)
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-            el = float(te.item())
+        el = m2c_dist.max_over_ranks(el, device=dev)
         e2e = {"value": K / el, "unit": "tokens/s", "h2d_bytes_per_step": 2 * cfg.d_model,
                "d2h_bytes_per_step": 2 * cfg.d_model}
 

@@ -12,9 +12,10 @@
 //    INT8, INT4), balanced on bytes + lambda * weights (memory and issue cost both matter:
 //    an INT4 record has 1/4 of the bytes of an FP16 one but the same 3d weights to dequant).
 //  * Records stream into a shared-memory byte ring by 1-D TMA bulk copies (cp.async.bulk,
-//    SASS UBLKCP), one mbarrier per record, issued by one thread as ring space frees.
-//  * Batches of up to 16 records: gate/up dot products are warp-local (one warp, or a few
-//    warps splitting d, per record; warp-shuffle reductions only), then one barrier, then the
+//    SASS UBLKCP), one mbarrier per record, issued by one thread as ring space frees; the
+//    issuing thread publishes each record's ring offset, and precomputes the batches.
+//  * Batches of up to 16 records: gate/up dot products are warp-local (one warp, or up to
+//    four warps splitting d, per record; warp-shuffle reductions only), then the
 //    down-projection where thread t owns elements [8t, 8t+8) of y in registers.
 //  * Dequant in registers, ~2 instructions per weight: codes become the fp16 value 1024 + q
 //    (or 1024 + 16q for odd INT4 nibbles) by PRMT/LOP3 (magic-exponent trick); HFMA2 removes
@@ -24,9 +25,10 @@
 //  * The per-CTA partial y goes to a [G][d] fp32 buffer reduced in a fixed order by k_reduce.
 //  * k_ffn_sel (decode path) first derives the FP16/INT8/INT4 tier lists itself, redundantly
 //    in every CTA, from the predictor scores and the 4096-bin score histogram k_pred_s left in
-//    global memory (exact thresholds via a second-level histogram, ties by ascending id),
-//    and before waiting on its predecessor prefetches into L2 the records the previous token
-//    selected for this layer (~80% of them recur).
+//    global memory: exact thresholds via a second-level histogram, ties by ascending id,
+//    then warp-ballot classification of 32-id chunks and a block scan over chunks.  Before
+//    waiting on its predecessor it prefetches into L2 the records the previous token selected
+//    for this layer (~80% of them recur).
 #include "m2c_internal.cuh"
 
 namespace m2c {
@@ -34,10 +36,12 @@ namespace {
 
 constexpr int kNBMax = 16;   // records per batch
 constexpr int kNSlot = 32;   // mbarriers (>= records in flight)
-constexpr int kRingList = 192 * 1024;  // == kRingSel: identical batching, bit-identical y
-constexpr int kRingSel = 192 * 1024;
+constexpr int kRing = 192 * 1024;
 constexpr int kHistBins = 4096;
 constexpr int kMaxLocal = 1024;  // records one CTA may own
+constexpr int kXsBytes = 16384;  // x (fp16, d <= 8192)
+// dynamic smem: ring | xs | loc[kMaxLocal] | dsc[kMaxLocal] | bst[kMaxLocal + 1]
+constexpr size_t kSmemBytes = (size_t)kRing + kXsBytes + 4 * (3 * kMaxLocal + 4);
 
 struct FfnArgs {
     const uint8_t *pool[3];
@@ -100,7 +104,6 @@ __device__ __forceinline__ uint32_t zz2_16(uint32_t z) {  // fp16x2 (1024 + 16 z
 }
 
 // ---- warp-local partial dot products of one record over chunks [c0, c1) (8 elements each)
-// xs: fp16 x in smem.  Returns (gate, up) partial sums (scaled) of this lane.
 template <int TIER>
 __device__ __forceinline__ void gu_chunks(const uint8_t *rec, const uint4 *xs, int d, int c0, int c1,
                                           float &pg, float &pu) {
@@ -232,7 +235,7 @@ __device__ __forceinline__ void down_any(int tier, const uint8_t *rec, int d, fl
     else down_t<2>(rec, d, a, y);
 }
 
-// exclusive block scan of up to 3 ints per thread; blockDim.x multiple of 32, <= 1024
+// exclusive block scan of 3 ints per thread; blockDim.x multiple of 32, <= 1024
 __device__ __forceinline__ void block_scan3(const int v[3], int ex[3], int tot[3], int *sm /*[3][32]*/) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     int inc[3];
@@ -269,6 +272,26 @@ __device__ __forceinline__ void block_scan3(const int v[3], int ex[3], int tot[3
     __syncthreads();
 }
 
+// in-place exclusive scan of cnt[q][3] over q < Q (smem), all threads
+__device__ __forceinline__ void scan_chunks(int *cnt, int Q, int *sm) {
+    const int T = blockDim.x;
+    const int per = (Q + T - 1) / T;
+    const int q0 = min(Q, (int)threadIdx.x * per), q1 = min(Q, q0 + per);
+    int v[3] = {0, 0, 0}, ex[3], tot[3];
+    for (int q = q0; q < q1; q++)
+#pragma unroll
+        for (int t = 0; t < 3; t++) v[t] += cnt[3 * q + t];
+    block_scan3(v, ex, tot, sm);
+    for (int q = q0; q < q1; q++)
+#pragma unroll
+        for (int t = 0; t < 3; t++) {
+            const int c = cnt[3 * q + t];
+            cnt[3 * q + t] = ex[t];
+            ex[t] += c;
+        }
+    __syncthreads();
+}
+
 // this CTA's share [i0_t, i1_t) of each tier list, balanced on wt (computed by one thread)
 __device__ __forceinline__ void cta_ranges(const FfnArgs &a, int n0, int n1, int n2, int cta, int G,
                                            int (&r)[6]) {
@@ -292,38 +315,70 @@ struct FfnShared {
     uint64_t bars[kNSlot];
     int span[kNSlot];
     float part[kNBMax][4][2];
-    int rng[8];      // CTA ranges (6) + n_items, spare
+    float a_sm[kNBMax];
+    int ut[kNBMax][32];  // unit table: [nb-1][warp] -> b | p << 8 | P << 16 (-1: idle)
+    int cb[5][5];        // chunk bounds: cb[P][p] = nchunk * p / P
+    int rng[8];          // CTA ranges (6)
+    int nbatch;
     int scan[96];
-    int selv[12];    // select: bins, above, value, rem ...
+    int selv[16];
 };
 
-// The FFN main loop over this CTA's n_items records; item j -> (tier, global pointer)
-template <int RING, class SrcFn>
+// The FFN main loop over this CTA's n_items records; item j -> global record pointer src(j)
+template <class SrcFn>
 __device__ __forceinline__ void ffn_loop(const FfnArgs &a, int d, int act, const __half *x, int n_items,
                                          int c1, int c2, SrcFn src, uint8_t *ring, uint4 *xs,
-                                         FfnShared &sm, float *partial) {
+                                         int *dsc, int *bst, FfnShared &sm, float *partial) {
     const int nwarp = blockDim.x >> 5;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nbA = a.nb[0], nbB = a.nb[1], nbC = a.nb[2];
-    auto size_of = [&](int j) { return j < c1 ? nbA : (j < c2 ? nbB : nbC); };
-    auto tier_of = [&](int j) { return j < c1 ? 0 : (j < c2 ? 1 : 2); };
-    const int nbmax_bytes = nbA > nbB ? (nbA > nbC ? nbA : nbC) : (nbB > nbC ? nbB : nbC);
-
-    // producer state (thread 0)
+    const int nchunk = d / 8;
+    // tables: unit mapping per batch size, chunk bounds per split
+    for (int i = threadIdx.x; i < kNBMax * 32; i += blockDim.x) {
+        const int nb = i / 32 + 1, w = i % 32;
+        const int P = nwarp / nb >= 4 ? 4 : (nwarp / nb >= 1 ? nwarp / nb : 1);
+        sm.ut[nb - 1][w] = (w < nb * P || nwarp < nb) ? ((w % nb) | ((w / nb) << 8) | (P << 16)) : -1;
+    }
+    if (threadIdx.x < 25) {
+        const int P = threadIdx.x / 5, p = threadIdx.x % 5;
+        sm.cb[P][p] = P ? nchunk * p / P : 0;
+    }
+    // thread 0: batches (consecutive records that fit the ring together, with wrap slack)
+    if (threadIdx.x == 0) {
+        const int nbA = a.nb[0], nbB = a.nb[1], nbC = a.nb[2];
+        const int mx = nbA > nbB ? (nbA > nbC ? nbA : nbC) : (nbB > nbC ? nbB : nbC);
+        int nbt = 0;
+        for (int j0 = 0; j0 < n_items;) {
+            int nb = 0, bytes = 0;
+            while (nb < kNBMax && j0 + nb < n_items) {
+                const int j = j0 + nb;
+                const int sz = j < c1 ? nbA : (j < c2 ? nbB : nbC);
+                if (nb > 0 && bytes + sz + mx > kRing) break;
+                bytes += sz;
+                nb++;
+            }
+            bst[nbt++] = j0;
+            j0 += nb;
+        }
+        bst[nbt] = n_items;
+        sm.nbatch = nbt;
+    }
+    // producer state (thread 0): bump allocation in the byte ring; publishes dsc[j]
     int issued = 0, pos_issue = 0, used = 0;
     const uint64_t pol = policy_evict_first();
     auto issue_more = [&](int consumed) {
         while (issued < n_items && issued - consumed < kNSlot) {
             const int j = issued;
-            const int sz = size_of(j);
-            const int waste = (pos_issue + sz > RING) ? RING - pos_issue : 0;
-            if (used + waste + sz > RING) break;
+            const int t = j < c1 ? 0 : (j < c2 ? 1 : 2);
+            const int sz = t == 0 ? a.nb[0] : (t == 1 ? a.nb[1] : a.nb[2]);
+            const int waste = (pos_issue + sz > kRing) ? kRing - pos_issue : 0;
+            if (used + waste + sz > kRing) break;
             const int off = waste ? 0 : pos_issue;
             sm.span[j % kNSlot] = waste + sz;
             used += waste + sz;
             pos_issue = off + sz;
+            dsc[j] = off | (t << 24);
             uint64_t *bar = &sm.bars[j % kNSlot];
-            mbar_expect_tx(bar, (uint32_t)sz);
+            mbar_expect_tx(bar, (uint32_t)sz);  // release: dsc[j] is visible to its waiters
             bulk_g2s(ring + off, src(j), (uint32_t)sz, bar, pol);
             issued++;
         }
@@ -333,77 +388,81 @@ __device__ __forceinline__ void ffn_loop(const FfnArgs &a, int d, int act, const
         issue_more(0);
     }
     // x -> smem as fp16 (read by the warp-local dot products)
-    for (int c = threadIdx.x; c < d / 8; c += blockDim.x) xs[c] = reinterpret_cast<const uint4 *>(x)[c];
+    for (int c = threadIdx.x; c < nchunk; c += blockDim.x) xs[c] = reinterpret_cast<const uint4 *>(x)[c];
     __syncthreads();
 
     float y[8];
 #pragma unroll
     for (int i = 0; i < 8; i++) y[i] = 0.f;
-    const int nchunk = d / 8;
-    int pos_cons = 0;
-    for (int j0 = 0; j0 < n_items;) {
-        // batch: consecutive records that fit the ring together (with wrap slack)
-        int nb = 0, bytes = 0;
-        while (nb < kNBMax && j0 + nb < n_items && bytes + size_of(j0 + nb) + nbmax_bytes <= RING) {
-            bytes += size_of(j0 + nb);
-            nb++;
-        }
-        if (nb == 0) nb = 1;
-        int offs[kNBMax];
-#pragma unroll
-        for (int b = 0; b < kNBMax; b++) {
-            offs[b] = 0;
-            if (b < nb) {
-                const int sz = size_of(j0 + b);
-                if (pos_cons + sz > RING) pos_cons = 0;
-                offs[b] = pos_cons;
-                pos_cons += sz;
-            }
-        }
-        // gate/up: unit u = (item b, part p) per warp; P parts split the chunks of d
-        const int P = nwarp / nb >= 4 ? 4 : (nwarp / nb >= 1 ? nwarp / nb : 1);
-        for (int u = warp; u < nb * P; u += nwarp) {
-            const int b = u % nb, p = u / nb;
+    const int nbt = sm.nbatch;
+    for (int bi = 0; bi < nbt; bi++) {
+        const int j0 = bst[bi], nb = bst[bi + 1] - j0;
+        // gate/up: this warp's units (b, p) of the batch
+        int P = 1;
+        for (int w = warp; w < 32 * ((nb + 31) / 32) && w < (nb > nwarp ? nb : nwarp); w += nwarp) {
+            const int u = nb <= nwarp ? sm.ut[nb - 1][w] : (w | (1 << 16));
+            if (u < 0) break;
+            const int b = u & 0xff, p = (u >> 8) & 0xff;
+            P = u >> 16;
             const int j = j0 + b;
             mbar_wait(&sm.bars[j % kNSlot], (uint32_t)((j / kNSlot) & 1));
-            const int c0 = nchunk * p / P, c1x = nchunk * (p + 1) / P;
+            const int ds = dsc[j];
             float pg, pu;
-            int rb = 0;
-#pragma unroll
-            for (int bb = 0; bb < kNBMax; bb++) rb = (bb == b) ? offs[bb] : rb;
-            gu_any(tier_of(j), ring + rb, xs, d, c0, c1x, pg, pu);
+            gu_any(ds >> 24, ring + (ds & 0xffffff), xs, d, sm.cb[P][p], sm.cb[P][p + 1], pg, pu);
             pg = warp_sum_f(pg);
             pu = warp_sum_f(pu);
             if (lane == 0) {
-                sm.part[b][p][0] = pg;
-                sm.part[b][p][1] = pu;
+                if (P == 1) {
+                    sm.a_sm[b] = (act == 1) ? fmaxf(pg, 0.f) * pu : pg / (1.f + expf(-pg)) * pu;
+                } else {
+                    sm.part[b][p][0] = pg;
+                    sm.part[b][p][1] = pu;
+                }
             }
         }
+        P = nb <= nwarp ? (sm.ut[nb - 1][0] >> 16) : 1;
         __syncthreads();
-#pragma unroll
-        for (int b = 0; b < kNBMax; b++) {
-            if (b < nb) {
-                const int j = j0 + b;
+        if (P > 1) {  // combine the parts of each record, fixed order
+            if (threadIdx.x < nb) {
+                const int b = threadIdx.x;
                 float g = 0.f, u = 0.f;
                 for (int p = 0; p < P; p++) {
                     g += sm.part[b][p][0];
                     u += sm.part[b][p][1];
                 }
-                const float av = (act == 1) ? fmaxf(g, 0.f) * u : g / (1.f + expf(-g)) * u;
-                down_any(tier_of(j), ring + offs[b], d, av, y);
+                sm.a_sm[b] = (act == 1) ? fmaxf(g, 0.f) * u : g / (1.f + expf(-g)) * u;
             }
+            __syncthreads();
         }
-        __syncthreads();  // the batch's records are consumed; part[] reusable
+        for (int b = 0; b < nb; b++) {
+            const int ds = dsc[j0 + b];
+            down_any(ds >> 24, ring + (ds & 0xffffff), d, sm.a_sm[b], y);
+        }
+        __syncthreads();  // the batch's records are consumed; a_sm/part reusable
         if (threadIdx.x == 0) {
             for (int b = 0; b < nb; b++) used -= sm.span[(j0 + b) % kNSlot];
             fence_proxy_async();
             issue_more(j0 + nb);
         }
-        j0 += nb;
     }
     float *out = partial + (int64_t)blockIdx.x * d + 8 * threadIdx.x;
     reinterpret_cast<float4 *>(out)[0] = make_float4(y[0], y[1], y[2], y[3]);
     reinterpret_cast<float4 *>(out)[1] = make_float4(y[4], y[5], y[6], y[7]);
+}
+
+struct SmemPtrs {
+    uint8_t *ring;
+    uint4 *xs;
+    int *loc, *dsc, *bst;
+};
+__device__ __forceinline__ SmemPtrs carve(uint8_t *smem) {
+    SmemPtrs p;
+    p.ring = smem;
+    p.xs = reinterpret_cast<uint4 *>(smem + kRing);
+    p.loc = reinterpret_cast<int *>(smem + kRing + kXsBytes);
+    p.dsc = p.loc + kMaxLocal;
+    p.bst = p.dsc + kMaxLocal;
+    return p;
 }
 
 // ---- list-driven FFN (API path: m2c_sparse_ffn_forward, LRU hits / misses) --------------
@@ -412,8 +471,7 @@ __global__ void __launch_bounds__(1024, 1)
           const int32_t *__restrict__ counts, float *__restrict__ partial) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ FfnShared sm;
-    uint8_t *ring = smem;
-    uint4 *xs = reinterpret_cast<uint4 *>(smem + kRingList);
+    const SmemPtrs S = carve(smem);
     if (threadIdx.x == 0) {
         for (int i = 0; i < kNSlot; i++) mbar_init(&sm.bars[i], 1);
         fence_mbar_init();
@@ -433,7 +491,7 @@ __global__ void __launch_bounds__(1024, 1)
         if (j < c2) return a.pool[1] + (int64_t)items[a.seg[1] + a1 + (j - c1)] * a.nb[1];
         return a.pool[2] + (int64_t)items[a.seg[2] + a2 + (j - c2)] * a.nb[2];
     };
-    ffn_loop<kRingList>(a, d, act, x, n_items, c1, c2, src, ring, xs, sm, partial);
+    ffn_loop(a, d, act, x, n_items, c1, c2, src, S.ring, S.xs, S.dsc, S.bst, sm, partial);
 }
 
 // ---- decode path: select (tier lists from scores + histogram) fused with the FFN ----------
@@ -442,14 +500,17 @@ __global__ void __launch_bounds__(1024, 1)
               float *__restrict__ partial) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ FfnShared sm;
-    uint8_t *ring = smem;
-    uint4 *xs = reinterpret_cast<uint4 *>(smem + kRingSel);           // [d/8], 16 KB reserved
-    int *loc = reinterpret_cast<int *>(smem + kRingSel + 16384);     // [kMaxLocal]
-    // the select scratch lives in the ring (unused until the records are requested)
-    int *hist = reinterpret_cast<int *>(smem);                       // [4096]
-    int *sub = hist + kHistBins;                                     // [3][2^sh]
+    const SmemPtrs S = carve(smem);
+    // select scratch inside the ring (unused until the records are requested):
+    // hist[4096] | sub[3][2^sh] | cnt[Q][3] | scores[F_r]
+    int *hist = reinterpret_cast<int *>(S.ring);
+    int *sub = hist + kHistBins;
+    const int nsub = 1 << s.sh;
+    const int Q = (s.F_r + 31) / 32;
+    int *cnt = sub + 3 * nsub;
+    int *sc = cnt + 3 * Q;
     const int T = blockDim.x, tid = threadIdx.x;
-    const int warp = tid >> 5, lane = tid & 31;
+    const int nwarp = T >> 5, warp = tid >> 5, lane = tid & 31;
     const int n0 = s.k16, n1 = s.k8, n2 = s.k - s.k16 - s.k8;
     if (tid == 0) {
         for (int i = 0; i < kNSlot; i++) mbar_init(&sm.bars[i], 1);
@@ -462,71 +523,67 @@ __global__ void __launch_bounds__(1024, 1)
     const int a0 = sm.rng[0], a1 = sm.rng[2], a2 = sm.rng[4];
     const int c1 = sm.rng[1] - a0, c2 = c1 + sm.rng[3] - a1, n_items = c2 + sm.rng[5] - a2;
     // speculative L2 prefetch of the records the previous token selected (hint only)
-    if (warp == 1 && s.prev_ids) {
+    if (warp == nwarp - 1 && s.prev_ids) {
         for (int j = lane; j < n_items; j += 32) {
             int t, id;
             if (j < c1) { t = 0; id = s.prev_ids[a0 + j]; }
             else if (j < c2) { t = 1; id = s.prev_ids[n0 + a1 + (j - c1)]; }
             else { t = 2; id = s.prev_ids[n0 + n1 + a2 + (j - c2)]; }
-            if (id >= 0 && id < s.F_r) {
-                const uint8_t *p = a.pool[t] + (int64_t)id * a.nb[t];
-                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(a.nb[t]) : "memory");
-            }
+            if (id >= 0 && id < s.F_r) prefetch_l2(a.pool[t] + (int64_t)id * a.nb[t], (uint32_t)a.nb[t]);
         }
     }
     griddep_launch();
     griddep_wait();
 
-    // ---- 1. histogram -> bin holding the target-th largest, for the three targets ----
-    const int tg[3] = {s.k16, s.k16 + s.k8, s.k};
+    // ---- 0. stage the scores (coalesced) and the histogram ----
+    for (int n = tid; n < s.F_r; n += T) sc[n] = s.scores[n] + s.smax;  // biased, >= 0
+    const int tg0 = s.k16, tg1 = s.k16 + s.k8, tg2 = s.k;
     const int BPT = (kHistBins + T - 1) / T;
     int lsum = 0;
     for (int i = 0; i < BPT; i++) {  // descending bins: thread t covers [4095 - t*BPT - i]
         const int b = kHistBins - 1 - (tid * BPT + i);
-        const int v = b >= 0 ? s.hist[b] : 0;
-        if (b >= 0) hist[b] = v;
+        if (b < 0) break;
+        const int v = s.hist[b];
+        hist[b] = v;
         lsum += v;
     }
+    // ---- 1. bin holding the target-th largest, for the three targets ----
     {
-        int vv[3] = {lsum, 0, 0}, ex[3], tot[3];
+        const int vv[3] = {lsum, 0, 0};
+        int ex[3], tot[3];
         block_scan3(vv, ex, tot, sm.scan);
         int cum = ex[0];
         for (int i = 0; i < BPT; i++) {
             const int b = kHistBins - 1 - (tid * BPT + i);
             if (b < 0) break;
             const int v = hist[b];
-#pragma unroll
-            for (int t = 0; t < 3; t++)
-                if (tg[t] > 0 && cum < tg[t] && cum + v >= tg[t]) {
-                    sm.selv[t] = b;          // bin
-                    sm.selv[3 + t] = cum;    // elements above the bin
-                }
+            if (tg0 > 0 && cum < tg0 && cum + v >= tg0) { sm.selv[0] = b; sm.selv[3] = cum; }
+            if (tg1 > 0 && cum < tg1 && cum + v >= tg1) { sm.selv[1] = b; sm.selv[4] = cum; }
+            if (tg2 > 0 && cum < tg2 && cum + v >= tg2) { sm.selv[2] = b; sm.selv[5] = cum; }
             cum += v;
         }
     }
-    const int nsub = 1 << s.sh;
     for (int i = tid; i < 3 * nsub; i += T) sub[i] = 0;
     __syncthreads();
-    int bin[3], need[3];
-#pragma unroll
-    for (int t = 0; t < 3; t++) {
-        bin[t] = tg[t] > 0 ? sm.selv[t] : -1;
-        need[t] = tg[t] > 0 ? tg[t] - sm.selv[3 + t] : 0;
-    }
+    const int bin0 = tg0 > 0 ? sm.selv[0] : -1, bin1 = tg1 > 0 ? sm.selv[1] : -1,
+              bin2 = tg2 > 0 ? sm.selv[2] : -1;
     // ---- 2. second level: exact values inside the chosen bins ----
     for (int n = tid; n < s.F_r; n += T) {
-        const int v = s.scores[n] + s.smax;
-        const int b = v >> s.sh;
-#pragma unroll
-        for (int t = 0; t < 3; t++)
-            if (b == bin[t]) atomicAdd(&sub[t * nsub + (v & (nsub - 1))], 1);
+        const int v = sc[n];
+        const int b = v >> s.sh, lo = v & (nsub - 1);
+        if (b == bin0) atomicAdd(&sub[lo], 1);
+        if (b == bin1) atomicAdd(&sub[nsub + lo], 1);
+        if (b == bin2) atomicAdd(&sub[2 * nsub + lo], 1);
     }
     __syncthreads();
-    if (warp < 3 && tg[warp] > 0) {  // warp t scans sub[t] from the top for need[t]
-        const int t = warp;
+    for (int t = warp; t < 3; t += nwarp) {  // warp t scans sub[t] from the top
+        const int tg = t == 0 ? tg0 : (t == 1 ? tg1 : tg2);
+        if (tg <= 0) continue;
+        const int need = tg - sm.selv[3 + t], bin = sm.selv[t];
         const int per = nsub / 32;
+        const int *st = sub + t * nsub;
         int loc_sum = 0;
-        for (int i = 0; i < per; i++) loc_sum += sub[t * nsub + nsub - 1 - (lane * per + i)];
+        for (int i = 0; i < per; i++) loc_sum += st[nsub - 1 - (lane * per + i)];
         int inc = loc_sum;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -534,14 +591,15 @@ __global__ void __launch_bounds__(1024, 1)
             if (lane >= o) inc += y2;
         }
         const int excl = inc - loc_sum;
-        if (excl < need[t] && inc >= need[t]) {
+        if (excl < need && inc >= need) {
             int cum = excl;
             for (int i = 0; i < per; i++) {
                 const int c = nsub - 1 - (lane * per + i);
-                const int v = sub[t * nsub + c];
-                if (cum + v >= need[t]) {
-                    sm.selv[6 + t] = (bin[t] << s.sh) | c;  // exact biased value V_t
-                    sm.selv[9 + t] = need[t] - cum;         // how many equal to V_t are in
+                const int v = st[c];
+                if (cum + v >= need) {
+                    sm.selv[6 + t] = (bin << s.sh) | c;  // exact biased value V_t
+                    sm.selv[9 + t] = need - cum;         // how many equal to V_t are in
+                    sm.selv[12 + t] = v;                 // how many equal to V_t exist
                     break;
                 }
                 cum += v;
@@ -549,86 +607,96 @@ __global__ void __launch_bounds__(1024, 1)
         }
     }
     __syncthreads();
-    int V[3], R[3];
-#pragma unroll
-    for (int t = 0; t < 3; t++) {
-        V[t] = tg[t] > 0 ? sm.selv[6 + t] : 0x7fffffff;
-        R[t] = tg[t] > 0 ? sm.selv[9 + t] : 0;
-    }
-    // ---- 3. classify in id order, compact; keep this CTA's records, CTA 0 writes the lists ----
-    const int CH = (s.F_r + T - 1) / T;
-    const int i0 = min(s.F_r, tid * CH), i1 = min(s.F_r, i0 + CH);
-    int eqv[3] = {0, 0, 0}, eqx[3], tot[3];
-    for (int n = i0; n < i1; n++) {
-        const int v = s.scores[n] + s.smax;
-#pragma unroll
-        for (int t = 0; t < 3; t++) eqv[t] += (v == V[t]);
-    }
-    block_scan3(eqv, eqx, tot, sm.scan);
-    int cnt[3] = {0, 0, 0};
-    for (int n = i0; n < i1; n++) {
-        const int v = s.scores[n] + s.smax;
-        int tr = -1;
-#pragma unroll
-        for (int t = 2; t >= 0; t--) {
-            bool in = v > V[t];
-            if (v == V[t]) in = (eqx[t]++ < R[t]);
-            if (in) tr = t;
+    const int V0 = tg0 > 0 ? sm.selv[6] : 0x7fffffff, V1 = tg1 > 0 ? sm.selv[7] : 0x7fffffff,
+              V2 = tg2 > 0 ? sm.selv[8] : 0x7fffffff;
+    const int R0 = tg0 > 0 ? sm.selv[9] : 0, R1 = tg1 > 0 ? sm.selv[10] : 0, R2 = tg2 > 0 ? sm.selv[11] : 0;
+    const bool tie = (tg0 > 0 && R0 < sm.selv[12]) || (tg1 > 0 && R1 < sm.selv[13]) ||
+                     (tg2 > 0 && R2 < sm.selv[14]);
+    const unsigned lt_mask = (1u << lane) - 1u;
+    // ---- 3a. (only with partial ties) equal-key ranks in id order: per-chunk counts ----
+    if (tie) {
+        for (int q = warp; q < Q; q += nwarp) {
+            const int n = 32 * q + lane;
+            const int v = n < s.F_r ? sc[n] : -1;
+            const unsigned e0 = __ballot_sync(0xffffffffu, v == V0), e1 = __ballot_sync(0xffffffffu, v == V1),
+                           e2 = __ballot_sync(0xffffffffu, v == V2);
+            if (lane == 0) {
+                cnt[3 * q] = __popc(e0);
+                cnt[3 * q + 1] = __popc(e1);
+                cnt[3 * q + 2] = __popc(e2);
+            }
         }
-        if (tr >= 0) cnt[tr]++;
+        __syncthreads();
+        scan_chunks(cnt, Q, sm.scan);
     }
-    int pos[3], tot2[3];
-    block_scan3(cnt, pos, tot2, sm.scan);
-    // re-walk (recomputing the equal-key ranks) to emit positions
-    eqx[0] = eqx[0] - eqv[0];
-    eqx[1] = eqx[1] - eqv[1];
-    eqx[2] = eqx[2] - eqv[2];
-    const int segs[3] = {0, n0, n0 + n1};
-    const int lo_t[3] = {a0, a1, a2}, hi_t[3] = {a0 + c1, a1 + (c2 - c1), a2 + (n_items - c2)};
-    const int lb_t[3] = {0, c1, c2};
-    for (int n = i0; n < i1; n++) {
-        const int v = s.scores[n] + s.smax;
-        int tr = -1;
-#pragma unroll
-        for (int t = 2; t >= 0; t--) {
-            bool in = v > V[t];
-            if (v == V[t]) in = (eqx[t]++ < R[t]);
-            if (in) tr = t;
+    // tier of element n (lane of chunk q); `eq` holds the chunk's equal-key prefix (if tie)
+    auto tier_at = [&](int v, int q) -> int {
+        bool in0 = v > V0, in1 = v > V1, in2 = v > V2;
+        if (tie) {
+            const unsigned e0 = __ballot_sync(0xffffffffu, v == V0), e1 = __ballot_sync(0xffffffffu, v == V1),
+                           e2 = __ballot_sync(0xffffffffu, v == V2);
+            if (v == V0) in0 = cnt[3 * q] + __popc(e0 & lt_mask) < R0;
+            if (v == V1) in1 = cnt[3 * q + 1] + __popc(e1 & lt_mask) < R1;
+            if (v == V2) in2 = cnt[3 * q + 2] + __popc(e2 & lt_mask) < R2;
+        } else {
+            in0 = in0 || v == V0;
+            in1 = in1 || v == V1;
+            in2 = in2 || v == V2;
         }
+        return in0 ? 0 : (in1 ? 1 : (in2 ? 2 : -1));
+    };
+    // ---- 3b. tier membership per 32-id chunk (ballots) -> positions by a scan over chunks ----
+    int *tcnt = tie ? sc + s.F_r : cnt;  // keep the eq prefixes if needed: second table after sc
+    for (int q = warp; q < Q; q += nwarp) {
+        const int n = 32 * q + lane;
+        const int v = n < s.F_r ? sc[n] : -1;
+        const int tr = tier_at(v, q);
+        const unsigned m0 = __ballot_sync(0xffffffffu, tr == 0), m1 = __ballot_sync(0xffffffffu, tr == 1),
+                       m2 = __ballot_sync(0xffffffffu, tr == 2);
+        if (lane == 0) {
+            tcnt[3 * q] = __popc(m0);
+            tcnt[3 * q + 1] = __popc(m1);
+            tcnt[3 * q + 2] = __popc(m2);
+        }
+    }
+    __syncthreads();
+    scan_chunks(tcnt, Q, sm.scan);
+    // ---- 3c. emit: this CTA's records into loc[], CTA 0 the whole lists ----
+    const int lo0 = a0, hi0 = a0 + c1, lo1 = a1, hi1 = a1 + (c2 - c1), lo2 = a2, hi2 = a2 + (n_items - c2);
+    for (int q = warp; q < Q; q += nwarp) {
+        const int b0 = tcnt[3 * q], b1 = tcnt[3 * q + 1], b2 = tcnt[3 * q + 2];
+        const int e0n = q + 1 < Q ? tcnt[3 * q + 3] : s.k16, e1n = q + 1 < Q ? tcnt[3 * q + 4] : s.k8,
+                  e2n = q + 1 < Q ? tcnt[3 * q + 5] : n2;
+        const bool mine = (b0 < hi0 && e0n > lo0) || (b1 < hi1 && e1n > lo1) || (b2 < hi2 && e2n > lo2);
+        if (!mine && !(blockIdx.x == 0 && s.out_ids)) continue;
+        const int n = 32 * q + lane;
+        const int v = n < s.F_r ? sc[n] : -1;
+        const int tr = tier_at(v, q);
+        const unsigned m0 = __ballot_sync(0xffffffffu, tr == 0), m1 = __ballot_sync(0xffffffffu, tr == 1),
+                       m2 = __ballot_sync(0xffffffffu, tr == 2);
         if (tr >= 0) {
-            int p = 0, lo = 0, hi = 0, lb = 0, sg = 0;
-#pragma unroll
-            for (int t = 0; t < 3; t++)
-                if (t == tr) {
-                    p = pos[t]++;
-                    lo = lo_t[t];
-                    hi = hi_t[t];
-                    lb = lb_t[t];
-                    sg = segs[t];
-                }
-            if (p >= lo && p < hi) loc[lb + p - lo] = n;
-            if (blockIdx.x == 0 && s.out_ids) s.out_ids[sg + p] = n;
+            const unsigned m = tr == 0 ? m0 : (tr == 1 ? m1 : m2);
+            const int p = (tr == 0 ? b0 : (tr == 1 ? b1 : b2)) + __popc(m & lt_mask);
+            const int lo = tr == 0 ? lo0 : (tr == 1 ? lo1 : lo2), hi = tr == 0 ? hi0 : (tr == 1 ? hi1 : hi2);
+            const int lb = tr == 0 ? 0 : (tr == 1 ? c1 : c2);
+            if (p >= lo && p < hi) S.loc[lb + p - lo] = n;
+            if (blockIdx.x == 0 && s.out_ids) s.out_ids[(tr == 0 ? 0 : (tr == 1 ? n0 : n0 + n1)) + p] = n;
         }
     }
     __syncthreads();
     auto src = [&](int j) -> const uint8_t * {
         const int t = j < c1 ? 0 : (j < c2 ? 1 : 2);
-        return a.pool[t] + (int64_t)loc[j] * a.nb[t];
+        return a.pool[t] + (int64_t)S.loc[j] * a.nb[t];
     };
-    ffn_loop<kRingSel>(a, d, act, x, n_items, c1, c2, src, ring, xs, sm, partial);
+    ffn_loop(a, d, act, x, n_items, c1, c2, src, S.ring, S.xs, S.dsc, S.bst, sm, partial);
 }
 
 }  // namespace
 
-static size_t sel_smem(int sh) {
-    (void)sh;  // hist + 3 sub-histograms (<= 64 KB) live inside the ring
-    return (size_t)kRingSel + 16384 + 4 * (size_t)kMaxLocal;
-}
-
 cudaError_t init_ffn_attrs() {
-    cudaError_t e = cudaFuncSetAttribute(k_ffn, cudaFuncAttributeMaxDynamicSharedMemorySize, kRingList + 16384);
+    cudaError_t e = cudaFuncSetAttribute(k_ffn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
     if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(k_ffn_sel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sel_smem(12));
+        e = cudaFuncSetAttribute(k_ffn_sel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
     return e;
 }
 
@@ -650,21 +718,23 @@ cudaError_t launch_ffn(m2c_ctx *c, const LayerState &L, const __half *x, const i
     const int d = c->desc.d_model;
     FfnArgs a;
     fill_args(c, L, p, a);
-    cudaError_t e = launch_k(k_ffn, dim3(c->G), dim3(d / 8), (size_t)kRingList + 2 * (size_t)d, st, a, d,
-                             c->desc.act, x, items, counts, partial);
+    cudaError_t e = launch_k(k_ffn, dim3(c->G), dim3(d / 8), kSmemBytes, st, a, d, c->desc.act, x,
+                             items, counts, partial);
     c->launch_counter++;
     return e;
 }
 
 bool ffn_sel_supported(m2c_ctx *c, const m2c_tier_plan &p) {
-    // every CTA's share must fit the local item list; sh <= 12
+    // every CTA's share must fit the local item list; select scratch must fit the ring
     FfnArgs a;
     LayerState dummy;
     fill_args(c, dummy, p, a);
     const long long W = (long long)p.k_fp16 * a.wt[0] + (long long)p.k_int8 * a.wt[1] + (long long)p.k_int4 * a.wt[2];
     const long long per = W / c->G + 1;
     const int wmin = a.wt[2] < a.wt[1] ? (a.wt[2] < a.wt[0] ? a.wt[2] : a.wt[0]) : (a.wt[1] < a.wt[0] ? a.wt[1] : a.wt[0]);
-    return per / wmin + 3 <= kMaxLocal && c->sel_sh <= 12;
+    const long long Q = (c->F_r + 31) / 32;
+    const long long scratch = 4LL * (kHistBins + 3 * (1LL << c->sel_sh) + 6 * Q + 2LL * c->F_r);
+    return per / wmin + 3 <= kMaxLocal && c->sel_sh <= 12 && scratch <= kRing;
 }
 
 cudaError_t launch_ffn_sel(m2c_ctx *c, const LayerState &L, const __half *x, const int32_t *scores,
@@ -684,8 +754,8 @@ cudaError_t launch_ffn_sel(m2c_ctx *c, const LayerState &L, const __half *x, con
     s.k8 = p.k_int8;
     s.smax = c->sel_smax;
     s.sh = c->sel_sh;
-    cudaError_t e = launch_k(k_ffn_sel, dim3(c->G), dim3(d / 8), sel_smem(c->sel_sh), st, a, s, d,
-                             c->desc.act, x, partial);
+    cudaError_t e = launch_k(k_ffn_sel, dim3(c->G), dim3(d / 8), kSmemBytes, st, a, s, d, c->desc.act,
+                             x, partial);
     c->launch_counter++;
     return e;
 }
