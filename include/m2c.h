@@ -182,9 +182,10 @@ m2c_status m2c_decode_step(m2c_ctx *ctx, void *x_inout, int64_t step);
 /* Disables (0) or enables (1, default) CUDA-graph capture of m2c_decode_step. */
 m2c_status m2c_set_graph(m2c_ctx *ctx, int32_t enable);
 
-/* Resident layers in m2c_decode_step: 1 (default) = top-k/tier split fused into the FFN kernel
- * (predictor -> select+FFN -> reduce, with an L2 prefetch of the previous token's selection);
- * 0 = the separate m2c_predict_rank select kernel.  Results are identical (tests). */
+/* Resident layers in m2c_decode_step: 1 (default) = the predictor kernel also prefetches into
+ * L2 the records the previous token selected for the layer (adjacent tokens share ~80% of
+ * their active neurons), so most of the FFN's reads hit L2; 0 = no prefetch.  A hint
+ * only: results are bit-identical either way (tests). */
 m2c_status m2c_set_fused(m2c_ctx *ctx, int32_t enable);
 
 /* Phase timing (CUDA events recorded inside the decode graph, on the compute stream):

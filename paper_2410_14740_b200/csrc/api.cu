@@ -23,8 +23,6 @@ m2c_status cuda_fail(cudaError_t e, const char *what) {
     return M2C_ERR_CUDA;
 }
 
-size_t select_smem_bytes(int F_r, int P2);
-size_t select_smem_limit();
 size_t lru_smem_bytes(int P2, int maxcnt);
 
 // ---- NCCL, loaded at run time (no link-time dependency) ----
@@ -148,20 +146,20 @@ static cudaError_t enqueue_layer(m2c_ctx *c, int l, __half *x) {
     const m2c_tier_plan &p = c->plan;
     cudaStream_t st = c->compute;
     cudaError_t e;
-    // resident layers: predictor (+ score histogram) -> fused select+FFN -> reduce (4 kernels)
-    const bool fused = L.mode == 0 && c->use_fused && ffn_sel_supported(c, p);
+    // resident: predictor (+ score histogram, + L2 prefetch of the previous token's records)
+    // -> multi-CTA select writing this layer's tier lists -> FFN -> reduce (PDL-chained).
+    // The lists of layer l persist to the next token as its prefetch hint.
     int32_t *lists = c->prev_ids + (size_t)l * (p.k > 0 ? p.k : 1);
+    const bool prefetch = L.mode == 0 && c->use_fused;
+    int32_t *ids = L.mode == 0 ? lists : c->ws.tier_ids;
     if ((e = mark(c, l, 0))) return e;
-    if ((e = launch_predict(c, L, x, c->ws.s, fused ? c->ghist : nullptr, st))) return e;
+    if ((e = launch_predict(c, L, x, c->ws.s, c->ghist, prefetch ? lists : nullptr, st))) return e;
     if ((e = mark(c, l, 1))) return e;
-    if (!fused && (e = launch_select(c, c->ws.s, p, nullptr, nullptr, c->ws.tier_ids, st))) return e;
+    if ((e = launch_select(c, c->ws.s, c->ghist, p, nullptr, nullptr, ids, st))) return e;
     if ((e = mark(c, l, 2))) return e;
     int np = c->G;
-    if (fused) {
-        e = launch_ffn_sel(c, L, x, c->ws.s, c->ghist, lists, lists, p, c->ws.partial, st);
-        if (e) return e;
-    } else if (L.mode == 0) {
-        e = launch_ffn(c, L, x, c->ws.tier_ids, c->ws.counts, p, c->ws.partial, st);
+    if (L.mode == 0) {
+        e = launch_ffn(c, L, x, ids, c->ws.counts, p, c->ws.partial, st);
         if (e) return e;
     } else {
         e = launch_lru(c, L, step_ptr(c), c->ws.tier_ids, p, c->ws.slots, c->ws.hit_bits, nullptr, nullptr, st);
@@ -180,17 +178,14 @@ static cudaError_t enqueue_layer(m2c_ctx *c, int l, __half *x) {
     }
     if ((e = mark(c, l, 3))) return e;
     if (c->nranks > 1) {
-        if ((e = launch_reduce(c, np, c->ws.partial, x, c->ws.y32, nullptr, nullptr,
-                               fused ? c->ghist : nullptr, st)))
+        if ((e = launch_reduce(c, np, c->ws.partial, x, c->ws.y32, nullptr, nullptr, nullptr, st)))
             return e;
         int r = c->nccl->allReduce(c->ws.y32, c->ws.y32, (size_t)c->desc.d_model, 7 /*f32*/,
                                    0 /*sum*/, c->comm, st);
         if (r != 0) return cudaErrorUnknown;
         if ((e = launch_finalize(c, c->ws.y32, x, nullptr, x, st))) return e;
     } else {
-        if ((e = launch_reduce(c, np, c->ws.partial, x, nullptr, nullptr, x,
-                               fused ? c->ghist : nullptr, st)))
-            return e;
+        if ((e = launch_reduce(c, np, c->ws.partial, x, nullptr, nullptr, x, nullptr, st))) return e;
     }
     return mark(c, l, 4);
 }
@@ -317,7 +312,8 @@ m2c_status m2c_create(const m2c_model_desc *desc, int32_t device, m2c_stream_t c
                  o_mid = take(4 * (size_t)F_r), o_cnt = take(4 * 16),
                  o_part = take(4 * (size_t)2 * c->G * d), o_y = take(4 * (size_t)d),
                  o_x = take(2 * (size_t)d), o_stats = take(8 * 6), o_err = take(4),
-                 o_hist = take(4 * 4096),
+                 o_hist = take(4 * 4096), o_sst = take(8 * (size_t)select_blocks(F_r)),
+                 o_sdone = take(4), o_sepoch = take(4),
                  o_prev = take(4 * (size_t)desc->n_layers * (plan->k > 0 ? plan->k : 1));
     // score histogram geometry: |s| <= 127^2 r, bins of 2^sh over [0, 2 smax] (4096 bins)
     c->sel_smax = 16129 * desc->pred_rank;
@@ -350,6 +346,9 @@ m2c_status m2c_create(const m2c_model_desc *desc, int32_t device, m2c_stream_t c
     c->ws.err = (uint32_t *)(b + o_err);
     c->ghist = (int *)(b + o_hist);
     c->prev_ids = (int32_t *)(b + o_prev);
+    c->sel_status = (unsigned long long *)(b + o_sst);
+    c->sel_done = (int *)(b + o_sdone);
+    c->sel_epoch = (int *)(b + o_sepoch);
     e = cudaMemset(c->ws_mem, 0, off);
     if (e == cudaSuccess)  // no previous selection yet: -1 disables the prefetch hint
         e = cudaMemset(c->prev_ids, 0xff, 4 * (size_t)desc->n_layers * (plan->k > 0 ? plan->k : 1));
@@ -471,17 +470,12 @@ m2c_status m2c_predict_rank(m2c_ctx *c, int32_t layer, const void *x, const m2c_
     m2c_status st = check_plan(plan, c->F_r);
     if (st) return st;
     if (!al16(x)) return fail(M2C_ERR_INVALID_ARG, "x must be 16-B aligned");
-    if (rank_list && plan->k > 0) {
-        int P2 = 2;
-        while (P2 < plan->k) P2 <<= 1;
-        if (select_smem_bytes(c->F_r, P2) > select_smem_limit())
-            return fail(M2C_ERR_CAPACITY, "rank_list: k too large for the on-chip sort");
-    } else if (select_smem_bytes(c->F_r, 0) > select_smem_limit()) {
-        return fail(M2C_ERR_CAPACITY, "F_r too large for the single-CTA select");
-    }
+    if (rank_list && plan->k > 16384)
+        return fail(M2C_ERR_CAPACITY, "rank_list: k too large for the on-chip sort (<= 16384)");
     int32_t *s = scores ? scores : c->ws.s;
-    M2C_CUDA(launch_predict(c, c->layers[layer], (const __half *)x, s, nullptr, c->compute));
-    M2C_CUDA(launch_select(c, s, *plan, rank_list, tier_of, tier_ids, c->compute));
+    // the select kernel consumes and clears the score histogram the predictor builds
+    M2C_CUDA(launch_predict(c, c->layers[layer], (const __half *)x, s, c->ghist, nullptr, c->compute));
+    M2C_CUDA(launch_select(c, s, c->ghist, *plan, rank_list, tier_of, tier_ids, c->compute));
     return M2C_OK;
 }
 
@@ -642,8 +636,6 @@ m2c_status m2c_decode_step(m2c_ctx *c, void *x_inout, int64_t step) {
                 return fail(M2C_ERR_STATE, "decode_step: step must strictly increase");
         }
     }
-    if (select_smem_bytes(c->F_r, 0) > select_smem_limit())
-        return fail(M2C_ERR_CAPACITY, "F_r too large for the single-CTA select");
     cudaStream_t cs = c->compute;
     if (any_lru) {
         const int32_t st32 = (int32_t)step;  // pageable source: staged before return

@@ -1,5 +1,4 @@
-// k_ffn.cu -- a6: fused dequant-GEMV (gate, up) -> act(g) * u -> sparse down-projection,
-// and (decode path) the fused top-k/tier split in front of it.
+// k_ffn.cu -- a6: fused dequant-GEMV (gate, up) -> act(g) * u -> sparse down-projection.
 //
 // Paper: a neuron is a row of the first FFN matrices and the matching column of the next
 // (P:58); only the active neurons are computed; the cache unit memory "can be
@@ -23,12 +22,6 @@
 //    (q - z) by fp16 x with an exact product and fp32 accumulation.  Per 128-group
 //    s * sum (q - z) x (R5).
 //  * The per-CTA partial y goes to a [G][d] fp32 buffer reduced in a fixed order by k_reduce.
-//  * k_ffn_sel (decode path) first derives the FP16/INT8/INT4 tier lists itself, redundantly
-//    in every CTA, from the predictor scores and the 4096-bin score histogram k_pred_s left in
-//    global memory: exact thresholds via a second-level histogram, ties by ascending id,
-//    then warp-ballot classification of 32-id chunks and a block scan over chunks.  Before
-//    waiting on its predecessor it prefetches into L2 the records the previous token selected
-//    for this layer (~80% of them recur).
 #include "m2c_internal.cuh"
 
 namespace m2c {
@@ -37,7 +30,6 @@ namespace {
 constexpr int kNBMax = 16;   // records per batch
 constexpr int kNSlot = 32;   // mbarriers (>= records in flight)
 constexpr int kRing = 192 * 1024;
-constexpr int kHistBins = 4096;
 constexpr int kMaxLocal = 1024;  // records one CTA may own
 constexpr int kXsBytes = 16384;  // x (fp16, d <= 8192)
 // dynamic smem: ring | xs | loc[kMaxLocal] | dsc[kMaxLocal] | bst[kMaxLocal + 1]
@@ -48,14 +40,6 @@ struct FfnArgs {
     int nb[3];     // record bytes per tier
     int seg[3];    // tier segment offsets in the item lists
     int wt[3];     // balancing weight per record (bytes + lambda * 3d), in 16-B units
-};
-
-struct SelArgs {
-    const int32_t *scores;  // [F_r]
-    const int32_t *hist;    // [4096] histogram of (s + smax) >> sh
-    int32_t *out_ids;       // [k] tier lists written by CTA 0 (also next token's prefetch hint)
-    const int32_t *prev_ids;  // [k] previous token's lists for this layer (prefetch hint)
-    int F_r, k, k16, k8, smax, sh;
 };
 
 __device__ __forceinline__ void hfma32(float &acc, uint32_t a, uint32_t b, int ha, int hb) {
@@ -233,63 +217,6 @@ __device__ __forceinline__ void down_any(int tier, const uint8_t *rec, int d, fl
     if (tier == 0) down_t<0>(rec, d, a, y);
     else if (tier == 1) down_t<1>(rec, d, a, y);
     else down_t<2>(rec, d, a, y);
-}
-
-// exclusive block scan of 3 ints per thread; blockDim.x multiple of 32, <= 1024
-__device__ __forceinline__ void block_scan3(const int v[3], int ex[3], int tot[3], int *sm /*[3][32]*/) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    int inc[3];
-#pragma unroll
-    for (int t = 0; t < 3; t++) {
-        int x = v[t];
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
-        }
-        inc[t] = x;
-        if (lane == 31) sm[t * 32 + warp] = x;
-    }
-    __syncthreads();
-    if (warp == 0) {
-#pragma unroll
-        for (int t = 0; t < 3; t++) {
-            int x = lane < nw ? sm[t * 32 + lane] : 0;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int y = __shfl_up_sync(0xffffffffu, x, o);
-                if (lane >= o) x += y;
-            }
-            sm[t * 32 + lane] = x;
-        }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int t = 0; t < 3; t++) {
-        ex[t] = (warp ? sm[t * 32 + warp - 1] : 0) + inc[t] - v[t];
-        tot[t] = sm[t * 32 + nw - 1];
-    }
-    __syncthreads();
-}
-
-// in-place exclusive scan of cnt[q][3] over q < Q (smem), all threads
-__device__ __forceinline__ void scan_chunks(int *cnt, int Q, int *sm) {
-    const int T = blockDim.x;
-    const int per = (Q + T - 1) / T;
-    const int q0 = min(Q, (int)threadIdx.x * per), q1 = min(Q, q0 + per);
-    int v[3] = {0, 0, 0}, ex[3], tot[3];
-    for (int q = q0; q < q1; q++)
-#pragma unroll
-        for (int t = 0; t < 3; t++) v[t] += cnt[3 * q + t];
-    block_scan3(v, ex, tot, sm);
-    for (int q = q0; q < q1; q++)
-#pragma unroll
-        for (int t = 0; t < 3; t++) {
-            const int c = cnt[3 * q + t];
-            cnt[3 * q + t] = ex[t];
-            ex[t] += c;
-        }
-    __syncthreads();
 }
 
 // this CTA's share [i0_t, i1_t) of each tier list, balanced on wt (computed by one thread)
@@ -494,210 +421,10 @@ __global__ void __launch_bounds__(1024, 1)
     ffn_loop(a, d, act, x, n_items, c1, c2, src, S.ring, S.xs, S.dsc, S.bst, sm, partial);
 }
 
-// ---- decode path: select (tier lists from scores + histogram) fused with the FFN ----------
-__global__ void __launch_bounds__(1024, 1)
-    k_ffn_sel(FfnArgs a, SelArgs s, int d, int act, const __half *__restrict__ x,
-              float *__restrict__ partial) {
-    extern __shared__ __align__(128) uint8_t smem[];
-    __shared__ FfnShared sm;
-    const SmemPtrs S = carve(smem);
-    // select scratch inside the ring (unused until the records are requested):
-    // hist[4096] | sub[3][2^sh] | cnt[Q][3] | scores[F_r]
-    int *hist = reinterpret_cast<int *>(S.ring);
-    int *sub = hist + kHistBins;
-    const int nsub = 1 << s.sh;
-    const int Q = (s.F_r + 31) / 32;
-    int *cnt = sub + 3 * nsub;
-    int *sc = cnt + 3 * Q;
-    const int T = blockDim.x, tid = threadIdx.x;
-    const int nwarp = T >> 5, warp = tid >> 5, lane = tid & 31;
-    const int n0 = s.k16, n1 = s.k8, n2 = s.k - s.k16 - s.k8;
-    if (tid == 0) {
-        for (int i = 0; i < kNSlot; i++) mbar_init(&sm.bars[i], 1);
-        fence_mbar_init();
-        int r[6];
-        cta_ranges(a, n0, n1, n2, blockIdx.x, gridDim.x, r);
-        for (int i = 0; i < 6; i++) sm.rng[i] = r[i];
-    }
-    __syncthreads();
-    const int a0 = sm.rng[0], a1 = sm.rng[2], a2 = sm.rng[4];
-    const int c1 = sm.rng[1] - a0, c2 = c1 + sm.rng[3] - a1, n_items = c2 + sm.rng[5] - a2;
-    // speculative L2 prefetch of the records the previous token selected (hint only)
-    if (warp == nwarp - 1 && s.prev_ids) {
-        for (int j = lane; j < n_items; j += 32) {
-            int t, id;
-            if (j < c1) { t = 0; id = s.prev_ids[a0 + j]; }
-            else if (j < c2) { t = 1; id = s.prev_ids[n0 + a1 + (j - c1)]; }
-            else { t = 2; id = s.prev_ids[n0 + n1 + a2 + (j - c2)]; }
-            if (id >= 0 && id < s.F_r) prefetch_l2(a.pool[t] + (int64_t)id * a.nb[t], (uint32_t)a.nb[t]);
-        }
-    }
-    griddep_launch();
-    griddep_wait();
-
-    // ---- 0. stage the scores (coalesced) and the histogram ----
-    for (int n = tid; n < s.F_r; n += T) sc[n] = s.scores[n] + s.smax;  // biased, >= 0
-    const int tg0 = s.k16, tg1 = s.k16 + s.k8, tg2 = s.k;
-    const int BPT = (kHistBins + T - 1) / T;
-    int lsum = 0;
-    for (int i = 0; i < BPT; i++) {  // descending bins: thread t covers [4095 - t*BPT - i]
-        const int b = kHistBins - 1 - (tid * BPT + i);
-        if (b < 0) break;
-        const int v = s.hist[b];
-        hist[b] = v;
-        lsum += v;
-    }
-    // ---- 1. bin holding the target-th largest, for the three targets ----
-    {
-        const int vv[3] = {lsum, 0, 0};
-        int ex[3], tot[3];
-        block_scan3(vv, ex, tot, sm.scan);
-        int cum = ex[0];
-        for (int i = 0; i < BPT; i++) {
-            const int b = kHistBins - 1 - (tid * BPT + i);
-            if (b < 0) break;
-            const int v = hist[b];
-            if (tg0 > 0 && cum < tg0 && cum + v >= tg0) { sm.selv[0] = b; sm.selv[3] = cum; }
-            if (tg1 > 0 && cum < tg1 && cum + v >= tg1) { sm.selv[1] = b; sm.selv[4] = cum; }
-            if (tg2 > 0 && cum < tg2 && cum + v >= tg2) { sm.selv[2] = b; sm.selv[5] = cum; }
-            cum += v;
-        }
-    }
-    for (int i = tid; i < 3 * nsub; i += T) sub[i] = 0;
-    __syncthreads();
-    const int bin0 = tg0 > 0 ? sm.selv[0] : -1, bin1 = tg1 > 0 ? sm.selv[1] : -1,
-              bin2 = tg2 > 0 ? sm.selv[2] : -1;
-    // ---- 2. second level: exact values inside the chosen bins ----
-    for (int n = tid; n < s.F_r; n += T) {
-        const int v = sc[n];
-        const int b = v >> s.sh, lo = v & (nsub - 1);
-        if (b == bin0) atomicAdd(&sub[lo], 1);
-        if (b == bin1) atomicAdd(&sub[nsub + lo], 1);
-        if (b == bin2) atomicAdd(&sub[2 * nsub + lo], 1);
-    }
-    __syncthreads();
-    for (int t = warp; t < 3; t += nwarp) {  // warp t scans sub[t] from the top
-        const int tg = t == 0 ? tg0 : (t == 1 ? tg1 : tg2);
-        if (tg <= 0) continue;
-        const int need = tg - sm.selv[3 + t], bin = sm.selv[t];
-        const int per = nsub / 32;
-        const int *st = sub + t * nsub;
-        int loc_sum = 0;
-        for (int i = 0; i < per; i++) loc_sum += st[nsub - 1 - (lane * per + i)];
-        int inc = loc_sum;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y2 = __shfl_up_sync(0xffffffffu, inc, o);
-            if (lane >= o) inc += y2;
-        }
-        const int excl = inc - loc_sum;
-        if (excl < need && inc >= need) {
-            int cum = excl;
-            for (int i = 0; i < per; i++) {
-                const int c = nsub - 1 - (lane * per + i);
-                const int v = st[c];
-                if (cum + v >= need) {
-                    sm.selv[6 + t] = (bin << s.sh) | c;  // exact biased value V_t
-                    sm.selv[9 + t] = need - cum;         // how many equal to V_t are in
-                    sm.selv[12 + t] = v;                 // how many equal to V_t exist
-                    break;
-                }
-                cum += v;
-            }
-        }
-    }
-    __syncthreads();
-    const int V0 = tg0 > 0 ? sm.selv[6] : 0x7fffffff, V1 = tg1 > 0 ? sm.selv[7] : 0x7fffffff,
-              V2 = tg2 > 0 ? sm.selv[8] : 0x7fffffff;
-    const int R0 = tg0 > 0 ? sm.selv[9] : 0, R1 = tg1 > 0 ? sm.selv[10] : 0, R2 = tg2 > 0 ? sm.selv[11] : 0;
-    const bool tie = (tg0 > 0 && R0 < sm.selv[12]) || (tg1 > 0 && R1 < sm.selv[13]) ||
-                     (tg2 > 0 && R2 < sm.selv[14]);
-    const unsigned lt_mask = (1u << lane) - 1u;
-    // ---- 3a. (only with partial ties) equal-key ranks in id order: per-chunk counts ----
-    if (tie) {
-        for (int q = warp; q < Q; q += nwarp) {
-            const int n = 32 * q + lane;
-            const int v = n < s.F_r ? sc[n] : -1;
-            const unsigned e0 = __ballot_sync(0xffffffffu, v == V0), e1 = __ballot_sync(0xffffffffu, v == V1),
-                           e2 = __ballot_sync(0xffffffffu, v == V2);
-            if (lane == 0) {
-                cnt[3 * q] = __popc(e0);
-                cnt[3 * q + 1] = __popc(e1);
-                cnt[3 * q + 2] = __popc(e2);
-            }
-        }
-        __syncthreads();
-        scan_chunks(cnt, Q, sm.scan);
-    }
-    // tier of element n (lane of chunk q); `eq` holds the chunk's equal-key prefix (if tie)
-    auto tier_at = [&](int v, int q) -> int {
-        bool in0 = v > V0, in1 = v > V1, in2 = v > V2;
-        if (tie) {
-            const unsigned e0 = __ballot_sync(0xffffffffu, v == V0), e1 = __ballot_sync(0xffffffffu, v == V1),
-                           e2 = __ballot_sync(0xffffffffu, v == V2);
-            if (v == V0) in0 = cnt[3 * q] + __popc(e0 & lt_mask) < R0;
-            if (v == V1) in1 = cnt[3 * q + 1] + __popc(e1 & lt_mask) < R1;
-            if (v == V2) in2 = cnt[3 * q + 2] + __popc(e2 & lt_mask) < R2;
-        } else {
-            in0 = in0 || v == V0;
-            in1 = in1 || v == V1;
-            in2 = in2 || v == V2;
-        }
-        return in0 ? 0 : (in1 ? 1 : (in2 ? 2 : -1));
-    };
-    // ---- 3b. tier membership per 32-id chunk (ballots) -> positions by a scan over chunks ----
-    int *tcnt = tie ? sc + s.F_r : cnt;  // keep the eq prefixes if needed: second table after sc
-    for (int q = warp; q < Q; q += nwarp) {
-        const int n = 32 * q + lane;
-        const int v = n < s.F_r ? sc[n] : -1;
-        const int tr = tier_at(v, q);
-        const unsigned m0 = __ballot_sync(0xffffffffu, tr == 0), m1 = __ballot_sync(0xffffffffu, tr == 1),
-                       m2 = __ballot_sync(0xffffffffu, tr == 2);
-        if (lane == 0) {
-            tcnt[3 * q] = __popc(m0);
-            tcnt[3 * q + 1] = __popc(m1);
-            tcnt[3 * q + 2] = __popc(m2);
-        }
-    }
-    __syncthreads();
-    scan_chunks(tcnt, Q, sm.scan);
-    // ---- 3c. emit: this CTA's records into loc[], CTA 0 the whole lists ----
-    const int lo0 = a0, hi0 = a0 + c1, lo1 = a1, hi1 = a1 + (c2 - c1), lo2 = a2, hi2 = a2 + (n_items - c2);
-    for (int q = warp; q < Q; q += nwarp) {
-        const int b0 = tcnt[3 * q], b1 = tcnt[3 * q + 1], b2 = tcnt[3 * q + 2];
-        const int e0n = q + 1 < Q ? tcnt[3 * q + 3] : s.k16, e1n = q + 1 < Q ? tcnt[3 * q + 4] : s.k8,
-                  e2n = q + 1 < Q ? tcnt[3 * q + 5] : n2;
-        const bool mine = (b0 < hi0 && e0n > lo0) || (b1 < hi1 && e1n > lo1) || (b2 < hi2 && e2n > lo2);
-        if (!mine && !(blockIdx.x == 0 && s.out_ids)) continue;
-        const int n = 32 * q + lane;
-        const int v = n < s.F_r ? sc[n] : -1;
-        const int tr = tier_at(v, q);
-        const unsigned m0 = __ballot_sync(0xffffffffu, tr == 0), m1 = __ballot_sync(0xffffffffu, tr == 1),
-                       m2 = __ballot_sync(0xffffffffu, tr == 2);
-        if (tr >= 0) {
-            const unsigned m = tr == 0 ? m0 : (tr == 1 ? m1 : m2);
-            const int p = (tr == 0 ? b0 : (tr == 1 ? b1 : b2)) + __popc(m & lt_mask);
-            const int lo = tr == 0 ? lo0 : (tr == 1 ? lo1 : lo2), hi = tr == 0 ? hi0 : (tr == 1 ? hi1 : hi2);
-            const int lb = tr == 0 ? 0 : (tr == 1 ? c1 : c2);
-            if (p >= lo && p < hi) S.loc[lb + p - lo] = n;
-            if (blockIdx.x == 0 && s.out_ids) s.out_ids[(tr == 0 ? 0 : (tr == 1 ? n0 : n0 + n1)) + p] = n;
-        }
-    }
-    __syncthreads();
-    auto src = [&](int j) -> const uint8_t * {
-        const int t = j < c1 ? 0 : (j < c2 ? 1 : 2);
-        return a.pool[t] + (int64_t)S.loc[j] * a.nb[t];
-    };
-    ffn_loop(a, d, act, x, n_items, c1, c2, src, S.ring, S.xs, S.dsc, S.bst, sm, partial);
-}
-
 }  // namespace
 
 cudaError_t init_ffn_attrs() {
-    cudaError_t e = cudaFuncSetAttribute(k_ffn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(k_ffn_sel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
-    return e;
+    return cudaFuncSetAttribute(k_ffn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
 }
 
 // balancing weight of one record: bytes + lambda * 3d weights (lambda = 0.5 B per weight)
@@ -720,42 +447,6 @@ cudaError_t launch_ffn(m2c_ctx *c, const LayerState &L, const __half *x, const i
     fill_args(c, L, p, a);
     cudaError_t e = launch_k(k_ffn, dim3(c->G), dim3(d / 8), kSmemBytes, st, a, d, c->desc.act, x,
                              items, counts, partial);
-    c->launch_counter++;
-    return e;
-}
-
-bool ffn_sel_supported(m2c_ctx *c, const m2c_tier_plan &p) {
-    // every CTA's share must fit the local item list; select scratch must fit the ring
-    FfnArgs a;
-    LayerState dummy;
-    fill_args(c, dummy, p, a);
-    const long long W = (long long)p.k_fp16 * a.wt[0] + (long long)p.k_int8 * a.wt[1] + (long long)p.k_int4 * a.wt[2];
-    const long long per = W / c->G + 1;
-    const int wmin = a.wt[2] < a.wt[1] ? (a.wt[2] < a.wt[0] ? a.wt[2] : a.wt[0]) : (a.wt[1] < a.wt[0] ? a.wt[1] : a.wt[0]);
-    const long long Q = (c->F_r + 31) / 32;
-    const long long scratch = 4LL * (kHistBins + 3 * (1LL << c->sel_sh) + 6 * Q + 2LL * c->F_r);
-    return per / wmin + 3 <= kMaxLocal && c->sel_sh <= 12 && scratch <= kRing;
-}
-
-cudaError_t launch_ffn_sel(m2c_ctx *c, const LayerState &L, const __half *x, const int32_t *scores,
-                           const int32_t *hist, int32_t *out_ids, const int32_t *prev_ids,
-                           const m2c_tier_plan &p, float *partial, cudaStream_t st) {
-    const int d = c->desc.d_model;
-    FfnArgs a;
-    fill_args(c, L, p, a);
-    SelArgs s;
-    s.scores = scores;
-    s.hist = hist;
-    s.out_ids = out_ids;
-    s.prev_ids = prev_ids;
-    s.F_r = c->F_r;
-    s.k = p.k;
-    s.k16 = p.k_fp16;
-    s.k8 = p.k_int8;
-    s.smax = c->sel_smax;
-    s.sh = c->sel_sh;
-    cudaError_t e = launch_k(k_ffn_sel, dim3(c->G), dim3(d / 8), kSmemBytes, st, a, s, d, c->desc.act,
-                             x, partial);
     c->launch_counter++;
     return e;
 }

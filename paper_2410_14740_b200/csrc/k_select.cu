@@ -4,25 +4,31 @@
 // higher scores are loaded in higher float-point precision"; mix
 // 25% FP16 / 25% INT8 / 50% INT4.  Order (score desc, id asc) (R3).
 //
-// One CTA of 1024 threads.  Scores -> order-preserving uint32 keys in smem.  The three rank
-// thresholds (k16-th, (k16+k8)-th, k-th largest key) are found by an MSB-first radix select
-// that starts at the highest bit where min and max key differ (the predictor scores span
-// ~20 of the 32 bits), uses one shared 256-bin histogram for the first digit (the three
-// searches share an empty prefix) and afterwards iterates only over a compacted candidate
-// list (the elements inside the chosen bins).  Ties at a threshold are resolved by ascending
-// id with a block scan; a second scan compacts the three tiers into ascending id lists.
-// Optional rank_list: bitonic sort of the k selected (key, ~id) composites.
+// Multi-CTA, single pass, fed by the 4096-bin histogram of (s + smax) >> sh that k_pred_s
+// accumulates.  Every CTA (512 threads) redundantly derives the three rank thresholds:
+//  1. suffix scan of the histogram -> the bin holding the k16-th, (k16+k8)-th and k-th score;
+//  2. one pass over all scores builds 2^sh-bin sub-histograms of those bins -> the exact
+//     values V_t and how many of the E_t elements equal to V_t are in (R_t);
+//  3. partial ties (R_t < E_t): the tied ids are collected and sorted; the R_t-th smallest
+//     is the id cut I_t (ties by ascending id);
+// then classifies its own block of 32-id chunks with warp ballots, obtains the tier-list
+// positions of its block with a decoupled look-back over the preceding blocks' published
+// counts (one 64-bit status word per block, epoch-tagged so it never needs clearing), and
+// writes its part of the three ascending id lists (and tier_of).  The last CTA to finish
+// clears the histogram for the next layer.  The rank list (API only) is a separate 1-CTA sort.
 #include "m2c_internal.cuh"
 
 namespace m2c {
 namespace {
 
-constexpr int NT = kSelectThreads;
+constexpr int NT = 512;
 constexpr int NW = NT / 32;
-constexpr int kMaxCand = 2048;  // candidate list capacity (falls back to a full scan beyond)
+constexpr int kBins = 4096;
+constexpr int kTieCap = 1024;
+constexpr int kChunksPerCta = 16;  // 512 ids per CTA
 
 // exclusive block scan of 3 ints per thread (all threads participate)
-__device__ __forceinline__ void block_scan3(int v[3], int excl[3], int tot[3], int *sm /*[3][NW]*/) {
+__device__ __forceinline__ void block_scan3(const int v[3], int ex[3], int tot[3], int *sm /*[3][32]*/) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     int inc[3];
 #pragma unroll
@@ -30,296 +36,359 @@ __device__ __forceinline__ void block_scan3(int v[3], int excl[3], int tot[3], i
         int x = v[t];
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            int y = __shfl_up_sync(0xffffffffu, x, o);
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
             if (lane >= o) x += y;
         }
         inc[t] = x;
-        if (lane == 31) sm[t * NW + warp] = x;
+        if (lane == 31) sm[t * 32 + warp] = x;
     }
     __syncthreads();
     if (warp == 0) {
 #pragma unroll
         for (int t = 0; t < 3; t++) {
-            int x = (lane < NW) ? sm[t * NW + lane] : 0;
+            int x = lane < NW ? sm[t * 32 + lane] : 0;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
-                int y = __shfl_up_sync(0xffffffffu, x, o);
+                const int y = __shfl_up_sync(0xffffffffu, x, o);
                 if (lane >= o) x += y;
             }
-            if (lane < NW) sm[t * NW + lane] = x;  // inclusive warp totals
+            sm[t * 32 + lane] = x;
         }
     }
     __syncthreads();
 #pragma unroll
     for (int t = 0; t < 3; t++) {
-        const int wbase = warp ? sm[t * NW + warp - 1] : 0;
-        excl[t] = wbase + inc[t] - v[t];
-        tot[t] = sm[t * NW + NW - 1];
+        ex[t] = (warp ? sm[t * 32 + warp - 1] : 0) + inc[t] - v[t];
+        tot[t] = sm[t * 32 + NW - 1];
     }
     __syncthreads();
 }
 
-// warp w < 3 finds, in hist[w] (scanned from the top bin), the bin holding the need-th
-// element; writes the new prefix bits and the remaining rank.
-__device__ __forceinline__ void pick_bin(const int *hist, int need, uint32_t prefix, int shift,
-                                         uint32_t *out_prefix, int *out_rem) {
-    const int lane = threadIdx.x & 31;
-    int loc[8], sum = 0;
-#pragma unroll
-    for (int j = 0; j < 8; j++) {
-        loc[j] = hist[255 - 8 * lane - j];
-        sum += loc[j];
-    }
-    int inc = sum;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        int y = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= o) inc += y;
-    }
-    const int excl = inc - sum;
-    const unsigned ball = __ballot_sync(0xffffffffu, inc >= need);
-    const int src = __ffs(ball) - 1;
-    if (lane == src) {
-        int cum = excl, b = -1, before = 0;
-#pragma unroll
-        for (int j = 0; j < 8; j++) {
-            if (b < 0 && cum + loc[j] >= need) {
-                b = 255 - 8 * lane - j;
-                before = cum;
-            }
-            cum += loc[j];
-        }
-        *out_prefix = prefix | ((uint32_t)b << shift);
-        *out_rem = need - before;
-    }
-}
-
-__global__ void __launch_bounds__(NT, 1)
-    k_select(int F_r, const int32_t *__restrict__ s, int k, int k16, int k8,
-             int32_t *__restrict__ rank_list, int8_t *__restrict__ tier_of,
-             int32_t *__restrict__ tier_ids, int P2) {
-    extern __shared__ __align__(16) uint8_t smraw[];
-    uint32_t *keys = reinterpret_cast<uint32_t *>(smraw);                     // [F_r]
-    int8_t *tier = reinterpret_cast<int8_t *>(smraw + 4 * ((F_r + 3) & ~3));  // [F_r]
-    unsigned long long *ck = reinterpret_cast<unsigned long long *>(
-        smraw + 4 * ((F_r + 3) & ~3) + ((F_r + 15) & ~15));                      // [P2]
-    __shared__ int hist[3][256];
-    __shared__ int scan_sm[3 * NW];
-    __shared__ uint32_t sel_prefix[3], mm[2 * NW];
-    __shared__ int sel_rem[3];
-    __shared__ uint32_t cand[3][kMaxCand];
-    __shared__ int ncand[3];
-    griddep_wait();
-
-    uint32_t kmin = 0xffffffffu, kmax = 0;
-    for (int n = threadIdx.x; n < F_r; n += NT) {
-        const uint32_t key = (uint32_t)s[n] ^ 0x80000000u;
-        keys[n] = key;
-        kmin = min(kmin, key);
-        kmax = max(kmax, key);
-    }
-    for (int i = threadIdx.x; i < 3 * 256; i += NT) (&hist[0][0])[i] = 0;
-    kmin = __reduce_min_sync(0xffffffffu, kmin);
-    kmax = __reduce_max_sync(0xffffffffu, kmax);
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (lane == 0) {
-        mm[warp] = kmin;
-        mm[NW + warp] = kmax;
-    }
-    if (threadIdx.x < 3) ncand[threadIdx.x] = 0;
+// bitonic sort of n <= P2 keys in smem (P2 power of two), padded with `pad`; desc or asc
+template <typename K>
+__device__ __forceinline__ void bitonic(K *a, int n, int P2, K pad, bool desc, int nt) {
+    for (int i = n + threadIdx.x; i < P2; i += nt) a[i] = pad;
     __syncthreads();
-    if (warp == 0) {  // one warp folds the per-warp extrema, then broadcasts through smem
-        const uint32_t a = __reduce_min_sync(0xffffffffu, lane < NW ? mm[lane] : 0xffffffffu);
-        const uint32_t b = __reduce_max_sync(0xffffffffu, lane < NW ? mm[NW + lane] : 0u);
-        if (lane == 0) {
-            mm[0] = a;
-            mm[1] = b;
-        }
-    }
-    __syncthreads();
-    kmin = mm[0];
-    kmax = mm[1];
-    const int target[3] = {k16, k16 + k8, k};
-    const uint32_t diff = kmin ^ kmax;
-    // highest varying bit hb; digit passes cover bits [0, hb]; bits above are common
-    const int hb = diff ? 31 - __clz(diff) : 0;
-    int shift = hb >= 7 ? hb - 7 : 0;
-    uint32_t mask = diff ? ~((2u << hb) - 1u) : 0xffffffffu;  // hb == 31 -> mask 0
-    if (hb == 31) mask = 0;
-    const uint32_t common = kmin & mask;
-    uint32_t prefix[3] = {common, common, common};
-    int rem[3] = {target[0], target[1], target[2]};
-
-    // ---- pass 1: one histogram over all keys (shared by the three searches) ----
-    if (k > 0 && diff) {
-        for (int n = threadIdx.x; n < F_r; n += NT) atomicAdd(&hist[0][(keys[n] >> shift) & 255], 1);
-        __syncthreads();
-        if (warp < 3 && rem[warp] > 0)
-            pick_bin(hist[0], rem[warp], prefix[warp], shift, &sel_prefix[warp], &sel_rem[warp]);
-        __syncthreads();
-#pragma unroll
-        for (int t = 0; t < 3; t++)
-            if (rem[t] > 0) {
-                prefix[t] = sel_prefix[t];
-                rem[t] = sel_rem[t];
-            }
-        mask |= 255u << shift;
-        // ---- compact the candidates of each search (keys inside the chosen bin) ----
-        for (int n = threadIdx.x; n < F_r; n += NT) {
-            const uint32_t key = keys[n];
-#pragma unroll
-            for (int t = 0; t < 3; t++)
-                if (rem[t] > 0 && (key & mask) == prefix[t]) {
-                    const int p = atomicAdd(&ncand[t], 1);
-                    if (p < kMaxCand) cand[t][p] = key;
-                }
-        }
-        __syncthreads();
-        // ---- remaining digits over the candidate lists only ----
-        while (shift > 0) {
-            const int nshift = shift >= 8 ? shift - 8 : 0;
-            const uint32_t dmask = ((1u << (shift - nshift)) - 1u);
-            for (int i = threadIdx.x; i < 3 * 256; i += NT) (&hist[0][0])[i] = 0;
-            __syncthreads();
-#pragma unroll
-            for (int t = 0; t < 3; t++) {
-                if (rem[t] <= 0) continue;
-                const int nc = ncand[t];
-                if (nc <= kMaxCand) {
-                    for (int i = threadIdx.x; i < nc; i += NT) {
-                        const uint32_t key = cand[t][i];
-                        if ((key & mask) == prefix[t]) atomicAdd(&hist[t][(key >> nshift) & dmask], 1);
-                    }
-                } else {  // overflowed candidate list: scan every key
-                    for (int n = threadIdx.x; n < F_r; n += NT) {
-                        const uint32_t key = keys[n];
-                        if ((key & mask) == prefix[t]) atomicAdd(&hist[t][(key >> nshift) & dmask], 1);
-                    }
-                }
-            }
-            __syncthreads();
-            if (warp < 3 && rem[warp] > 0)
-                pick_bin(hist[warp], rem[warp], prefix[warp], nshift, &sel_prefix[warp], &sel_rem[warp]);
-            __syncthreads();
-#pragma unroll
-            for (int t = 0; t < 3; t++)
-                if (rem[t] > 0) {
-                    prefix[t] = sel_prefix[t];
-                    rem[t] = sel_rem[t];
-                }
-            mask |= dmask << nshift;
-            shift = nshift;
-        }
-    } else if (k > 0) {  // all keys equal: the threshold is that key, ties by id
-#pragma unroll
-        for (int t = 0; t < 3; t++) prefix[t] = kmin;
-    }
-    // now: element n has rank < target[t] iff key > prefix[t], or key == prefix[t] and it is
-    // among the first rem[t] such elements in ascending id order (target 0: nobody).
-
-    // ---- classify (needs the running count of equal keys in id order) ----
-    const int CH = (F_r + NT - 1) / NT;
-    const int n0 = min(F_r, (int)threadIdx.x * CH), n1 = min(F_r, n0 + CH);
-    int v[3], ex[3], tot[3];
-#pragma unroll
-    for (int t = 0; t < 3; t++) v[t] = 0;
-    for (int n = n0; n < n1; n++) {
-        const uint32_t key = keys[n];
-#pragma unroll
-        for (int t = 0; t < 3; t++) v[t] += (target[t] > 0 && key == prefix[t]);
-    }
-    block_scan3(v, ex, tot, scan_sm);
-    int cnt[3] = {0, 0, 0};
-    for (int n = n0; n < n1; n++) {
-        const uint32_t key = keys[n];
-        int tr = -1;
-#pragma unroll
-        for (int t = 2; t >= 0; t--) {
-            bool in = false;
-            if (target[t] > 0) {
-                if (key > prefix[t]) in = true;
-                else if (key == prefix[t]) in = (ex[t]++ < rem[t]);
-            }
-            if (in) tr = t;
-        }
-        tier[n] = (int8_t)tr;
-        if (tr >= 0) cnt[tr]++;
-    }
-    // ---- compact the tiers into ascending id lists ----
-    block_scan3(cnt, ex, tot, scan_sm);
-    const int seg[3] = {0, k16, k16 + k8};
-    for (int n = n0; n < n1; n++) {
-        const int tr = tier[n];
-        if (tier_of) tier_of[n] = (int8_t)tr;
-        if (tr >= 0) tier_ids[seg[tr] + ex[tr]++] = n;
-    }
-    griddep_launch();
-    if (rank_list == nullptr || k == 0) return;
-
-    // ---- rank list: bitonic sort (descending) of the selected (key, ~id) composites ----
-    __syncthreads();
-    int c3[3] = {0, 0, 0};
-    for (int n = n0; n < n1; n++) c3[0] += (tier[n] >= 0);
-    block_scan3(c3, ex, tot, scan_sm);
-    int pos = ex[0];
-    for (int n = n0; n < n1; n++)
-        if (tier[n] >= 0)
-            ck[pos++] = ((unsigned long long)keys[n] << 32) | (uint32_t)(~(uint32_t)n);
-    for (int i = k + (int)threadIdx.x; i < P2; i += NT) ck[i] = 0ull;
-    __syncthreads();
-    for (int size = 2; size <= P2; size <<= 1) {
+    for (int size = 2; size <= P2; size <<= 1)
         for (int stride = size >> 1; stride > 0; stride >>= 1) {
-            for (int i = threadIdx.x; i < P2 / 2; i += NT) {
-                const int lo = 2 * i - (i & (stride - 1));
-                const int hi = lo + stride;
-                const bool desc = ((lo & size) == 0);
-                const unsigned long long a = ck[lo], b = ck[hi];
-                if ((a < b) == desc) {
-                    ck[lo] = b;
-                    ck[hi] = a;
+            for (int i = threadIdx.x; i < P2 / 2; i += nt) {
+                const int lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
+                const bool dir = ((lo & size) == 0) != desc;
+                const K x = a[lo], y = a[hi];
+                if ((x > y) == dir) {
+                    a[lo] = y;
+                    a[hi] = x;
                 }
             }
             __syncthreads();
         }
+}
+
+// status word: [63:62] state (1 aggregate, 2 inclusive) | [61:56] epoch | 3 x 18-bit counts
+__device__ __forceinline__ unsigned long long pack_st(int state, int epoch, int c0, int c1, int c2) {
+    return ((unsigned long long)state << 62) | ((unsigned long long)(epoch & 63) << 56) |
+           ((unsigned long long)c2 << 36) | ((unsigned long long)c1 << 18) | (unsigned long long)c0;
+}
+
+struct SelParams {
+    const int32_t *s;
+    int *ghist;
+    unsigned long long *status;  // [nblk]
+    int *done;                   // completion counter (last CTA clears the histogram)
+    int *epoch_ptr;              // device launch counter (advanced by the last CTA)
+    int F_r, k, k16, k8, smax, sh;
+    int32_t *tier_ids;           // [k] three ascending segments
+    int8_t *tier_of;             // [F_r] or null
+};
+
+__global__ void __launch_bounds__(NT, 1) k_select(SelParams p) {
+    extern __shared__ __align__(16) uint8_t smraw[];
+    const int nsub = 1 << p.sh;
+    int *hist = reinterpret_cast<int *>(smraw);  // [4096]
+    int *sub = hist + kBins;                     // [3][nsub]
+    int *ties = sub + 3 * nsub;                  // [3][kTieCap]
+    __shared__ int scan_sm[96];
+    __shared__ int selv[16];
+    __shared__ int ntie[3], blk_cnt[NW][3];
+    __shared__ int prefix_sh[3];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int F_r = p.F_r;
+    griddep_launch();
+    griddep_wait();
+    const int epoch = *(volatile const int *)p.epoch_ptr;
+
+    // ---- 1. histogram suffix scan -> bins of the three targets ----
+    const int tg[3] = {p.k16, p.k16 + p.k8, p.k};
+    constexpr int BPT = kBins / NT;  // 8 bins per thread, descending order
+    int lsum = 0;
+    {
+        int v[BPT];
+#pragma unroll
+        for (int i = 0; i < BPT; i++) v[i] = p.ghist[kBins - 1 - (tid * BPT + i)];
+#pragma unroll
+        for (int i = 0; i < BPT; i++) {
+            hist[kBins - 1 - (tid * BPT + i)] = v[i];
+            lsum += v[i];
+        }
     }
-    for (int i = threadIdx.x; i < k; i += NT) rank_list[i] = (int32_t)(~(uint32_t)(ck[i] & 0xffffffffu));
+    if (tid < 3) ntie[tid] = 0;
+    {
+        const int vv[3] = {lsum, 0, 0};
+        int ex[3], tot[3];
+        block_scan3(vv, ex, tot, scan_sm);
+        int cum = ex[0];
+#pragma unroll
+        for (int i = 0; i < BPT; i++) {
+            const int b = kBins - 1 - (tid * BPT + i);
+            const int v = hist[b];
+#pragma unroll
+            for (int t = 0; t < 3; t++)
+                if (tg[t] > 0 && cum < tg[t] && cum + v >= tg[t]) {
+                    selv[t] = b;
+                    selv[3 + t] = tg[t] - cum;  // rank needed inside the bin
+                }
+            cum += v;
+        }
+    }
+    for (int i = tid; i < 3 * nsub; i += NT) sub[i] = 0;
+    __syncthreads();
+    const int bin0 = tg[0] > 0 ? selv[0] : -1, bin1 = tg[1] > 0 ? selv[1] : -1,
+              bin2 = tg[2] > 0 ? selv[2] : -1;
+    // ---- 2. sub-histograms of the chosen bins (8 score loads in flight per thread) ----
+    for (int n0 = tid; n0 < F_r; n0 += 8 * NT) {
+        int v[8];
+#pragma unroll
+        for (int i = 0; i < 8; i++) v[i] = n0 + i * NT < F_r ? p.s[n0 + i * NT] + p.smax : -1;
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+            if (v[i] < 0) continue;
+            const int b = v[i] >> p.sh, lo = v[i] & (nsub - 1);
+            if (b == bin0) atomicAdd(&sub[lo], 1);
+            if (b == bin1) atomicAdd(&sub[nsub + lo], 1);
+            if (b == bin2) atomicAdd(&sub[2 * nsub + lo], 1);
+        }
+    }
+    __syncthreads();
+    {
+        const int SPT = (nsub + NT - 1) / NT;
+        int v3[3] = {0, 0, 0}, ex[3], tot[3];
+        for (int i = 0; i < SPT; i++) {
+            const int c = nsub - 1 - (tid * SPT + i);
+            if (c < 0) break;
+#pragma unroll
+            for (int t = 0; t < 3; t++) v3[t] += sub[t * nsub + c];
+        }
+        block_scan3(v3, ex, tot, scan_sm);
+#pragma unroll
+        for (int t = 0; t < 3; t++) {
+            if (tg[t] <= 0) continue;
+            const int need = selv[3 + t];
+            int cum = ex[t];
+            for (int i = 0; i < SPT; i++) {
+                const int c = nsub - 1 - (tid * SPT + i);
+                if (c < 0) break;
+                const int v = sub[t * nsub + c];
+                if (cum < need && cum + v >= need) {
+                    selv[6 + t] = ((t == 0 ? bin0 : (t == 1 ? bin1 : bin2)) << p.sh) | c;  // V_t
+                    selv[9 + t] = need - cum;                                            // R_t
+                    selv[12 + t] = v;                                                    // E_t
+                }
+                cum += v;
+            }
+        }
+    }
+    __syncthreads();
+    int V[3], I[3];
+    bool part[3];
+#pragma unroll
+    for (int t = 0; t < 3; t++) {
+        V[t] = tg[t] > 0 ? selv[6 + t] : 0x7fffffff;
+        part[t] = tg[t] > 0 && selv[9 + t] < selv[12 + t];
+        I[t] = 0x7fffffff;
+    }
+    // ---- 3. partial ties: the R_t smallest ids among those equal to V_t are in ----
+    if (part[0] || part[1] || part[2]) {
+        for (int n = tid; n < F_r; n += NT) {
+            const int v = p.s[n] + p.smax;
+#pragma unroll
+            for (int t = 0; t < 3; t++)
+                if (part[t] && v == V[t]) {
+                    const int q = atomicAdd(&ntie[t], 1);
+                    if (q < kTieCap) ties[t * kTieCap + q] = n;
+                }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int t = 0; t < 3; t++) {
+            if (!part[t]) continue;
+            const int m = ntie[t], R = selv[9 + t];
+            if (m <= kTieCap) {
+                int P2 = 1;
+                while (P2 < m) P2 <<= 1;
+                bitonic<int>(ties + t * kTieCap, m, P2, 0x7fffffff, false, NT);
+                I[t] = ties[t * kTieCap + R - 1];
+                __syncthreads();
+            } else {
+                // degenerate (e.g. x = 0: every score ties): binary search the smallest id I
+                // with #{tied ids <= I} >= R, one block-wide count per step
+                int lo = 0, hi = F_r - 1;
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    int c = 0;
+                    for (int nn = tid; nn <= mid; nn += NT) c += (p.s[nn] + p.smax == V[t]);
+                    const int vv[3] = {c, 0, 0};
+                    int ex[3], tot[3];
+                    block_scan3(vv, ex, tot, scan_sm);
+                    if (tot[0] >= R) hi = mid;
+                    else lo = mid + 1;
+                }
+                I[t] = lo;
+            }
+        }
+    }
+    // ---- 4. classify this CTA's chunks; look back for the tier-list positions ----
+    const int Q = (F_r + 31) / 32;
+    const int q0 = blockIdx.x * kChunksPerCta;
+    int cnt_w[3] = {0, 0, 0};
+    int trs = -1;
+    unsigned msk[3] = {0, 0, 0};
+    const int q = q0 + warp;  // kChunksPerCta == NW: one chunk per warp
+    const int n = 32 * q + lane;
+    if (q < Q) {
+        const int v = n < F_r ? p.s[n] + p.smax : -1;
+        bool in[3];
+#pragma unroll
+        for (int t = 0; t < 3; t++) in[t] = v > V[t] || (v == V[t] && n <= I[t]);
+        trs = in[0] ? 0 : (in[1] ? 1 : (in[2] ? 2 : -1));
+        if (n >= F_r) trs = -1;
+#pragma unroll
+        for (int t = 0; t < 3; t++) {
+            msk[t] = __ballot_sync(0xffffffffu, trs == t);
+            cnt_w[t] = __popc(msk[t]);
+        }
+    }
+    if (lane == 0)
+#pragma unroll
+        for (int t = 0; t < 3; t++) blk_cnt[warp][t] = cnt_w[t];
+    __syncthreads();
+    if (warp == 0) {  // exclusive prefix over the CTA's warps (chunks) and block totals
+        int c[3];
+#pragma unroll
+        for (int t = 0; t < 3; t++) {
+            int x = lane < NW ? blk_cnt[lane][t] : 0;
+            int inc = x;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += y;
+            }
+            if (lane < NW) blk_cnt[lane][t] = inc - x;
+            c[t] = __shfl_sync(0xffffffffu, inc, NW - 1);
+        }
+        if (lane == 0) {  // decoupled look-back
+            const int b = blockIdx.x;
+            unsigned long long *st = p.status;
+            int pre[3] = {0, 0, 0};
+            if (b == 0) {
+                st[0] = pack_st(2, epoch, c[0], c[1], c[2]);
+            } else {
+                atomicExch(&st[b], pack_st(1, epoch, c[0], c[1], c[2]));
+                for (int j = b - 1; j >= 0; j--) {
+                    unsigned long long w;
+                    do {
+                        w = *((volatile unsigned long long *)&st[j]);
+                    } while ((int)((w >> 56) & 63) != (epoch & 63) || (w >> 62) == 0);
+                    pre[0] += (int)(w & 0x3ffff);
+                    pre[1] += (int)((w >> 18) & 0x3ffff);
+                    pre[2] += (int)((w >> 36) & 0x3ffff);
+                    if ((w >> 62) == 2) break;
+                }
+                __threadfence();
+                atomicExch(&st[b], pack_st(2, epoch, pre[0] + c[0], pre[1] + c[1], pre[2] + c[2]));
+            }
+#pragma unroll
+            for (int t = 0; t < 3; t++) prefix_sh[t] = pre[t];
+        }
+    }
+    __syncthreads();
+    if (q < Q) {
+        const int seg[3] = {0, p.k16, p.k16 + p.k8};
+        if (n < F_r && p.tier_of) p.tier_of[n] = (int8_t)trs;
+        if (trs >= 0) {
+            const unsigned lt = (1u << lane) - 1u;
+            const unsigned m = trs == 0 ? msk[0] : (trs == 1 ? msk[1] : msk[2]);
+            const int pos = prefix_sh[trs] + blk_cnt[warp][trs] + __popc(m & lt);
+            p.tier_ids[seg[trs] + pos] = n;
+        }
+    }
+    // ---- the last CTA clears the histogram for the next layer ----
+    __syncthreads();
+    __shared__ int last;
+    if (tid == 0) {
+        __threadfence();
+        last = atomicAdd(p.done, 1) == (int)gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last) {  // every CTA has read the histogram and the epoch: reset for the next launch
+        for (int i = tid; i < kBins; i += NT) p.ghist[i] = 0;
+        if (tid == 0) {
+            *p.done = 0;
+            *p.epoch_ptr = (epoch + 1) & 63;
+        }
+    }
+}
+
+// API path: the rank list = the selected ids sorted by (score desc, id asc)
+__global__ void __launch_bounds__(1024, 1)
+    k_rank_list(const int32_t *__restrict__ s, const int32_t *__restrict__ tier_ids, int k,
+                int P2, int32_t *__restrict__ rank_list) {
+    extern __shared__ __align__(16) unsigned long long ck[];
+    griddep_wait();
+    for (int i = threadIdx.x; i < k; i += blockDim.x) {
+        const int n = tier_ids[i];
+        ck[i] = ((unsigned long long)((uint32_t)s[n] ^ 0x80000000u) << 32) | (uint32_t)(~(uint32_t)n);
+    }
+    __syncthreads();
+    bitonic<unsigned long long>(ck, k, P2, 0ull, true, blockDim.x);
+    for (int i = threadIdx.x; i < k; i += blockDim.x) rank_list[i] = (int32_t)(~(uint32_t)(ck[i] & 0xffffffffu));
 }
 
 }  // namespace
 
-size_t select_smem_bytes(int F_r, int P2) {
-    return 4 * (size_t)((F_r + 3) & ~3) + (size_t)((F_r + 15) & ~15) + 8 * (size_t)P2;
-}
-
-static size_t g_select_smem_max = 0;
+size_t select_smem_bytes(int sh) { return 4 * ((size_t)kBins + 3 * ((size_t)1 << sh) + 3 * (size_t)kTieCap); }
+int select_blocks(int F_r) { return ((F_r + 31) / 32 + kChunksPerCta - 1) / kChunksPerCta; }
 
 cudaError_t init_select_attrs() {
-    // opt-in limit per block minus this kernel's static shared memory
-    int dev = 0, optin = 0;
-    cudaError_t e = cudaGetDevice(&dev);
-    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    cudaFuncAttributes fa;
-    if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, k_select);
-    if (e != cudaSuccess) return e;
-    g_select_smem_max = (size_t)optin - fa.sharedSizeBytes;
-    return cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)g_select_smem_max);
+    cudaError_t e = cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)select_smem_bytes(12));
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_rank_list, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 16384);
+    return e;
 }
 
-size_t select_smem_limit() { return g_select_smem_max; }
-
-cudaError_t launch_select(m2c_ctx *c, const int32_t *scores, const m2c_tier_plan &p,
-                          int32_t *rank_list, int8_t *tier_of, int32_t *tier_ids,
-                          cudaStream_t st) {
-    int P2 = 0;
-    if (rank_list && p.k > 0) {
-        P2 = 1;
-        while (P2 < p.k) P2 <<= 1;
-        if (P2 < 2) P2 = 2;
-    }
-    const size_t smem = select_smem_bytes(c->F_r, P2);
-    cudaError_t e = launch_k(k_select, dim3(1), dim3(NT), smem, st, c->F_r, scores, p.k, p.k_fp16,
-                             p.k_int8, rank_list, tier_of, tier_ids, P2);
+cudaError_t launch_select(m2c_ctx *c, const int32_t *scores, int *hist, const m2c_tier_plan &p,
+                          int32_t *rank_list, int8_t *tier_of, int32_t *tier_ids, cudaStream_t st) {
+    cudaError_t e;
+    SelParams sp;
+    sp.s = scores;
+    sp.ghist = hist;
+    sp.status = c->sel_status;
+    sp.done = c->sel_done;
+    sp.epoch_ptr = c->sel_epoch;
+    sp.F_r = c->F_r;
+    sp.k = p.k;
+    sp.k16 = p.k_fp16;
+    sp.k8 = p.k_int8;
+    sp.smax = c->sel_smax;
+    sp.sh = c->sel_sh;
+    sp.tier_ids = tier_ids;
+    sp.tier_of = tier_of;
+    e = launch_k(k_select, dim3(select_blocks(c->F_r)), dim3(NT), select_smem_bytes(c->sel_sh), st, sp);
+    c->launch_counter++;
+    if (e != cudaSuccess || rank_list == nullptr || p.k == 0) return e;
+    int P2 = 2;
+    while (P2 < p.k) P2 <<= 1;
+    e = launch_k(k_rank_list, dim3(1), dim3(1024), 8 * (size_t)P2, st, scores, tier_ids, p.k, P2, rank_list);
     c->launch_counter++;
     return e;
 }

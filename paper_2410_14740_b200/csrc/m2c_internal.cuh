@@ -48,6 +48,7 @@ struct LayerState {
 
 struct NcclApi;  // dlopen'd NCCL entry points
 
+
 struct Workspace {
     int32_t *h = nullptr;          // [r]
     int32_t *s = nullptr;          // [F_r]
@@ -95,6 +96,9 @@ struct m2c_ctx {
     int sel_smax = 0, sel_sh = 0;
     int *ghist = nullptr;       // [4096]
     int32_t *prev_ids = nullptr;  // [n_layers][k]
+    unsigned long long *sel_status = nullptr;  // [select blocks] decoupled look-back words
+    int *sel_done = nullptr;    // select completion counter
+    int *sel_epoch = nullptr;   // select launch epoch
     bool use_fused = true;
     // multi-GPU
     m2c::NcclApi *nccl = nullptr;
@@ -109,14 +113,20 @@ namespace m2c {
 // ----------------------------------------------------------------------------------------
 cudaError_t launch_pack(int d, int bits, const __half *g, const __half *u, const __half *dn,
                         int64_t n0, int64_t n1, uint8_t *out, cudaStream_t st);
+// L2 prefetch hint: the previous token's tier lists of this layer (resident pools, ids = slots)
+struct PrefetchArgs {
+    const int32_t *prev_ids = nullptr;  // [k] or null
+    const uint8_t *pool[3] = {nullptr, nullptr, nullptr};
+    int nb[3] = {0, 0, 0};
+    int k[3] = {0, 0, 0};
+    int F_r = 0;
+};
 cudaError_t launch_predict(m2c_ctx *c, const LayerState &L, const __half *x, int32_t *scores,
-                           int *hist, cudaStream_t st);
-cudaError_t launch_ffn_sel(m2c_ctx *c, const LayerState &L, const __half *x, const int32_t *scores,
-                           const int32_t *hist, int32_t *out_ids, const int32_t *prev_ids,
-                           const m2c_tier_plan &p, float *partial, cudaStream_t st);
-bool ffn_sel_supported(m2c_ctx *c, const m2c_tier_plan &p);
-cudaError_t launch_select(m2c_ctx *c, const int32_t *scores, const m2c_tier_plan &p,
+                           int *hist, const int32_t *prefetch_ids, cudaStream_t st);
+cudaError_t launch_select(m2c_ctx *c, const int32_t *scores, int *hist, const m2c_tier_plan &p,
                           int32_t *rank_list, int8_t *tier_of, int32_t *tier_ids, cudaStream_t st);
+size_t select_smem_bytes(int sh);
+int select_blocks(int F_r);
 cudaError_t launch_lru(m2c_ctx *c, LayerState &L, const int32_t *step_dev, const int32_t *tier_ids,
                        const m2c_tier_plan &p, int32_t *slots, uint32_t *hit_bits,
                        int32_t *miss_log, int32_t *evict_log, cudaStream_t st);
