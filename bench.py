@@ -174,7 +174,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--eager", action="store_true", help="no CUDA graph")
-    ap.add_argument("--unfused", action="store_true", help="separate select kernel")
+    ap.add_argument("--unfused", action="store_true", help="per-phase kernel chain instead of k_decode")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -259,7 +259,8 @@ def main():
     peak, peak_src = _peaks()
     gbs = ab["token"] * K / (ms / 1e3) / 1e9 * P / P  # per-GPU bytes x tokens / time
 
-    # ---- phase breakdown + dominant-kernel roofline (events inside the graph) ----
+    # ---- phase breakdown + dominant-kernel roofline ----
+    fused = kpt == 1  # the persistent decode kernel k_decode is the whole token
     ctx.profile(True)
     prof = [[0.0] * 4 for _ in range(cfg.n_layers)]
     nprof = min(K, 32)
@@ -273,9 +274,26 @@ def main():
                 prof[l][i] += p[l][i] / nprof
     ctx.profile(False)
     phase_ms = [sum(prof[l][i] for l in range(cfg.n_layers)) for i in range(4)]
-    ffn_launch_ms = phase_ms[2] / (cfg.n_layers * n_ffn)
-    ffn_bytes_launch = ab["ffn_per_launch"] / n_ffn
-    achieved = ffn_bytes_launch / (ffn_launch_ms / 1e3) / 1e9
+    if fused:
+        # k_decode launch durations, CUDA events on its own (compute) stream, after warm-up
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(nprof)]
+        with torch.cuda.stream(ctx.compute):
+            for t in range(nprof):
+                x.copy_(toks[W + t % K])
+                evs[t][0].record(ctx.compute)
+                ctx.decode_step(x, step)
+                evs[t][1].record(ctx.compute)
+                step += 1
+        torch.cuda.synchronize()
+        launch_ms = sum(a.elapsed_time(b) for a, b in evs) / nprof
+        bytes_launch = ab["token"]
+        kname = "k_decode (persistent: predictor + select + FFN + reduce, all layers)"
+    else:
+        launch_ms = phase_ms[2] / (cfg.n_layers * n_ffn)
+        bytes_launch = ab["ffn_per_launch"] / n_ffn
+        kname = "k_ffn (fused dequant-GEMV + SiLU*mul + down)"
+    achieved = bytes_launch / (launch_ms / 1e3) / 1e9
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ffn_traffic.json")) as f:
@@ -321,12 +339,12 @@ def main():
                        "cache": cfg.cache_mode, "global_batch": 1, "seq_len": 1,
                        "parallelism": f"dff-shard{P}" if P > 1 else "single",
                        "l2": "inputs larger than L2 (%.0f MB touched per token)" % (ab["token"] / 1e6),
-                       "graph": not args.eager},
+                       "graph": not args.eager, "persistent_kernel": fused},
             "hbm_gbs": gbs, "hbm_frac": gbs / peak,
-            "roofline": {"kernel": "k_ffn (fused dequant-GEMV + SiLU*mul + down)", "bound": "hbm",
+            "roofline": {"kernel": kname, "bound": "hbm",
                          "achieved": achieved, "peak": peak, "peak_src": peak_src,
                          "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
-                         "bytes_per_launch": ffn_bytes_launch, "ms_per_launch": ffn_launch_ms},
+                         "bytes_per_launch": bytes_launch, "ms_per_launch": launch_ms},
             "phase_ms_per_token": dict(zip(["predict", "select", "cache+ffn", "reduce"], phase_ms)),
             "gpu_launches": kpt * K,
             "kernels_per_token": kpt,

@@ -179,23 +179,40 @@ m2c_status m2c_comm_init(m2c_ctx *ctx, int32_t nranks, int32_t rank, const void 
  * x_{l+1} = fp16(x_l + fp16(y_l)) (R14).  step: strictly increasing (LRU timestamps). */
 m2c_status m2c_decode_step(m2c_ctx *ctx, void *x_inout, int64_t step);
 
+/* The tier lists the last m2c_decode_step selected for resident layer `layer`: int32 [k],
+ * three ascending segments k16 | k8 | k4 (the layout of m2c_predict_rank's tier_ids), copied
+ * to the device buffer tier_ids_out on the compute stream.  M2C_ERR_STATE for an LRU/ATU layer
+ * (its lists are not kept per layer) or before the first decode step. */
+m2c_status m2c_decode_lists(m2c_ctx *ctx, int32_t layer, int32_t *tier_ids_out);
+
 /* Disables (0) or enables (1, default) CUDA-graph capture of m2c_decode_step. */
 m2c_status m2c_set_graph(m2c_ctx *ctx, int32_t enable);
 
-/* Resident layers in m2c_decode_step: 1 (default) = the predictor kernel also prefetches into
- * L2 the records the previous token selected for the layer (adjacent tokens share ~80% of
- * their active neurons), so most of the FFN's reads hit L2; 0 = no prefetch.  A hint
- * only: results are bit-identical either way (tests). */
+/* m2c_decode_step engine.  1 (default): a stack whose layers are all resident, unsharded
+ * (no communicator), with F_r <= 40960 and ceil(F_r / SMs) <= d_model / 8 runs as ONE
+ * persistent cooperative kernel per token
+ * (k_decode: one CTA per SM, grid barriers between the phases of a layer, L2 lookahead of the
+ * next layer's predictor slices and of the records the previous token selected for it --
+ * adjacent tokens share ~80% of their active neurons); other stacks run the per-phase
+ * kernel chain with the same L2 prefetch hint.  0: the per-phase kernel chain, no prefetch.
+ * Results are bit-identical either way (tests). */
 m2c_status m2c_set_fused(m2c_ctx *ctx, int32_t enable);
 
-/* Phase timing (CUDA events recorded inside the decode graph, on the compute stream):
- * m2c_profile(ctx, 1) instruments every layer of m2c_decode_step with 5 timing events
- * (before predict | after predict | after select | after cache+FFN | after reduce); the graph
- * is re-captured.  m2c_profile_read synchronises the compute stream and writes, for the last
- * decode step, ms[l*4 + {0,1,2,3}] = predictor, select, cache lookup + FFN (all launches),
- * reduce/all-reduce/residual of layer l.  ffn_launches_out = FFN kernel launches per layer. */
+/* Phase timing.  m2c_profile(ctx, 1) instruments m2c_decode_step (the graph is re-captured):
+ * the kernel chain records 5 CUDA events per layer (before predict | after predict | after
+ * select | after cache+FFN | after reduce); k_decode records globaltimer stamps per (layer,
+ * CTA).  m2c_profile_read synchronises the compute stream and writes, for the last decode
+ * step, ms[l*4 + {0,1,2,3}] = predictor, select, cache lookup + FFN, reduce/all-reduce/residual
+ * of layer l (k_decode: measured on the slowest CTA, barriers included in the phase they
+ * end).  ffn_launches_out = FFN kernel launches per layer (0 for k_decode).
+ * m2c_profile_stamps copies k_decode's raw stamps, uint64 ns [n_layers][G][16] (0 layer start,
+ * 1 P1 done, 2 after barrier 1, 3 P2 done, 4 after barrier 2, 5 select done, 6 FFN done,
+ * 7 after barrier 3, 8 reduce done, 9 kernel end, 10..13 select sub-steps, 14..15 unused);
+ * *n_out = the element count (out may be null to query it); M2C_ERR_STATE if the last step
+ * did not run on k_decode with profiling. */
 m2c_status m2c_profile(m2c_ctx *ctx, int32_t enable);
 m2c_status m2c_profile_read(m2c_ctx *ctx, float *ms, int32_t *ffn_launches_out);
+m2c_status m2c_profile_stamps(m2c_ctx *ctx, uint64_t *out, int64_t cap, int64_t *n_out);
 
 /* Kernels launched by the last m2c_decode_step (per token), and cumulative cache counters
  * (hits, misses per tier) since the last reset (device counters; synchronises). */

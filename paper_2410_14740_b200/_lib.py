@@ -60,11 +60,13 @@ SIGNATURES = [
     ("m2c_nccl_unique_id", C.c_int, [C.c_char_p, _vp]),
     ("m2c_comm_init", C.c_int, [_vp, _i32, _i32, _vp, C.c_char_p]),
     ("m2c_decode_step", C.c_int, [_vp, _vp, _i64]),
+    ("m2c_decode_lists", C.c_int, [_vp, _i32, _vp]),
     ("m2c_set_graph", C.c_int, [_vp, _i32]),
     ("m2c_set_fused", C.c_int, [_vp, _i32]),
     ("m2c_stats", C.c_int, [_vp, _P(_i64), _P(_i64), _P(_i64), _i32]),
     ("m2c_profile", C.c_int, [_vp, _i32]),
     ("m2c_profile_read", C.c_int, [_vp, _P(C.c_float), _P(_i32)]),
+    ("m2c_profile_stamps", C.c_int, [_vp, _P(C.c_uint64), _i64, _P(_i64)]),
 ]
 
 _lib = None

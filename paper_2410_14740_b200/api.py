@@ -111,7 +111,10 @@ class M2CContext:
             cur.wait_stream(self.compute)
 
     def __del__(self):
-        self.close()
+        try:
+            self.close()
+        except Exception:  # interpreter shutdown: modules may already be torn down
+            pass
 
     def close(self):
         if getattr(self, "_h", None):
@@ -212,6 +215,12 @@ class M2CContext:
     def decode_step(self, x_inout, step: int):
         self._call(lib().m2c_decode_step, self._h, _ptr(x_inout), int(step))
 
+    def decode_lists(self, layer):
+        """Tier lists [k] (k16 | k8 | k4 ascending segments) of the last decode step's layer."""
+        out = torch.empty(max(self.plan.k, 1), dtype=torch.int32, device=self.device)
+        self._call(lib().m2c_decode_lists, self._h, layer, _ptr(out))
+        return out[:self.plan.k]
+
     def set_graph(self, enable: bool):
         check(lib().m2c_set_graph(self._h, 1 if enable else 0))
 
@@ -229,6 +238,17 @@ class M2CContext:
         n = C.c_int32()
         check(lib().m2c_profile_read(self._h, ms, C.byref(n)))
         return [list(ms[4 * l:4 * l + 4]) for l in range(L)], n.value
+
+    def profile_stamps(self):
+        """Raw k_decode stamps of the last decode step (profiling on): numpy uint64
+        [n_layers, G, 16] in ns (include/m2c.h documents the stamp points)."""
+        import numpy as np
+        n = C.c_int64()
+        check(lib().m2c_profile_stamps(self._h, None, 0, C.byref(n)))
+        buf = (C.c_uint64 * n.value)()
+        check(lib().m2c_profile_stamps(self._h, buf, n.value, C.byref(n)))
+        a = np.frombuffer(buf, dtype=np.uint64).copy()
+        return a.reshape(self.desc.n_layers, -1, 16)
 
     def stats(self, reset=False):
         kpt = C.c_int64()

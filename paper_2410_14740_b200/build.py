@@ -8,7 +8,7 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SOURCES = ["api.cu", "k_pack.cu", "k_pred.cu", "k_select.cu", "k_cache.cu", "k_ffn.cu",
-           "k_reduce.cu"]
+           "k_reduce.cu", "k_decode.cu"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared"]
 

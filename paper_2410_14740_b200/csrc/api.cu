@@ -2,6 +2,7 @@
 // orchestration, CUDA-graph capture of the decode step, NCCL (dlopen) for d_ff sharding.
 #include <dlfcn.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -190,8 +191,22 @@ static cudaError_t enqueue_layer(m2c_ctx *c, int l, __half *x) {
     return mark(c, l, 4);
 }
 
+// the persistent decode kernel covers a resident, unsharded stack whose scores fit in smem
+static bool decode_fused(const m2c_ctx *c) {
+    const int rps = (c->F_r + c->G - 1) / c->G;  // a CTA's own neurons: one pass of its threads
+    if (!c->use_fused || c->nranks > 1 || c->F_r > decode_max_F() || rps > c->desc.d_model / 8 ||
+        rps > 4096)
+        return false;
+    for (const LayerState &L : c->layers)
+        if (L.mode != 0) return false;
+    return true;
+}
+
 static cudaError_t enqueue_token(m2c_ctx *c, __half *x) {
     const m2c_tier_plan &p = c->plan;
+    c->last_token_fused = decode_fused(c);
+    if (c->last_token_fused)
+        return launch_decode(c, x, c->prof_ev.empty() ? nullptr : c->dec_prof, c->compute);
     cudaError_t e = launch_set_counts(c->ws.counts, p.k_fp16, p.k_int8, p.k_int4, c->compute);
     c->launch_counter++;
     if (e) return e;
@@ -312,8 +327,14 @@ m2c_status m2c_create(const m2c_model_desc *desc, int32_t device, m2c_stream_t c
                  o_mid = take(4 * (size_t)F_r), o_cnt = take(4 * 16),
                  o_part = take(4 * (size_t)2 * c->G * d), o_y = take(4 * (size_t)d),
                  o_x = take(2 * (size_t)d), o_stats = take(8 * 6), o_err = take(4),
-                 o_hist = take(4 * 4096), o_sst = take(8 * (size_t)select_blocks(F_r)),
-                 o_sdone = take(4), o_sepoch = take(4),
+                 o_hist = take(4 * 2 * 4096), o_sst = take(8 * (size_t)select_blocks(F_r)),
+                 o_sdone = take(4), o_sepoch = take(4), o_bflags = take(4 * (size_t)c->G),
+                 o_bepoch = take(4), o_dlay = take(decode_layer_table_bytes(desc->n_layers)),
+                 o_dprof = take(8 * (size_t)kDecodeStamps * c->G * desc->n_layers),
+                 o_binsh = take(4 * (size_t)desc->n_layers), o_sabs = take(4 * (size_t)desc->n_layers),
+                 o_bucket = take(decode_bucket_bytes()), o_chist = take(4 * 2 * (size_t)decode_coarse_bins()),
+                 o_stage = take(4 * 3 * (size_t)c->G * ((F_r + c->G - 1) / c->G)),
+                 o_ccount = take(16 * (size_t)c->G),
                  o_prev = take(4 * (size_t)desc->n_layers * (plan->k > 0 ? plan->k : 1));
     // score histogram geometry: |s| <= 127^2 r, bins of 2^sh over [0, 2 smax] (4096 bins)
     c->sel_smax = 16129 * desc->pred_rank;
@@ -349,7 +370,23 @@ m2c_status m2c_create(const m2c_model_desc *desc, int32_t device, m2c_stream_t c
     c->sel_status = (unsigned long long *)(b + o_sst);
     c->sel_done = (int *)(b + o_sdone);
     c->sel_epoch = (int *)(b + o_sepoch);
+    c->bar_flags = (unsigned *)(b + o_bflags);
+    c->bar_epoch = (unsigned *)(b + o_bepoch);
+    c->dec_layers = b + o_dlay;
+    c->dec_prof = (unsigned long long *)(b + o_dprof);
+    c->dec_bin_sh = (int *)(b + o_binsh);
+    c->dec_sabs = (unsigned *)(b + o_sabs);
+    c->dec_bucket = b + o_bucket;
+    c->dec_chist = (int *)(b + o_chist);
+    c->dec_stage = (int *)(b + o_stage);
+    c->dec_ccount = (int *)(b + o_ccount);
     e = cudaMemset(c->ws_mem, 0, off);
+    if (e == cudaSuccess) {  // k_decode's first token: a histogram scale that covers |s| <= smax
+        int sh0 = 0;
+        while ((c->sel_smax >> sh0) >= 2048) sh0++;
+        std::vector<int> v(desc->n_layers, sh0);
+        e = cudaMemcpy(c->dec_bin_sh, v.data(), 4 * v.size(), cudaMemcpyHostToDevice);
+    }
     if (e == cudaSuccess)  // no previous selection yet: -1 disables the prefetch hint
         e = cudaMemset(c->prev_ids, 0xff, 4 * (size_t)desc->n_layers * (plan->k > 0 ? plan->k : 1));
     static bool attrs_done = false;
@@ -357,6 +394,7 @@ m2c_status m2c_create(const m2c_model_desc *desc, int32_t device, m2c_stream_t c
         e = init_select_attrs();
         if (e == cudaSuccess) e = init_cache_attrs();
         if (e == cudaSuccess) e = init_ffn_attrs();
+        if (e == cudaSuccess) e = init_decode_attrs();
         attrs_done = e == cudaSuccess;
     }
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_lookup, cudaEventDisableTiming);
@@ -453,6 +491,7 @@ m2c_status m2c_load_layer(m2c_ctx *c, int32_t layer, const void *g, const void *
     }
     M2C_CUDA(cudaStreamSynchronize(st));
     L.loaded = true;
+    c->dec_table_dirty = true;
     if (c->graph) {  // topology may have changed
         cudaGraphExecDestroy(c->graph);
         c->graph = nullptr;
@@ -642,6 +681,11 @@ m2c_status m2c_decode_step(m2c_ctx *c, void *x_inout, int64_t step) {
         M2C_CUDA(cudaMemcpyAsync(step_ptr(c), &st32, 4, cudaMemcpyHostToDevice, cs));
     }
     __half *x = static_cast<__half *>(x_inout);
+    if (c->dec_table_dirty) {  // pool / predictor pointers of every layer for k_decode
+        M2C_CUDA(cudaStreamSynchronize(cs));
+        M2C_CUDA(decode_write_layer_table(c, c->dec_layers));
+        c->dec_table_dirty = false;
+    }
     if (c->use_graph) {
         if (c->graph && c->graph_x != x_inout) {
             cudaGraphExecDestroy(c->graph);
@@ -672,6 +716,19 @@ m2c_status m2c_decode_step(m2c_ctx *c, void *x_inout, int64_t step) {
     }
     for (int l = 0; l < c->desc.n_layers; l++)
         if (c->layers[l].mode != 0) c->layers[l].last_step = step;
+    c->decoded = true;
+    return M2C_OK;
+}
+
+m2c_status m2c_decode_lists(m2c_ctx *c, int32_t layer, int32_t *tier_ids_out) {
+    if (!c || !tier_ids_out) return fail(M2C_ERR_INVALID_ARG, "decode_lists: null argument");
+    if (layer < 0 || layer >= c->desc.n_layers) return fail(M2C_ERR_INVALID_ARG, "bad layer");
+    if (c->layers[layer].mode != 0 || !c->decoded)
+        return fail(M2C_ERR_STATE, "decode_lists: no decode step yet, or an LRU/ATU layer");
+    const int k = c->plan.k;
+    if (k > 0)
+        M2C_CUDA(cudaMemcpyAsync(tier_ids_out, c->prev_ids + (size_t)layer * k, 4 * (size_t)k,
+                                 cudaMemcpyDeviceToDevice, c->compute));
     return M2C_OK;
 }
 
@@ -695,10 +752,48 @@ m2c_status m2c_profile_read(m2c_ctx *c, float *ms, int32_t *ffn_launches) {
     if (!c || !ms) return fail(M2C_ERR_INVALID_ARG, "null argument");
     if (c->prof_ev.empty()) return fail(M2C_ERR_STATE, "profiling not enabled");
     M2C_CUDA(cudaStreamSynchronize(c->compute));
+    if (c->last_token_fused) {  // in-kernel per-CTA stamps (ns): see k_decode.cu
+        const int L = c->desc.n_layers, G = c->G, S = kDecodeStamps;
+        std::vector<unsigned long long> t((size_t)S * G * L);
+        M2C_CUDA(cudaMemcpy(t.data(), c->dec_prof, 8 * t.size(), cudaMemcpyDeviceToHost));
+        auto mx = [&](int l, int i) {
+            unsigned long long v = 0;
+            for (int g = 0; g < G; g++) v = std::max(v, t[((size_t)l * G + g) * S + i]);
+            return v;
+        };
+        auto mn = [&](int l, int i) {
+            unsigned long long v = ~0ull;
+            for (int g = 0; g < G; g++) v = std::min(v, t[((size_t)l * G + g) * S + i]);
+            return v;
+        };
+        for (int l = 0; l < L; l++) {
+            const unsigned long long s0 = mn(l, 0), s4 = mx(l, 4), s5 = mx(l, 5), s7 = mx(l, 7);
+            const unsigned long long nx = l + 1 < L ? mn(l + 1, 0) : mx(l, 9);
+            ms[4 * l + 0] = (float)((double)(s4 - s0) * 1e-6);
+            ms[4 * l + 1] = (float)((double)(s5 - s4) * 1e-6);
+            ms[4 * l + 2] = (float)((double)(s7 - s5) * 1e-6);
+            ms[4 * l + 3] = (float)((double)(nx - s7) * 1e-6);
+        }
+        if (ffn_launches) *ffn_launches = 0;
+        return M2C_OK;
+    }
     for (int l = 0; l < c->desc.n_layers; l++)
         for (int i = 0; i < 4; i++)
             M2C_CUDA(cudaEventElapsedTime(&ms[4 * l + i], c->prof_ev[5 * l + i], c->prof_ev[5 * l + i + 1]));
     if (ffn_launches) *ffn_launches = c->layers[0].mode == 0 ? 1 : 2;
+    return M2C_OK;
+}
+
+m2c_status m2c_profile_stamps(m2c_ctx *c, uint64_t *out, int64_t cap, int64_t *n_out) {
+    if (!c || !n_out) return fail(M2C_ERR_INVALID_ARG, "null argument");
+    const int64_t n = (int64_t)kDecodeStamps * c->G * c->desc.n_layers;
+    *n_out = n;
+    if (!out) return M2C_OK;
+    if (cap < n) return fail(M2C_ERR_INVALID_ARG, "profile_stamps: buffer too small");
+    if (c->prof_ev.empty() || !c->last_token_fused)
+        return fail(M2C_ERR_STATE, "profile_stamps: profiling off or last token not on k_decode");
+    M2C_CUDA(cudaStreamSynchronize(c->compute));
+    M2C_CUDA(cudaMemcpy(out, c->dec_prof, 8 * (size_t)n, cudaMemcpyDeviceToHost));
     return M2C_OK;
 }
 
@@ -717,7 +812,11 @@ m2c_status m2c_stats(m2c_ctx *c, int64_t *kpt, int64_t hits[3], int64_t misses[3
     if (reset) M2C_CUDA(cudaMemset(c->ws.stats, 0, sizeof(h)));
     if (err) {
         cudaMemset(c->ws.err, 0, 4);
-        return fail(M2C_ERR_STATE, "device flagged a non-finite input x");
+        std::string m = "device flagged:";
+        if (err & 1) m += " non-finite input x;";
+        if (err & 4) m += " decode grid-barrier timeout;";
+        if (err & 8) m += " decode select count mismatch;";
+        return fail(M2C_ERR_STATE, m);
     }
     return M2C_OK;
 }

@@ -1,0 +1,448 @@
+// ffn_dev.cuh -- device code of the fused dequant-GEMV FFN (a6), shared by k_ffn (API /
+// LRU path) and k_decode (persistent decode kernel).
+//
+// Paper: a neuron is a row of the first FFN matrices and the matching column of the next
+// (P:58); only the active neurons are computed; the cache unit memory "can be
+// directly used for inference computation, avoiding unnecessary copying from the cache to
+// inference tensors"; low-bit neurons are dequantised for compute.  Decode is
+// memory-bound: batch-1 GEMV at ~1 flop/byte, so CUDA cores, not tensor cores.
+//
+// B200 design (one persistent CTA per SM, T = d/8 threads):
+//  * Work split: each CTA owns a contiguous share of the active records (tier order FP16,
+//    INT8, INT4), balanced on bytes + lambda * weights (memory and issue cost both matter:
+//    an INT4 record has 1/4 of the bytes of an FP16 one but the same 3d weights to dequant).
+//  * Records stream into a shared-memory byte ring by 1-D TMA bulk copies (cp.async.bulk,
+//    SASS UBLKCP), one mbarrier per record, issued by one thread as ring space frees; the
+//    issuing thread publishes each record's ring offset, and precomputes the batches.
+//  * Batches of up to 16 records: gate/up dot products are warp-local (one warp, or up to
+//    four warps splitting d, per record; warp-shuffle reductions only), then the
+//    down-projection where thread t owns elements [8t, 8t+8) of y in registers.
+//  * Dequant in registers, ~2 instructions per weight: codes become the fp16 value 1024 + q
+//    (or 1024 + 16q for odd INT4 nibbles) by PRMT/LOP3 (magic-exponent trick); HFMA2 removes
+//    the offset and zero point exactly; fma.rn.f32.f16 (SASS FHFMA) multiplies exact fp16
+//    (q - z) by fp16 x with an exact product and fp32 accumulation.  Per 128-group
+//    s * sum (q - z) x (R5).
+//  * The per-CTA partial y goes to a [G][d] fp32 buffer reduced in a fixed order by k_reduce.
+#pragma once
+#include "m2c_internal.cuh"
+
+namespace m2c {
+namespace {
+
+constexpr int kNBMax = 16;   // records per batch
+constexpr int kNSlot = 32;   // mbarriers (>= records in flight)
+constexpr int kRing = 192 * 1024;
+constexpr int kMaxLocal = 1024;  // records one CTA may own
+constexpr int kXsBytes = 16384;  // x (fp16, d <= 8192)
+// dynamic smem: ring | xs | loc[kMaxLocal] | dsc[kMaxLocal] | bst[kMaxLocal + 1]
+constexpr size_t kSmemBytes = (size_t)kRing + kXsBytes + 4 * (3 * kMaxLocal + 4);
+
+struct FfnArgs {
+    const uint8_t *pool[3];
+    int nb[3];     // record bytes per tier
+    int seg[3];    // tier segment offsets in the item lists
+    int wt[3];     // balancing weight per record (bytes + lambda * 3d), in 16-B units
+};
+
+__device__ __forceinline__ void hfma32(float &acc, uint32_t a, uint32_t b, int ha, int hb) {
+    // acc += a.h[ha] * b.h[hb]  (fp16 x fp16 exact, fp32 accumulate)
+    const uint16_t x = ha ? (uint16_t)(a >> 16) : (uint16_t)a;
+    const uint16_t y = hb ? (uint16_t)(b >> 16) : (uint16_t)b;
+    asm("fma.rn.f32.f16 %0, %1, %2, %0;" : "+f"(acc) : "h"(x), "h"(y));
+}
+__device__ __forceinline__ float h2f_lo(uint32_t v) { return __half2float(__ushort_as_half((uint16_t)v)); }
+__device__ __forceinline__ float h2f_hi(uint32_t v) { return __half2float(__ushort_as_half((uint16_t)(v >> 16))); }
+__device__ __forceinline__ uint32_t hsub2(uint32_t a, uint32_t b) {
+    const __half2 r = __hsub2(*reinterpret_cast<const __half2 *>(&a), *reinterpret_cast<const __half2 *>(&b));
+    return *reinterpret_cast<const uint32_t *>(&r);
+}
+__device__ __forceinline__ uint32_t lop_andor(uint32_t a, uint32_t m, uint32_t c) {
+    uint32_t r;  // (a & m) | c in one LOP3 with register operands
+    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(r) : "r"(a), "r"(m), "r"(c));
+    return r;
+}
+__device__ __forceinline__ float half_bits_f(uint16_t h) { return __half2float(__ushort_as_half(h)); }
+
+// ---- INT8: 8 codes (2 words) -> 4 words of fp16 pairs (q - z) --------------------------
+__device__ __forceinline__ void deq8(uint32_t w0, uint32_t w1, uint32_t zz, uint32_t (&p)[4]) {
+    p[0] = hsub2(__byte_perm(w0, 0x64646464u, 0x4140), zz);  // elements 0, 1
+    p[1] = hsub2(__byte_perm(w0, 0x64646464u, 0x4342), zz);  // 2, 3
+    p[2] = hsub2(__byte_perm(w1, 0x64646464u, 0x4140), zz);  // 4, 5
+    p[3] = hsub2(__byte_perm(w1, 0x64646464u, 0x4342), zz);  // 6, 7
+}
+// ---- INT4: 8 codes (1 word, element m in bits [4m, 4m+4)) -> 4 fp16 pairs --------------
+// p[0] = (e0, e4) - z, p[1] = 16 (e1, e5) - 16 z, p[2] = (e2, e6) - z, p[3] = 16 (e3, e7) - 16 z
+__device__ __forceinline__ void deq4(uint32_t w, uint32_t zz, uint32_t zz16, uint32_t (&p)[4]) {
+    const uint32_t M0 = 0x000F000Fu, M1 = 0x00F000F0u, MAG = 0x64006400u;
+    const uint32_t w8 = w >> 8;
+    p[0] = hsub2(lop_andor(w, M0, MAG), zz);
+    p[1] = hsub2(lop_andor(w, M1, MAG), zz16);
+    p[2] = hsub2(lop_andor(w8, M0, MAG), zz);
+    p[3] = hsub2(lop_andor(w8, M1, MAG), zz16);
+}
+__device__ __forceinline__ uint32_t zz2(uint32_t z) {  // fp16x2 (1024 + z)
+    const uint32_t h = 0x6400u | z;
+    return h | (h << 16);
+}
+__device__ __forceinline__ uint32_t zz2_16(uint32_t z) {  // fp16x2 (1024 + 16 z)
+    const uint32_t h = 0x6400u | (z << 4);
+    return h | (h << 16);
+}
+
+// ---- warp-local partial dot products of one record over chunks [c0, c1) (8 elements each)
+template <int TIER>
+__device__ __forceinline__ void gu_chunks(const uint8_t *rec, const uint4 *xs, int d, int c0, int c1,
+                                          float &pg, float &pu) {
+    const int lane = threadIdx.x & 31;
+    const int G = d >> 7;
+    float ag = 0.f, au = 0.f;
+    for (int c = c0 + lane; c < c1; c += 32) {
+        const uint4 xv = xs[c];
+        const uint32_t xw[4] = {xv.x, xv.y, xv.z, xv.w};
+        if (TIER == 0) {
+            const uint4 gv = *reinterpret_cast<const uint4 *>(rec + 16 * c);
+            const uint4 uv = *reinterpret_cast<const uint4 *>(rec + 2 * d + 16 * c);
+            const uint32_t gw[4] = {gv.x, gv.y, gv.z, gv.w}, uw[4] = {uv.x, uv.y, uv.z, uv.w};
+#pragma unroll
+            for (int i = 0; i < 4; i++) {
+                hfma32(ag, gw[i], xw[i], 0, 0);
+                hfma32(ag, gw[i], xw[i], 1, 1);
+                hfma32(au, uw[i], xw[i], 0, 0);
+                hfma32(au, uw[i], xw[i], 1, 1);
+            }
+        } else {
+            const uint8_t *scales = rec + (TIER == 1 ? 3 * d : 3 * (d >> 1));
+            const uint8_t *zeros = scales + 6 * G;
+            const int grp = c >> 4;
+            const float sg = half_bits_f(*reinterpret_cast<const uint16_t *>(scales + 2 * grp));
+            const float su = half_bits_f(*reinterpret_cast<const uint16_t *>(scales + 2 * (G + grp)));
+            const uint32_t zg = zeros[grp], zu = zeros[G + grp];
+            float tg = 0.f, tu = 0.f;
+            if (TIER == 1) {
+                const uint2 gv = *reinterpret_cast<const uint2 *>(rec + 8 * c);
+                const uint2 uv = *reinterpret_cast<const uint2 *>(rec + d + 8 * c);
+                uint32_t pg_[4], pu_[4];
+                deq8(gv.x, gv.y, zz2(zg), pg_);
+                deq8(uv.x, uv.y, zz2(zu), pu_);
+#pragma unroll
+                for (int i = 0; i < 4; i++) {
+                    hfma32(tg, pg_[i], xw[i], 0, 0);
+                    hfma32(tg, pg_[i], xw[i], 1, 1);
+                    hfma32(tu, pu_[i], xw[i], 0, 0);
+                    hfma32(tu, pu_[i], xw[i], 1, 1);
+                }
+            } else {
+                const uint32_t gw = *reinterpret_cast<const uint32_t *>(rec + 4 * c);
+                const uint32_t uw = *reinterpret_cast<const uint32_t *>(rec + (d >> 1) + 4 * c);
+                uint32_t pg_[4], pu_[4];
+                deq4(gw, zz2(zg), zz2_16(zg), pg_);
+                deq4(uw, zz2(zu), zz2_16(zu), pu_);
+                // x pairs: (e0, e4) = (xw0.lo, xw2.lo), (e1, e5) = (xw0.hi, xw2.hi),
+                //          (e2, e6) = (xw1.lo, xw3.lo), (e3, e7) = (xw1.hi, xw3.hi)
+                float tg16 = 0.f, tu16 = 0.f;
+                hfma32(tg, pg_[0], xw[0], 0, 0);
+                hfma32(tg, pg_[0], xw[2], 1, 0);
+                hfma32(tg16, pg_[1], xw[0], 0, 1);
+                hfma32(tg16, pg_[1], xw[2], 1, 1);
+                hfma32(tg, pg_[2], xw[1], 0, 0);
+                hfma32(tg, pg_[2], xw[3], 1, 0);
+                hfma32(tg16, pg_[3], xw[1], 0, 1);
+                hfma32(tg16, pg_[3], xw[3], 1, 1);
+                hfma32(tu, pu_[0], xw[0], 0, 0);
+                hfma32(tu, pu_[0], xw[2], 1, 0);
+                hfma32(tu16, pu_[1], xw[0], 0, 1);
+                hfma32(tu16, pu_[1], xw[2], 1, 1);
+                hfma32(tu, pu_[2], xw[1], 0, 0);
+                hfma32(tu, pu_[2], xw[3], 1, 0);
+                hfma32(tu16, pu_[3], xw[1], 0, 1);
+                hfma32(tu16, pu_[3], xw[3], 1, 1);
+                tg = fmaf(tg16, 0.0625f, tg);
+                tu = fmaf(tu16, 0.0625f, tu);
+            }
+            ag = fmaf(sg, tg, ag);
+            au = fmaf(su, tu, au);
+        }
+    }
+    pg = ag;
+    pu = au;
+}
+
+__device__ __forceinline__ void gu_any(int tier, const uint8_t *rec, const uint4 *xs, int d, int c0,
+                                       int c1, float &pg, float &pu) {
+    if (tier == 0) gu_chunks<0>(rec, xs, d, c0, c1, pg, pu);
+    else if (tier == 1) gu_chunks<1>(rec, xs, d, c0, c1, pg, pu);
+    else gu_chunks<2>(rec, xs, d, c0, c1, pg, pu);
+}
+
+// ---- y[8t .. 8t+8) += a * deq(down column) --------------------------------------------
+template <int TIER>
+__device__ __forceinline__ void down_t(const uint8_t *rec, int d, float a, float (&y)[8]) {
+    const int t = threadIdx.x;
+    if (TIER == 0) {
+        const uint4 v = *reinterpret_cast<const uint4 *>(rec + 4 * d + 16 * t);
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            y[2 * i] = fmaf(a, h2f_lo(w[i]), y[2 * i]);
+            y[2 * i + 1] = fmaf(a, h2f_hi(w[i]), y[2 * i + 1]);
+        }
+    } else {
+        const int G = d >> 7, grp = t >> 4;
+        const uint8_t *scales = rec + (TIER == 1 ? 3 * d : 3 * (d >> 1));
+        const uint32_t z = (scales + 6 * G)[2 * G + grp];
+        const float as = a * half_bits_f(*reinterpret_cast<const uint16_t *>(scales + 2 * (2 * G + grp)));
+        uint32_t p[4];
+        if (TIER == 1) {
+            const uint2 v = *reinterpret_cast<const uint2 *>(rec + 2 * d + 8 * t);
+            deq8(v.x, v.y, zz2(z), p);
+#pragma unroll
+            for (int i = 0; i < 4; i++) {
+                y[2 * i] = fmaf(as, h2f_lo(p[i]), y[2 * i]);
+                y[2 * i + 1] = fmaf(as, h2f_hi(p[i]), y[2 * i + 1]);
+            }
+        } else {
+            const uint32_t w = *reinterpret_cast<const uint32_t *>(rec + d + 4 * t);
+            deq4(w, zz2(z), zz2_16(z), p);
+            const float as16 = as * 0.0625f;
+            y[0] = fmaf(as, h2f_lo(p[0]), y[0]);
+            y[4] = fmaf(as, h2f_hi(p[0]), y[4]);
+            y[1] = fmaf(as16, h2f_lo(p[1]), y[1]);
+            y[5] = fmaf(as16, h2f_hi(p[1]), y[5]);
+            y[2] = fmaf(as, h2f_lo(p[2]), y[2]);
+            y[6] = fmaf(as, h2f_hi(p[2]), y[6]);
+            y[3] = fmaf(as16, h2f_lo(p[3]), y[3]);
+            y[7] = fmaf(as16, h2f_hi(p[3]), y[7]);
+        }
+    }
+}
+__device__ __forceinline__ void down_any(int tier, const uint8_t *rec, int d, float a, float (&y)[8]) {
+    if (tier == 0) down_t<0>(rec, d, a, y);
+    else if (tier == 1) down_t<1>(rec, d, a, y);
+    else down_t<2>(rec, d, a, y);
+}
+
+// this CTA's share [i0_t, i1_t) of each tier list, balanced on wt (computed by one thread)
+__device__ __forceinline__ void cta_ranges(const FfnArgs &a, int n0, int n1, int n2, int cta, int G,
+                                           int (&r)[6]) {
+    const long long w0 = a.wt[0], w1 = a.wt[1], w2 = a.wt[2];
+    const long long W = n0 * w0 + n1 * w1 + n2 * w2;
+    const long long lo = W * cta / G, hi = W * (cta + 1) / G;
+    const long long base[3] = {0, n0 * w0, n0 * w0 + n1 * w1};
+    const long long ww[3] = {w0, w1, w2};
+    const int nn[3] = {n0, n1, n2};
+#pragma unroll
+    for (int t = 0; t < 3; t++) {
+        long long s0 = lo - base[t], s1 = hi - base[t];
+        s0 = s0 <= 0 ? 0 : (s0 + ww[t] - 1) / ww[t];
+        s1 = s1 <= 0 ? 0 : (s1 + ww[t] - 1) / ww[t];
+        r[2 * t] = (int)(s0 < nn[t] ? s0 : nn[t]);
+        r[2 * t + 1] = (int)(s1 < nn[t] ? s1 : nn[t]);
+    }
+}
+
+struct FfnShared {
+    uint64_t bars[kNSlot];
+    int span[kNSlot];
+    float part[kNBMax][4][2];
+    float a_sm[kNBMax];
+    int cb[5][5];        // chunk bounds: cb[P][p] = nchunk * p / P
+    int rng[8];          // CTA ranges (6)
+    int nbatch;
+    int scan[96];
+    int selv[16];
+};
+
+// table: chunk bounds per split into P parts (constant for a launch)
+__device__ __forceinline__ void ffn_tables(FfnShared &sm, int d) {
+    const int nchunk = d / 8;
+    if (threadIdx.x < 25) {
+        const int P = threadIdx.x / 5, p = threadIdx.x % 5;
+        sm.cb[P][p] = P ? nchunk * p / P : 0;
+    }
+}
+
+// The FFN main loop over this CTA's n_items records; item j -> global record pointer src(j).
+// jb: mbarrier uses so far in this CTA (item j uses barrier (jb + j) % kNSlot in phase
+// ((jb + j) / kNSlot) & 1), so a persistent kernel can run the loop once per layer.
+// x == nullptr: xs already holds x.
+template <class SrcFn>
+__device__ __forceinline__ void ffn_loop(const FfnArgs &a, int d, int act, const __half *x, int n_items,
+                                         int c1, int c2, SrcFn src, uint8_t *ring, uint4 *xs,
+                                         int *dsc, int *bst, FfnShared &sm, float *partial,
+                                         unsigned jb = 0, bool build_tables = true,
+                                         unsigned long long *stamps = nullptr) {
+    const int nwarp = blockDim.x >> 5;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nchunk = d / 8;
+    if (build_tables) ffn_tables(sm, d);
+    // fast path: every record fits the ring at once -> warp 0 issues them in parallel (lane j:
+    // record j, offsets by a warp prefix sum), batches of kNBMax
+    const int total_bytes = c1 * a.nb[0] + (c2 - c1) * a.nb[1] + (n_items - c2) * a.nb[2];
+    const bool fast = n_items <= kNSlot && total_bytes <= kRing;
+    const uint64_t pol = policy_evict_first();
+    if (fast) {
+        if (threadIdx.x < 32) {
+            const int j = threadIdx.x;
+            const int t = j < c1 ? 0 : (j < c2 ? 1 : 2);
+            const int sz = j < n_items ? a.nb[t] : 0;
+            int inc = sz;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, inc, o);
+                if (j >= o) inc += y;
+            }
+            if (j < n_items) {
+                const int off = inc - sz;
+                dsc[j] = off | (t << 24);
+                uint64_t *bar = &sm.bars[(jb + j) % kNSlot];
+                fence_proxy_async();
+                mbar_expect_tx(bar, (uint32_t)sz);
+                bulk_g2s(ring + off, src(j), (uint32_t)sz, bar, pol);
+            }
+            const int nbt = (n_items + kNBMax - 1) / kNBMax;
+            if (j == 0) sm.nbatch = nbt;
+            if (j <= nbt) bst[j] = min(j * kNBMax, n_items);
+        }
+    } else if (threadIdx.x == 0) {
+        // thread 0: batches (consecutive records that fit the ring together, with wrap slack)
+        const int nbA = a.nb[0], nbB = a.nb[1], nbC = a.nb[2];
+        const int mx = nbA > nbB ? (nbA > nbC ? nbA : nbC) : (nbB > nbC ? nbB : nbC);
+        int nbt = 0;
+        for (int j0 = 0; j0 < n_items;) {
+            int nb = 0, bytes = 0;
+            while (nb < kNBMax && j0 + nb < n_items) {
+                const int j = j0 + nb;
+                const int sz = j < c1 ? nbA : (j < c2 ? nbB : nbC);
+                if (nb > 0 && bytes + sz + mx > kRing) break;
+                bytes += sz;
+                nb++;
+            }
+            bst[nbt++] = j0;
+            j0 += nb;
+        }
+        bst[nbt] = n_items;
+        sm.nbatch = nbt;
+    }
+    // producer state (thread 0): bump allocation in the byte ring; publishes dsc[j]
+    int issued = fast ? n_items : 0, pos_issue = 0, used = 0;
+    auto issue_more = [&](int consumed) {
+        while (issued < n_items && issued - consumed < kNSlot) {
+            const int j = issued;
+            const int t = j < c1 ? 0 : (j < c2 ? 1 : 2);
+            const int sz = t == 0 ? a.nb[0] : (t == 1 ? a.nb[1] : a.nb[2]);
+            const bool wrap = pos_issue + sz > kRing;  // (pos_issue == kRing wraps with no waste)
+            const int waste = wrap ? kRing - pos_issue : 0;
+            if (used + waste + sz > kRing) break;
+            const int off = wrap ? 0 : pos_issue;
+            sm.span[(jb + j) % kNSlot] = waste + sz;
+            used += waste + sz;
+            pos_issue = off + sz;
+            dsc[j] = off | (t << 24);
+            uint64_t *bar = &sm.bars[(jb + j) % kNSlot];
+            mbar_expect_tx(bar, (uint32_t)sz);  // release: dsc[j] is visible to its waiters
+            bulk_g2s(ring + off, src(j), (uint32_t)sz, bar, pol);
+            issued++;
+        }
+    };
+    if (threadIdx.x == 0 && !fast) {
+        fence_proxy_async();
+        issue_more(0);
+    }
+    // x -> smem as fp16 (read by the warp-local dot products)
+    if (x)
+        for (int c = threadIdx.x; c < nchunk; c += blockDim.x) xs[c] = reinterpret_cast<const uint4 *>(x)[c];
+    __syncthreads();
+    if (stamps && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(stamps[0]));
+
+    float y[8];
+#pragma unroll
+    for (int i = 0; i < 8; i++) y[i] = 0.f;
+    const int nbt = sm.nbatch;
+    const int P = nchunk >= 512 ? 4 : 1;
+    for (int bi = 0; bi < nbt; bi++) {
+        const int j0 = bst[bi], nb = bst[bi + 1] - j0;
+        // gate/up: units (record b, quarter p) dealt round-robin to the warps (a warp may take
+        // several); each unit ends in a warp-shuffle reduction, quarters combine in order
+        for (int u = warp; u < nb * P; u += nwarp) {
+            const int b = P == 4 ? (u >> 2) : u, pp = P == 4 ? (u & 3) : 0;
+            const int j = j0 + b;
+            mbar_wait(&sm.bars[(jb + j) % kNSlot], (uint32_t)(((jb + j) / kNSlot) & 1));
+            const int ds = dsc[j];
+            float pg, pu;
+            gu_any(ds >> 24, ring + (ds & 0xffffff), xs, d, sm.cb[P][pp], sm.cb[P][pp + 1], pg, pu);
+            pg = warp_sum_f(pg);
+            pu = warp_sum_f(pu);
+            if (lane == 0) {
+                if (P == 1) {
+                    sm.a_sm[b] = (act == 1) ? fmaxf(pg, 0.f) * pu : pg / (1.f + expf(-pg)) * pu;
+                } else {
+                    sm.part[b][pp][0] = pg;
+                    sm.part[b][pp][1] = pu;
+                }
+            }
+        }
+        __syncthreads();
+        if (P > 1) {  // combine the parts of each record, fixed order
+            if (threadIdx.x < nb) {
+                const int b = threadIdx.x;
+                float g = 0.f, u = 0.f;
+                for (int p = 0; p < P; p++) {
+                    g += sm.part[b][p][0];
+                    u += sm.part[b][p][1];
+                }
+                sm.a_sm[b] = (act == 1) ? fmaxf(g, 0.f) * u : g / (1.f + expf(-g)) * u;
+            }
+            __syncthreads();
+        }
+        if (stamps && threadIdx.x == 0 && bi == nbt - 1)
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(stamps[1]));
+        for (int b = 0; b < nb; b++) {
+            const int ds = dsc[j0 + b];
+            down_any(ds >> 24, ring + (ds & 0xffffff), d, sm.a_sm[b], y);
+        }
+        __syncthreads();  // the batch's records are consumed; a_sm/part reusable
+        if (threadIdx.x == 0) {
+            for (int b = 0; b < nb; b++) used -= sm.span[(jb + j0 + b) % kNSlot];
+            fence_proxy_async();
+            issue_more(j0 + nb);
+        }
+    }
+    float *out = partial + (int64_t)blockIdx.x * d + 8 * threadIdx.x;
+    reinterpret_cast<float4 *>(out)[0] = make_float4(y[0], y[1], y[2], y[3]);
+    reinterpret_cast<float4 *>(out)[1] = make_float4(y[4], y[5], y[6], y[7]);
+}
+
+struct SmemPtrs {
+    uint8_t *ring;
+    uint4 *xs;
+    int *loc, *dsc, *bst;
+};
+__device__ __forceinline__ SmemPtrs carve(uint8_t *smem) {
+    SmemPtrs p;
+    p.ring = smem;
+    p.xs = reinterpret_cast<uint4 *>(smem + kRing);
+    p.loc = reinterpret_cast<int *>(smem + kRing + kXsBytes);
+    p.dsc = p.loc + kMaxLocal;
+    p.bst = p.dsc + kMaxLocal;
+    return p;
+}
+
+}  // namespace
+
+// balancing weight of one record, in 16-B units: bytes + lambda * 3d weights.  lambda = 6 B per
+// weight fits the per-CTA FFN times measured inside k_decode (profiles/: ~0.9 us of dequant +
+// FMA per record at any precision plus ~12 ns per KB), i.e. the split is close to per-record.
+constexpr int kLambda = 6;
+static inline int ffn_weight(int64_t nb, int d) { return (int)((nb + (int64_t)kLambda * 3 * d) / 16); }
+static inline void fill_args(m2c_ctx *c, const LayerState &L, const m2c_tier_plan &p, FfnArgs &a) {
+    const int d = c->desc.d_model;
+    const int seg[3] = {0, p.k_fp16, p.k_fp16 + p.k_int8};
+    for (int t = 0; t < 3; t++) {
+        a.pool[t] = L.pool[t];
+        a.nb[t] = (int)c->nb[t];
+        a.seg[t] = seg[t];
+        a.wt[t] = ffn_weight(c->nb[t], d);
+    }
+}
+
+}  // namespace m2c

@@ -28,6 +28,7 @@ m2c_status cuda_fail(cudaError_t e, const char *what);
 
 constexpr int kMaxPoolSlots = 8192;  // LRU / ATU pool limit (single-CTA bitonic victim sort)
 constexpr int kSelectThreads = 1024;
+constexpr int kDecodeStamps = 16;  // k_decode profiling stamps per (layer, CTA)
 
 // ----------------------------------------------------------------------------------------
 // context
@@ -94,12 +95,26 @@ struct m2c_ctx {
     // fused decode-path select: score histogram (s + sel_smax) >> sel_sh into 4096 bins,
     // and the previous token's tier lists per layer (L2 prefetch hint)
     int sel_smax = 0, sel_sh = 0;
-    int *ghist = nullptr;       // [4096]
+    int *ghist = nullptr;       // [2][4096] (the chain uses [0]; k_decode alternates by layer)
     int32_t *prev_ids = nullptr;  // [n_layers][k]
     unsigned long long *sel_status = nullptr;  // [select blocks] decoupled look-back words
     int *sel_done = nullptr;    // select completion counter
     int *sel_epoch = nullptr;   // select launch epoch
     bool use_fused = true;
+    // persistent decode kernel (k_decode): layer pointer table, grid-barrier flags, stamps
+    void *dec_layers = nullptr;
+    unsigned *bar_flags = nullptr;   // [G]
+    unsigned *bar_epoch = nullptr;
+    unsigned long long *dec_prof = nullptr;  // [n_layers][G][kDecodeStamps]
+    int *dec_bin_sh = nullptr;       // [n_layers] k_decode histogram scale per layer
+    void *dec_bucket = nullptr;      // [2][4096][32] int2 (score, id) per histogram bin
+    int *dec_chist = nullptr;        // [2][64] coarse histogram
+    int *dec_stage = nullptr;        // [3][G][ceil(F_r / G)] per-CTA selected ids
+    int *dec_ccount = nullptr;       // [G][4] per-CTA tier counts
+    unsigned *dec_sabs = nullptr;    // [n_layers] max |s| scratch
+    bool dec_table_dirty = true;
+    bool last_token_fused = false;
+    bool decoded = false;            // at least one m2c_decode_step enqueued
     // multi-GPU
     m2c::NcclApi *nccl = nullptr;
     void *comm = nullptr;
@@ -138,6 +153,14 @@ cudaError_t launch_reduce(m2c_ctx *c, int n_partials, const float *partial, cons
                           float *y32, __half *y16, __half *x_next, int *hist_zero, cudaStream_t st);
 cudaError_t launch_finalize(m2c_ctx *c, const float *y32, const __half *x, __half *y16,
                             __half *x_next, cudaStream_t st);
+// persistent decode kernel (k_decode.cu)
+cudaError_t launch_decode(m2c_ctx *c, __half *x, unsigned long long *prof, cudaStream_t st);
+cudaError_t init_decode_attrs();
+cudaError_t decode_write_layer_table(m2c_ctx *c, void *dev_table);
+size_t decode_layer_table_bytes(int n_layers);
+size_t decode_bucket_bytes();
+int decode_coarse_bins();
+int decode_max_F();
 cudaError_t init_select_attrs();
 cudaError_t init_cache_attrs();
 cudaError_t init_ffn_attrs();

@@ -343,16 +343,17 @@ def test_decode_step_equals_api_chain_and_layer0_oracle(m2c):
     assert np.abs(got.astype(np.float64) - x1.astype(np.float64)).max() <= \
         2.0 ** -9 * np.abs(x1.astype(np.float64)).max()
     st = ctx.stats()
-    assert st["kernels_per_token"] >= 4 * L
+    assert st["kernels_per_token"] == 1  # the persistent decode kernel (k_decode)
     ctx.close()
 
 
-@pytest.mark.parametrize("name,layers", [("T", 3), ("S7", 2), ("S70", 1)])
-def test_decode_fused_select_equals_unfused(m2c, name, layers):
-    """The decode path's fused select+FFN kernel (histogram thresholds, L2 prefetch of the
-    previous selection) gives bit-identical tokens to predict_rank's separate select."""
+@pytest.mark.parametrize("name,layers,parts", [("T", 3, 1), ("S7", 2, 1), ("S13", 1, 1),
+                                               ("S70", 1, 8), ("S70", 1, 1)])
+def test_decode_fused_select_equals_unfused(m2c, name, layers, parts):
+    """The persistent decode kernel (grid barriers, in-CTA select from the score histogram,
+    L2 lookahead) gives bit-identical tokens to the per-phase kernel chain."""
     cfg = get_config(name)
-    shard = (0, 8) if name == "S70" else (0, 1)
+    shard = (0, parts)
     plan = m2c.plan_of(cfg, shard[1])
     ctxs = []
     for fused in (True, False):
@@ -370,7 +371,11 @@ def test_decode_fused_select_equals_unfused(m2c, name, layers):
             ctx.decode_step(x, t + 1)
             outs.append(x)
         torch.cuda.synchronize()
+        for l in range(layers):  # the selected tier lists, then the token
+            assert torch.equal(ctxs[0].decode_lists(l), ctxs[1].decode_lists(l)), (t, l)
         assert torch.equal(outs[0], outs[1]), t
+    assert ctxs[0].stats()["kernels_per_token"] == 1  # fused: k_decode; the chain: > 4 per layer
+    assert ctxs[1].stats()["kernels_per_token"] > 4 * layers
     for ctx in ctxs:
         ctx.close()
 
@@ -408,3 +413,35 @@ def test_decode_step_lru_matches_api_chain(m2c):
     assert sum(sa["misses"]) > 0 and sum(sa["hits"]) > 0
     for c in ctxs:
         c.close()
+
+
+@pytest.mark.parametrize("kind", ["zero_x", "tied_B"])
+def test_decode_fused_degenerate_ties(m2c, kind):
+    """Massive score ties: x = 0 (every score 0: the binary-search cut) and a predictor whose
+    B rows repeat in runs of 7 (partial ties at every cut, ranked exactly by id)."""
+    cfg = get_config("S7")
+    L = 2
+    plan = m2c.plan_of(cfg)
+    ctxs = []
+    for fused in (True, False):
+        ctx = _ctx(m2c, cfg, plan, n_layers=L)
+        for l in range(L):
+            w = layer_weights(cfg, l, device="cuda")
+            B = w["pred_B"]
+            if kind == "tied_B":
+                B = B[torch.arange(B.shape[0], device=B.device) // 7 * 7].contiguous()
+            ctx.load_layer(l, w["w_gate"], w["w_up"], w["w_down_t"], w["pred_A"], B)
+        ctx.set_fused(fused)
+        ctxs.append(ctx)
+    xs = token_stream(cfg, 3, device="cuda")
+    for t in range(3):
+        outs = []
+        for ctx in ctxs:
+            x = torch.zeros_like(xs[t]) if kind == "zero_x" else xs[t].contiguous().clone()
+            ctx.decode_step(x, t + 1)
+            outs.append(x)
+        torch.cuda.synchronize()
+        assert torch.equal(outs[0], outs[1]), t
+    for ctx in ctxs:
+        ctx.stats()  # raises if the device flagged an error (barrier timeout, count mismatch)
+        ctx.close()
