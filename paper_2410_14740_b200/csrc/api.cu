@@ -331,8 +331,8 @@ m2c_status m2c_create(const m2c_model_desc *desc, int32_t device, m2c_stream_t c
                  o_sdone = take(4), o_sepoch = take(4), o_bflags = take(4 * (size_t)c->G),
                  o_bepoch = take(4), o_dlay = take(decode_layer_table_bytes(desc->n_layers)),
                  o_dprof = take(8 * (size_t)kDecodeStamps * c->G * desc->n_layers),
-                 o_binsh = take(4 * (size_t)desc->n_layers), o_sabs = take(4 * (size_t)desc->n_layers),
-                 o_bucket = take(decode_bucket_bytes()), o_chist = take(4 * 2 * (size_t)decode_coarse_bins()),
+                 o_binsh = take(4 * (size_t)desc->n_layers), o_sabs = take(4 * (size_t)c->G),
+                 o_bucket = take(decode_bucket_bytes()),
                  o_stage = take(4 * 3 * (size_t)c->G * ((F_r + c->G - 1) / c->G)),
                  o_ccount = take(16 * (size_t)c->G),
                  o_prev = take(4 * (size_t)desc->n_layers * (plan->k > 0 ? plan->k : 1));
@@ -377,7 +377,6 @@ m2c_status m2c_create(const m2c_model_desc *desc, int32_t device, m2c_stream_t c
     c->dec_bin_sh = (int *)(b + o_binsh);
     c->dec_sabs = (unsigned *)(b + o_sabs);
     c->dec_bucket = b + o_bucket;
-    c->dec_chist = (int *)(b + o_chist);
     c->dec_stage = (int *)(b + o_stage);
     c->dec_ccount = (int *)(b + o_ccount);
     e = cudaMemset(c->ws_mem, 0, off);

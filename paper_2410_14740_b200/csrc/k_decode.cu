@@ -69,11 +69,10 @@ struct DecArgs {
     unsigned long long *prof;   // [n_layers][G][kStamps] globaltimer stamps, or null
     int prefetch;
     int2 *bucket;               // [2][4096][kBucket] (score, id) per bin (layer parity)
-    int *chist;                 // [2][kCoarse] coarse histogram
     int *stage;                 // [3][G][ceil(F_r / G)] per-CTA compacted selected ids
     int *ccount;                // [G][4] per-CTA tier counts
     int *bin_sh;                // [n_layers] histogram scale per layer (adapted token to token)
-    unsigned *sabs;             // [n_layers] max |s| of the current token (atomicMax)
+    unsigned *sabs;             // [G] per-CTA max |s| of the current layer
 };
 
 // histogram bin of a raw score: monotone, clamped; 2^sh-wide bins centred on 0
@@ -342,7 +341,6 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
             unsigned amax = 0;
             int *own = reinterpret_cast<int *>(S.ring + kOwnOff);  // this CTA's scores (P3)
             int2 *bkt = p.bucket + (size_t)(l & 1) * kBins * kBucket;
-            int *chs = p.chist + (l & 1) * kCoarse;
             while (nb0 < n1) {
                 int accs[kPass];
 #pragma unroll
@@ -366,7 +364,6 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
                             p.s[n] = accs[i];
                             own[n - n0] = accs[i];
                             slot[i] = atomicAdd(&hist[bin[i]], 1);
-                            atomicAdd(&chs[bin[i] >> 6], 1);
                             amax = max(amax, (unsigned)abs(accs[i]));
                         }
                     }
@@ -378,25 +375,24 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
                 nb0 += kPass * step;
                 if (nb0 < n1) load_b();
             }
-            amax = __reduce_max_sync(0xffffffffu, amax);
-            if (lane == 0 && amax) atomicMax(p.sabs + l, amax);
+            amax = block_max_u(amax, red_u);  // one plain store per CTA (no same-address atomics)
+            if (tid == 0) p.sabs[cta] = amax;
         }
         STAMP(3);
         grid_sync(p.bar_flags, base + ++nbar, p.err);
         STAMP(4);
         // next token's histogram scale for this layer: |s| < 2048 << sh (no clamped bins)
-        if (cta == 0 && tid == 0) {
-            const unsigned m = __ldcg(p.sabs + l);
-            p.sabs[l] = 0;
+        if (cta == 0 && warp == 0) {
+            unsigned m = 0;
+            for (int c = lane; c < G; c += 32) m = max(m, __ldcg(p.sabs + c));
+            m = __reduce_max_sync(0xffffffffu, m);
             int sh = 0;
             while ((m >> sh) >= 2048u) sh++;
-            p.bin_sh[l] = sh;
+            if (lane == 0) p.bin_sh[l] = sh;
         }
         // the other histogram buffer was last read in layer l-1's P3: clear it for layer l+1
-        if (cta == G - 1) {
+        if (cta == G - 1)
             for (int i = tid; i < kBins; i += NT) p.ghist[((l + 1) & 1) * kBins + i] = 0;
-            for (int i = tid; i < kCoarse; i += NT) p.chist[((l + 1) & 1) * kCoarse + i] = 0;
-        }
 
         // ================= P3a: exact cuts (every CTA), classify own neurons, publish ========
         // Cut t (t = 0, 1, 2: the k16-th, (k16+k8)-th and k-th score in (score desc, id asc)
@@ -406,19 +402,22 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
         // ties) falls back to block-wide binary searches over all scores.
         {
             const int2 *bkt = p.bucket + (size_t)(l & 1) * kBins * kBucket;
-            const int *chs = p.chist + (l & 1) * kCoarse;
             if (tid < 3) {
                 cut_V[tid] = 0x7fffffff;  // empty cut: nothing is above it
                 cut_I[tid] = -1;
                 cut_bin[tid] = -1;
                 ncand[tid] = 0;
             }
-            // both histograms -> smem in one round of 16-B loads (fine [4096] | coarse [64])
+            // the histogram -> smem in one round of 16-B loads; coarse sums of 64 bins after it
             int *hs = reinterpret_cast<int *>(S.ring + kSbufOff);
 #pragma unroll 4
-            for (int i = tid; i < (kBins + kCoarse) / 4; i += NT)
-                reinterpret_cast<int4 *>(hs)[i] = i < kBins / 4 ? __ldcg(reinterpret_cast<const int4 *>(hist) + i)
-                                                                : __ldcg(reinterpret_cast<const int4 *>(chs) + i - kBins / 4);
+            for (int i = tid; i < kBins / 4; i += NT)
+                reinterpret_cast<int4 *>(hs)[i] = __ldcg(reinterpret_cast<const int4 *>(hist) + i);
+            __syncthreads();
+            for (int cidx = warp; cidx < kCoarse; cidx += NW) {
+                const int v = __reduce_add_sync(0xffffffffu, hs[64 * cidx + lane] + hs[64 * cidx + 32 + lane]);
+                if (lane == 0) hs[kBins + cidx] = v;
+            }
             __syncthreads();
             for (int t = warp; t < 3; t += NW) {
                 if (tg[t] <= 0) continue;
@@ -635,10 +634,8 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
         STAMP(6);
         grid_sync(p.bar_flags, base + ++nbar, p.err);
         STAMP(7);
-        if (l == p.n_layers - 1 && cta == G - 1) {  // leave both histograms clear for the next token
+        if (l == p.n_layers - 1 && cta == G - 1)  // leave both histograms clear for the next token
             for (int i = tid; i < kBins; i += NT) hist[i] = 0;
-            for (int i = tid; i < kCoarse; i += NT) p.chist[(l & 1) * kCoarse + i] = 0;
-        }
 
         // ================= P5: fixed-order reduction + residual ==========================
         {
@@ -691,7 +688,6 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
 
 size_t decode_layer_table_bytes(int n_layers) { return sizeof(DecLayer) * (size_t)n_layers; }
 size_t decode_bucket_bytes() { return (size_t)2 * kBins * kBucket * sizeof(int2); }
-int decode_coarse_bins() { return kCoarse; }
 // scores fit the fallback buffer; a CTA's own neurons fit one pass of its threads and kOwnOff
 int decode_max_F() { return (kRing - kSbufOff) / 4; }
 
@@ -745,7 +741,6 @@ cudaError_t launch_decode(m2c_ctx *c, __half *x, unsigned long long *prof, cudaS
     a.prof = prof;
     a.bin_sh = c->dec_bin_sh;
     a.bucket = reinterpret_cast<int2 *>(c->dec_bucket);
-    a.chist = c->dec_chist;
     a.stage = c->dec_stage;
     a.ccount = c->dec_ccount;
     a.sabs = c->dec_sabs;

@@ -108,10 +108,9 @@ struct m2c_ctx {
     unsigned long long *dec_prof = nullptr;  // [n_layers][G][kDecodeStamps]
     int *dec_bin_sh = nullptr;       // [n_layers] k_decode histogram scale per layer
     void *dec_bucket = nullptr;      // [2][4096][32] int2 (score, id) per histogram bin
-    int *dec_chist = nullptr;        // [2][64] coarse histogram
     int *dec_stage = nullptr;        // [3][G][ceil(F_r / G)] per-CTA selected ids
     int *dec_ccount = nullptr;       // [G][4] per-CTA tier counts
-    unsigned *dec_sabs = nullptr;    // [n_layers] max |s| scratch
+    unsigned *dec_sabs = nullptr;    // [G] per-CTA max |s| scratch
     bool dec_table_dirty = true;
     bool last_token_fused = false;
     bool decoded = false;            // at least one m2c_decode_step enqueued
@@ -159,7 +158,6 @@ cudaError_t init_decode_attrs();
 cudaError_t decode_write_layer_table(m2c_ctx *c, void *dev_table);
 size_t decode_layer_table_bytes(int n_layers);
 size_t decode_bucket_bytes();
-int decode_coarse_bins();
 int decode_max_F();
 cudaError_t init_select_attrs();
 cudaError_t init_cache_attrs();
