@@ -20,7 +20,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and os.path.exists(out) and all(os.path.getmtime(out) >= os.path.getmtime(p) for p in deps):
         return out
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-    cmd = [nvcc, *NVCC_FLAGS, "-o", out + ".tmp", *srcs, "-ldl"]
+    extra = os.environ.get("M2C_NVCC_EXTRA", "").split()  # measurement builds (tools/) only
+    cmd = [nvcc, *NVCC_FLAGS, *extra, "-o", out + ".tmp", *srcs, "-ldl"]
     if verbose:
         print(" ".join(cmd))
     subprocess.check_call(cmd)

@@ -221,6 +221,20 @@ __device__ __forceinline__ void down_any(int tier, const uint8_t *rec, int d, fl
     else down_t<2>(rec, d, a, y);
 }
 
+// down-projection of batch records [ja, jb) of one tier (j0: the batch's first record)
+template <int TIER>
+__device__ __forceinline__ void down_seg(const uint8_t *ring, const int *dsc, const float *a_sm, int j0,
+                                         int ja, int jb, int d, float (&y)[8]) {
+    int j = ja;
+    for (; j + 1 < jb; j += 2) {
+        const int d0 = dsc[j], d1 = dsc[j + 1];
+        const float a0 = a_sm[j - j0], a1 = a_sm[j + 1 - j0];
+        down_t<TIER>(ring + (d0 & 0xffffff), d, a0, y);
+        down_t<TIER>(ring + (d1 & 0xffffff), d, a1, y);
+    }
+    if (j < jb) down_t<TIER>(ring + (dsc[j] & 0xffffff), d, a_sm[j - j0], y);
+}
+
 // this CTA's share [i0_t, i1_t) of each tier list, balanced on wt (computed by one thread)
 __device__ __forceinline__ void cta_ranges(const FfnArgs &a, int n0, int n1, int n2, int cta, int G,
                                            int (&r)[6]) {
@@ -295,7 +309,8 @@ __device__ __forceinline__ void ffn_loop(const FfnArgs &a, int d, int act, const
                 const int off = inc - sz;
                 dsc[j] = off | (t << 24);
                 uint64_t *bar = &sm.bars[(jb + j) % kNSlot];
-                fence_proxy_async();
+                // no proxy fence: callers order earlier generic ring writes (k_decode fences
+                // before its FFN phase; k_ffn's ring has none)
                 mbar_expect_tx(bar, (uint32_t)sz);
                 bulk_g2s(ring + off, src(j), (uint32_t)sz, bar, pol);
             }
@@ -369,7 +384,12 @@ __device__ __forceinline__ void ffn_loop(const FfnArgs &a, int d, int act, const
             mbar_wait(&sm.bars[(jb + j) % kNSlot], (uint32_t)(((jb + j) / kNSlot) & 1));
             const int ds = dsc[j];
             float pg, pu;
+#ifdef M2C_EXP_SKIP_GU  // measurement build only (tools/): data arrival without the dot products
+            pg = pu = 0.f;
+            (void)ds;
+#else
             gu_any(ds >> 24, ring + (ds & 0xffffff), xs, d, sm.cb[P][pp], sm.cb[P][pp + 1], pg, pu);
+#endif
             pg = warp_sum_f(pg);
             pu = warp_sum_f(pu);
             if (lane == 0) {
@@ -396,9 +416,12 @@ __device__ __forceinline__ void ffn_loop(const FfnArgs &a, int d, int act, const
         }
         if (stamps && threadIdx.x == 0 && bi == nbt - 1)
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(stamps[1]));
-        for (int b = 0; b < nb; b++) {
-            const int ds = dsc[j0 + b];
-            down_any(ds >> 24, ring + (ds & 0xffffff), d, sm.a_sm[b], y);
+        {  // per tier segment of the batch, two records per step (independent loads in flight)
+            const int je = j0 + nb;
+            const int s1 = min(max(c1, j0), je), s2 = min(max(c2, j0), je);
+            down_seg<0>(ring, dsc, sm.a_sm, j0, j0, s1, d, y);
+            down_seg<1>(ring, dsc, sm.a_sm, j0, s1, s2, d, y);
+            down_seg<2>(ring, dsc, sm.a_sm, j0, s2, je, d, y);
         }
         __syncthreads();  // the batch's records are consumed; a_sm/part reusable
         if (threadIdx.x == 0) {

@@ -36,14 +36,15 @@ namespace {
 constexpr int kBins = 4096;
 // profiling stamps per (layer, CTA): 0 layer start, 1 P1 done, 2 after B1, 3 P2 done, 4 after
 // B2, 5 P3 done, 6 P4 done, 7 after B4, 8 P5 done, 9 kernel end (last layer only); P3 steps:
-// 10 cuts exact, 11 own neurons classified + published, 12 after B3, 13 list share gathered
+// 10 cuts exact, 11 own neurons classified + published, 12 after barrier 3, 13 list share
+// gathered.  (Publishing the counts as tagged words polled by every CTA instead of barrier 3
+// measured slower: 148 x 148 pollers on ten cache lines.)
 constexpr int kStamps = kDecodeStamps;
 constexpr int kBucket = 32;       // (score, id) pairs kept per histogram bin
 constexpr int kCoarse = 64;       // coarse bins (64 fine bins each)
-// ring-aliased scratch of P1..P3 (bytes): xq [0, 8K) | hq [8K, 8.5K) | own scores | prefixes |
-// all scores (degenerate-tie fallback only)
+// ring-aliased scratch of P1..P3 (bytes): xq [0, 8K) | hq [8K, 8.5K) | own scores | from 32K:
+// histogram (P3a), all scores (degenerate-tie fallback), per-CTA counts (P3b)
 constexpr int kOwnOff = 9216;     // <= 4096 ints: this CTA's scores
-constexpr int kPreOff = 25600;    // [3][G + 1] ints
 constexpr int kSbufOff = 32768;   // [F_r] ints
 
 struct DecLayer {
@@ -129,9 +130,7 @@ __device__ __forceinline__ int block_max_u(unsigned v, unsigned *sm32) {
     __syncthreads();
     if (lane == 0) sm32[warp] = v;
     __syncthreads();
-    unsigned m = sm32[0];
-    for (int w = 1; w < nw; w++) m = max(m, sm32[w]);
-    return (int)m;
+    return (int)__reduce_max_sync(0xffffffffu, lane < nw ? sm32[lane] : 0u);
 }
 __device__ __forceinline__ int block_sum(int v, int *sm32) {
     v = __reduce_add_sync(0xffffffffu, v);
@@ -139,10 +138,45 @@ __device__ __forceinline__ int block_sum(int v, int *sm32) {
     __syncthreads();
     if (lane == 0) sm32[warp] = v;
     __syncthreads();
-    int s = 0;
-    for (int w = 0; w < nw; w++) s += sm32[w];
-    return s;
+    return __reduce_add_sync(0xffffffffu, lane < nw ? sm32[lane] : 0);
 }
+// exclusive block scan of 3 ints (any blockDim multiple of 32, <= 1024); totals in tot
+__device__ __forceinline__ void block_exscan3(const int v[3], int ex[3], int tot[3], int *sm /*[3][32]*/) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    int inc[3];
+#pragma unroll
+    for (int t = 0; t < 3; t++) {
+        int x = v[t];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        inc[t] = x;
+        if (lane == 31) sm[t * 32 + warp] = x;
+    }
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+        for (int t = 0; t < 3; t++) {
+            int x = lane < nw ? sm[t * 32 + lane] : 0;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            sm[t * 32 + lane] = x;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int t = 0; t < 3; t++) {
+        ex[t] = (warp ? sm[t * 32 + warp - 1] : 0) + inc[t] - v[t];
+        tot[t] = sm[t * 32 + nw - 1];
+    }
+    __syncthreads();
+}
+
 __device__ __forceinline__ int q127_f32(float a, float M, float inv) {  // a = |v| >= 0, M > 0
     int q = (int)fmaf(a, inv, 0.5f);
     const float a254 = 254.f * a;
@@ -309,21 +343,19 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
         const int shl = __ldcg(p.bin_sh + l);  // this token's histogram scale for layer l
         {
             int8_t *hq = reinterpret_cast<int8_t *>(S.ring) + 8192;
-            const int LPR = r / 16, npw = 32 / LPR;
-            const int part = lane % LPR, sub = lane / LPR;
+            // lanes per neuron LPN, 16-B chunks per lane CPL (r = 256: 4 x 4; r = 32: 1 x 2)
+            const int C16 = r / 16, CPL = C16 >= 4 ? 4 : C16, LPN = C16 / CPL, npw = 32 / LPN;
+            const int part = lane % LPN, sub = lane / LPN;
             const int rps = (F_r + G - 1) / G;
             const int n0 = cta * rps, n1 = min(F_r, n0 + rps);
-            constexpr int kPass = 4;  // B loads of up to 4 passes in flight, issued before h
             const int step = NW * npw;
             int nb0 = n0 + warp * npw;
-            int4 bv[kPass];
-            auto load_b = [&]() {
+            int4 bv[4];
+            auto load_b = [&]() {  // B loads are independent of h: issued first
+                const int n = nb0 + sub;
+                const int4 *b4 = reinterpret_cast<const int4 *>(Ld.B + (int64_t)n * r) + part * CPL;
 #pragma unroll
-                for (int i = 0; i < kPass; i++) {
-                    const int n = nb0 + i * step + sub;
-                    bv[i] = n < n1 ? __ldg(reinterpret_cast<const int4 *>(Ld.B + (int64_t)n * r) + part)
-                                   : make_int4(0, 0, 0, 0);
-                }
+                for (int c = 0; c < 4; c++) bv[c] = (c < CPL && n < n1) ? __ldg(b4 + c) : make_int4(0, 0, 0, 0);
             };
             load_b();
             int hv0 = tid < r ? __ldcg(p.h + tid) : 0;
@@ -337,42 +369,32 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
                 hq[i] = (int8_t)(hv < 0 ? -q : q);
             }
             __syncthreads();
-            const int4 hv4 = reinterpret_cast<const int4 *>(hq)[part];
+            const int4 *hq4 = reinterpret_cast<const int4 *>(hq) + part * CPL;
             unsigned amax = 0;
             int *own = reinterpret_cast<int *>(S.ring + kOwnOff);  // this CTA's scores (P3)
             int2 *bkt = p.bucket + (size_t)(l & 1) * kBins * kBucket;
             while (nb0 < n1) {
-                int accs[kPass];
+                int acc = 0;
 #pragma unroll
-                for (int i = 0; i < kPass; i++) {
-                    int acc = 0;
-                    acc = __dp4a(bv[i].x, hv4.x, acc);
-                    acc = __dp4a(bv[i].y, hv4.y, acc);
-                    acc = __dp4a(bv[i].z, hv4.z, acc);
-                    acc = __dp4a(bv[i].w, hv4.w, acc);
-                    for (int o = LPR / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-                    accs[i] = acc;
-                }
-                if (part == 0) {  // all atomics of the passes in flight before their results are used
-                    int slot[kPass], bin[kPass];
-#pragma unroll
-                    for (int i = 0; i < kPass; i++) {
-                        const int n = nb0 + i * step + sub;
-                        slot[i] = kBucket;
-                        bin[i] = bin_of(accs[i], shl);
-                        if (n < n1) {
-                            p.s[n] = accs[i];
-                            own[n - n0] = accs[i];
-                            slot[i] = atomicAdd(&hist[bin[i]], 1);
-                            amax = max(amax, (unsigned)abs(accs[i]));
-                        }
+                for (int c = 0; c < 4; c++)
+                    if (c < CPL) {
+                        const int4 hv4 = hq4[c];
+                        acc = __dp4a(bv[c].x, hv4.x, acc);
+                        acc = __dp4a(bv[c].y, hv4.y, acc);
+                        acc = __dp4a(bv[c].z, hv4.z, acc);
+                        acc = __dp4a(bv[c].w, hv4.w, acc);
                     }
-#pragma unroll
-                    for (int i = 0; i < kPass; i++)
-                        if (slot[i] < kBucket)
-                            bkt[(size_t)bin[i] * kBucket + slot[i]] = make_int2(accs[i], nb0 + i * step + sub);
+                for (int o = LPN / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+                const int n = nb0 + sub;
+                if (part == 0 && n < n1) {
+                    const int b = bin_of(acc, shl);
+                    p.s[n] = acc;
+                    own[n - n0] = acc;
+                    amax = max(amax, (unsigned)abs(acc));
+                    const int slot = atomicAdd(&hist[b], 1);
+                    if (slot < kBucket) bkt[(size_t)b * kBucket + slot] = make_int2(acc, n);
                 }
-                nb0 += kPass * step;
+                nb0 += step;
                 if (nb0 < n1) load_b();
             }
             amax = block_max_u(amax, red_u);  // one plain store per CTA (no same-address atomics)
@@ -566,27 +588,24 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
         // ================= P3b: this CTA's share of the tier lists ============================
         int n_items, c1, c2;
         {
-            int *pre = reinterpret_cast<int *>(S.ring + kPreOff);  // [3][G + 1] exclusive prefixes
-            int *cc = reinterpret_cast<int *>(S.ring + kSbufOff);   // [G][4] counts, one load round
-            for (int i = tid; i < G; i += NT) reinterpret_cast<int4 *>(cc)[i] = __ldcg(reinterpret_cast<const int4 *>(p.ccount) + i);
-            __syncthreads();
-            for (int t = warp; t < 3; t += NW) {  // warp t scans tier t's per-CTA counts
-                int carry = 0;
-                for (int c0 = 0; c0 < G; c0 += 32) {
-                    const int c = c0 + lane;
-                    const int v = c < G ? cc[c * 4 + t] : 0;
-                    int inc = v;
+            // thread-contiguous source CTAs: their counts (one 16-B load each), a block scan of
+            // the three tier counts -> each source's list offsets; every thread copies the part of
+            // its sources' ids that falls into this CTA's share [lo_t, hi_t)
+            constexpr int kMaxCPT = 5;  // G <= 160, blockDim >= 32
+            const int CPT = (G + NT - 1) / NT;
+            const int cA = min(G, tid * CPT), cB = min(G, cA + CPT);
+            int4 *cc = reinterpret_cast<int4 *>(S.ring + kSbufOff);  // this thread's sources' counts
+            int sum3[3] = {0, 0, 0};
 #pragma unroll
-                    for (int o = 1; o < 32; o <<= 1) {
-                        const int y = __shfl_up_sync(0xffffffffu, inc, o);
-                        if (lane >= o) inc += y;
-                    }
-                    if (c < G) pre[t * (G + 1) + c] = carry + inc - v;
-                    carry += __shfl_sync(0xffffffffu, inc, 31);
-                }
-                if (lane == 0) pre[t * (G + 1) + G] = carry;
-            }
-            __syncthreads();
+            for (int k = 0; k < kMaxCPT; k++) {
+                const int4 q = (k < CPT && cA + k < cB) ? __ldcg(reinterpret_cast<const int4 *>(p.ccount) + cA + k)
+                                                        : make_int4(0, 0, 0, 0);
+                if (k < CPT && cA + k < cB) cc[cA + k] = q;
+                sum3[0] += q.x;
+                sum3[1] += q.y;
+                sum3[2] += q.z;
+            }            int ex[3], tot[3];
+            block_exscan3(sum3, ex, tot, scan_sm);
             int rg[6];
 #pragma unroll
             for (int i = 0; i < 6; i++) rg[i] = sm.rng[i];
@@ -595,22 +614,35 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
             c2 = off2;
             n_items = off2 + rg[5] - rg[4];
             const int rps = (F_r + G - 1) / G;
-            for (int j = tid; j < n_items; j += NT) {
-                const int t = j < off1 ? 0 : (j < off2 ? 1 : 2);
-                const int pos = j - (t == 0 ? 0 : (t == 1 ? off1 : off2)) + rg[2 * t];
-                const int *pt = pre + t * (G + 1);
-                int lo = 0, hi = G - 1;  // last CTA c with pt[c] <= pos
-                while (lo < hi) {
-                    const int mid = (lo + hi + 1) >> 1;
-                    if (pt[mid] <= pos) lo = mid;
-                    else hi = mid - 1;
+            const int offs[3] = {0, off1, off2};
+            const int segs[3] = {0, p.k16, p.k16 + p.k8};
+#pragma unroll
+            for (int k = 0; k < kMaxCPT; k++) {
+                if (k >= CPT || cA + k >= cB) break;
+                const int c = cA + k;
+                const int4 q = cc[c];
+                const int cnt[3] = {q.x, q.y, q.z};
+#pragma unroll
+                for (int t = 0; t < 3; t++) {
+                    const int s0 = ex[t];
+                    ex[t] += cnt[t];
+                    const int a = max(rg[2 * t], s0), b = min(rg[2 * t + 1], s0 + cnt[t]);
+                    const int *src = p.stage + ((size_t)t * G + c) * rps - s0;
+                    for (int pos0 = a; pos0 < b; pos0 += 8) {
+                        int ids[8];
+#pragma unroll
+                        for (int u = 0; u < 8; u++) ids[u] = pos0 + u < b ? __ldcg(src + pos0 + u) : 0;
+#pragma unroll
+                        for (int u = 0; u < 8; u++)
+                            if (pos0 + u < b) {
+                                S.loc[offs[t] + pos0 + u - rg[2 * t]] = ids[u];
+                                lst[segs[t] + pos0 + u] = ids[u];
+                            }
+                    }
                 }
-                const int id = __ldcg(p.stage + ((size_t)t * G + lo) * rps + (pos - pt[lo]));
-                S.loc[j] = id;
-                lst[(t == 0 ? 0 : (t == 1 ? p.k16 : p.k16 + p.k8)) + pos] = id;
             }
             if (tid == 0) {
-                if (pre[G] != p.k16 || pre[2 * G + 1] != p.k8 || pre[3 * G + 2] != p.k4) atomicOr(p.err, 8u);
+                if (tot[0] != p.k16 || tot[1] != p.k8 || tot[2] != p.k4) atomicOr(p.err, 8u);
                 for (int t = 0; t < 3; t++) fa.pool[t] = Ld.pool[t];
             }
             STAMP(13);

@@ -17,6 +17,36 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
     return v;
 }
 
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ unsigned cluster_rank() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ unsigned cluster_nrank() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+    return r;
+}
+
+// mode 3: cluster barrier, one arrival + one poller per cluster, cluster barrier to release
+__global__ void k_bar_cluster(unsigned *buf, int iters, unsigned long long *out) {
+    const unsigned ncl = gridDim.x / cluster_nrank();
+    unsigned long long t0 = clock64();
+    for (int it = 1; it <= iters; it++) {
+        cluster_sync_all();
+        if (cluster_rank() == 0 && threadIdx.x == 0) {
+            asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(buf + 256) : "memory");
+            while ((int)(ld_acquire(buf + 256) - (unsigned)(it * ncl)) < 0) {
+            }
+        }
+        cluster_sync_all();
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) *out = clock64() - t0;
+}
+
 template <int MODE>
 __global__ void k_bar(unsigned *buf, int iters, unsigned long long *out) {
     const int G = gridDim.x;
@@ -91,5 +121,38 @@ int main() {
             printf("mode %d threads %4d: %s  %.3f us/barrier (event), %.0f cycles/barrier\n", mode, nt,
                    cudaGetErrorString(e), ms * 1e3 / iters, (double)h / iters);
         }
+    for (int cs : {2, 4}) {
+        for (int nt : {512, 1024}) {
+            cudaMemset(buf, 0, 4 * 2048);
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(sms);
+            cfg.blockDim = dim3(nt);
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = cs;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            int ncl = 0;
+            cudaOccupancyMaxActiveClusters(&ncl, k_bar_cluster, &cfg);
+            if (ncl * cs < sms) {
+                printf("cluster %d threads %4d: only %d clusters co-resident, skipped\n", cs, nt, ncl);
+                continue;
+            }
+            cudaEvent_t e0, e1;
+            cudaEventCreate(&e0);
+            cudaEventCreate(&e1);
+            cudaEventRecord(e0);
+            cudaError_t e = cudaLaunchKernelEx(&cfg, k_bar_cluster, buf, iters, out);
+            cudaEventRecord(e1);
+            cudaEventSynchronize(e1);
+            float ms = 0;
+            cudaEventElapsedTime(&ms, e0, e1);
+            cudaMemcpy(&h, out, 8, cudaMemcpyDeviceToHost);
+            printf("cluster %d threads %4d (%d clusters fit): %s  %.3f us/barrier\n", cs, nt, ncl,
+                   cudaGetErrorString(e), ms * 1e3 / iters);
+        }
+    }
     return 0;
 }
