@@ -205,11 +205,14 @@ m2c_status m2c_set_fused(m2c_ctx *ctx, int32_t enable);
  * step, ms[l*4 + {0,1,2,3}] = predictor, select, cache lookup + FFN, reduce/all-reduce/residual
  * of layer l (k_decode: measured on the slowest CTA, barriers included in the phase they
  * end).  ffn_launches_out = FFN kernel launches per layer (0 for k_decode).
- * m2c_profile_stamps copies k_decode's raw stamps, uint64 ns [n_layers][G][16] (0 layer start,
- * 1 P1 done, 2 after barrier 1, 3 P2 done, 4 after barrier 2, 5 select done, 6 FFN done,
- * 7 after barrier 3, 8 reduce done, 9 kernel end, 10..13 select sub-steps, 14..15 unused);
+ * m2c_profile_stamps copies k_decode's raw stamps, uint64 ns [n_layers][G][M2C_DECODE_STAMPS]
+ * (0 layer start, 1 scores done, 4 after barrier Bs, 2/3/16/10 select sub-steps (runs in smem,
+ * cut bins, candidates, exact cuts), 18/19/11 list sub-steps, 5 select done, 14/15 FFN
+ * sub-steps, 6 FFN done, 7 after barrier By, 8 reduction + next h done, 9 kernel end,
+ * 12/13 prologue start / end (layer 0); stamps not listed are unused and hold garbage);
  * *n_out = the element count (out may be null to query it); M2C_ERR_STATE if the last step
  * did not run on k_decode with profiling. */
+#define M2C_DECODE_STAMPS 24
 m2c_status m2c_profile(m2c_ctx *ctx, int32_t enable);
 m2c_status m2c_profile_read(m2c_ctx *ctx, float *ms, int32_t *ffn_launches_out);
 m2c_status m2c_profile_stamps(m2c_ctx *ctx, uint64_t *out, int64_t cap, int64_t *n_out);

@@ -18,7 +18,7 @@
  *
  * Pins (tests/test_oracle_*.py): fp16 conversions vs numpy float16; O0 vs the
  * hand-verified worked examples in tests/golden/quant_examples.txt and closed
- * form invariants; O1-O4 vs numpy int64 matmul; O5 vs python sorted();
+ * form invariants; O1-O4 vs python big-integer matmul and exact rationals; O5 vs python sorted();
  * O6 vs numpy float64 dense FFN (100% active, FP16 tier) and gather-matmul;
  * O7 vs an independently written move-to-front list LRU and SPEC's examples.
  */
@@ -234,39 +234,48 @@ int orc_dequant_record(int bits, int d, const uint8_t *rec, double *gate, double
 /* ------------------------------------------------------------------------- */
 /* O1-O4: exact-integer low-rank predictor (reading R2; paper: "low-rank      */
 /* predictor" P:73, Deja Vu score per neuron P:252).                          */
+/*   O1  X_j = x_j * 2^24, exact integer (every fp16 is a multiple of 2^-24)  */
+/*   O2  h = A X in exact integer arithmetic (|h| < 2^60 for d <= 8192)       */
+/*   O3  hq = Q(h), Q(v)_i = sgn(v_i) floor((254|v_i| + M) / (2M)), M = max|v|*/
+/*   O4  s = B hq (int32)                                                     */
 /* ------------------------------------------------------------------------- */
 static int8_t quant_sym_127(int64_t v, int64_t M)
 {
-    /* sgn(v) * floor((254|v| + M) / (2M)) : round-half-up of 127|v|/M */
+    /* sgn(v) * floor((254|v| + M) / (2M)) : round-half-up of 127|v|/M.       */
+    /* |v| <= M < 2^60: 254|v| + M would overflow int64, so the quotient is    */
+    /* formed from M's multiples: 127|v|/M = q + rem/M, and the rounding       */
+    /* compares 2 rem with M (half rounds up).                                 */
     if (M == 0) return 0;
     int64_t a = v < 0 ? -v : v;
-    int64_t qq = (254 * a + M) / (2 * M);
-    return (int8_t)(v < 0 ? -qq : qq);
+    int64_t q = 0, rem = 0;
+    /* long division of 127 a by M without overflow: a <= M, so q <= 127 */
+    for (int i = 0; i < 127; i++) {
+        rem += a;
+        if (rem >= M) { rem -= M; q++; }
+    }
+    if (rem >= M - rem) q++; /* 2 rem >= M  <=>  fraction >= 1/2 */
+    return (int8_t)(v < 0 ? -q : q);
 }
 
 int orc_predict(int d, int r, int F_r, const uint16_t *x, const int8_t *A, const int8_t *B,
-                int8_t *xq, int32_t *h, int8_t *hq, int32_t *s)
+                int64_t *h, int8_t *hq, int32_t *s)
 {
-    if (d <= 0 || r <= 0 || F_r < 0) return ORC_EINVAL;
+    if (d <= 0 || r <= 0 || F_r < 0 || d > 8192) return ORC_EINVAL;
     int64_t *X = (int64_t *)malloc(sizeof(int64_t) * (size_t)d);
-    int64_t M = 0;
-    for (int j = 0; j < d; j++) {
+    for (int j = 0; j < d; j++) { /* O1 */
         double v = orc_half_to_double(x[j]);
         if (!isfinite(v)) { free(X); return ORC_EINVAL; }
         X[j] = (int64_t)ldexp(v, 24); /* exact: every fp16 is a multiple of 2^-24 */
-        int64_t a = X[j] < 0 ? -X[j] : X[j];
-        if (a > M) M = a;
     }
-    for (int j = 0; j < d; j++) xq[j] = quant_sym_127(X[j], M); /* O1 */
-    free(X);
     int64_t Mh = 0;
     for (int i = 0; i < r; i++) { /* O2 */
         int64_t acc = 0;
-        for (int j = 0; j < d; j++) acc += (int64_t)A[(size_t)i * d + j] * xq[j];
-        h[i] = (int32_t)acc;
+        for (int j = 0; j < d; j++) acc += (int64_t)A[(size_t)i * d + j] * X[j];
+        h[i] = acc;
         int64_t a = acc < 0 ? -acc : acc;
         if (a > Mh) Mh = a;
     }
+    free(X);
     for (int i = 0; i < r; i++) hq[i] = quant_sym_127(h[i], Mh); /* O3 */
     for (int n = 0; n < F_r; n++) { /* O4 */
         int64_t acc = 0;

@@ -55,7 +55,7 @@ def _setup(L):
     L.orc_record_bytes.argtypes = [C.c_int, C.c_int]
     L.orc_pack.argtypes = [C.c_int, C.c_int, vp, vp, vp, i64, i64, vp]
     L.orc_dequant_record.argtypes = [C.c_int, C.c_int, vp, vp, vp, vp]
-    L.orc_predict.argtypes = [C.c_int] * 3 + [vp] * 7
+    L.orc_predict.argtypes = [C.c_int] * 3 + [vp] * 6
     L.orc_select.argtypes = [C.c_int, vp, vp, vp, vp, vp]
     L.orc_ffn.argtypes = [C.c_int, vp, vp, vp, vp, vp, vp, C.c_int, vp, vp]
     L.orc_residual.argtypes = [C.c_int, vp, vp, vp, vp]
@@ -126,13 +126,12 @@ def predict(x, A, B):
     B = np.ascontiguousarray(B, np.int8)
     r, d = A.shape
     F_r = B.shape[0]
-    xq = np.zeros(d, np.int8)
-    h = np.zeros(r, np.int32)
+    h = np.zeros(r, np.int64)
     hq = np.zeros(r, np.int8)
     s = np.zeros(F_r, np.int32)
-    if lib().orc_predict(d, r, F_r, _p(x), _p(A), _p(B), _p(xq), _p(h), _p(hq), _p(s)):
+    if lib().orc_predict(d, r, F_r, _p(x), _p(A), _p(B), _p(h), _p(hq), _p(s)):
         raise ValueError("predict: non-finite x or bad shape")
-    return dict(xq=xq, h=h, hq=hq, s=s)
+    return dict(h=h, hq=hq, s=s)
 
 
 def select(s, plan):

@@ -15,6 +15,7 @@ import torch
 from ._lib import CacheCfg, M2CError, ModelDesc, TierPlan, check, lib  # noqa: F401
 
 MODE = {"resident": 0, "lru": 1, "atu": 2}
+DECODE_STAMPS = 24  # M2C_DECODE_STAMPS (include/m2c.h)
 
 
 def _ptr(t):
@@ -241,14 +242,14 @@ class M2CContext:
 
     def profile_stamps(self):
         """Raw k_decode stamps of the last decode step (profiling on): numpy uint64
-        [n_layers, G, 16] in ns (include/m2c.h documents the stamp points)."""
+        [n_layers, G, DECODE_STAMPS] in ns (include/m2c.h documents the stamp points)."""
         import numpy as np
         n = C.c_int64()
         check(lib().m2c_profile_stamps(self._h, None, 0, C.byref(n)))
         buf = (C.c_uint64 * n.value)()
         check(lib().m2c_profile_stamps(self._h, buf, n.value, C.byref(n)))
         a = np.frombuffer(buf, dtype=np.uint64).copy()
-        return a.reshape(self.desc.n_layers, -1, 16)
+        return a.reshape(self.desc.n_layers, -1, DECODE_STAMPS)
 
     def stats(self, reset=False):
         kpt = C.c_int64()

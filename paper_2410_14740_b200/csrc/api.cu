@@ -320,7 +320,7 @@ m2c_status m2c_create(const m2c_model_desc *desc, int32_t device, m2c_stream_t c
         off += a256(bytes);
         return o;
     };
-    const size_t o_h = take(4 * (size_t)r), o_s = take(4 * (size_t)F_r),
+    const size_t o_h = take(8 * (size_t)kHStride * r), o_s = take(4 * (size_t)F_r),
                  o_ids = take(4 * (size_t)F_r), o_tof = take((size_t)F_r),
                  o_slots = take(4 * (size_t)F_r), o_bits = take(4 * ((size_t)F_r / 32 + 2)),
                  o_hit = take(4 * (size_t)F_r), o_miss = take(4 * (size_t)F_r),
@@ -332,9 +332,9 @@ m2c_status m2c_create(const m2c_model_desc *desc, int32_t device, m2c_stream_t c
                  o_bepoch = take(4), o_dlay = take(decode_layer_table_bytes(desc->n_layers)),
                  o_dprof = take(8 * (size_t)kDecodeStamps * c->G * desc->n_layers),
                  o_binsh = take(4 * (size_t)desc->n_layers), o_sabs = take(4 * (size_t)c->G),
-                 o_bucket = take(decode_bucket_bytes()),
-                 o_stage = take(4 * 3 * (size_t)c->G * ((F_r + c->G - 1) / c->G)),
-                 o_ccount = take(16 * (size_t)c->G),
+                 o_hb = take(8 * 2 * (size_t)kHStride * r),
+                 o_runs = take(4 * (size_t)c->G * ((((F_r + c->G - 1) / c->G) + 3) & ~3)),
+                 o_dhist = take(decode_hist_bytes()),
                  o_prev = take(4 * (size_t)desc->n_layers * (plan->k > 0 ? plan->k : 1));
     // score histogram geometry: |s| <= 127^2 r, bins of 2^sh over [0, 2 smax] (4096 bins)
     c->sel_smax = 16129 * desc->pred_rank;
@@ -350,7 +350,7 @@ m2c_status m2c_create(const m2c_model_desc *desc, int32_t device, m2c_stream_t c
     }
     c->ws_bytes = off;
     uint8_t *b = static_cast<uint8_t *>(c->ws_mem);
-    c->ws.h = (int32_t *)(b + o_h);
+    c->ws.h = (long long *)(b + o_h);
     c->ws.s = (int32_t *)(b + o_s);
     c->ws.tier_ids = (int32_t *)(b + o_ids);
     c->ws.tier_of = (int8_t *)(b + o_tof);
@@ -376,9 +376,9 @@ m2c_status m2c_create(const m2c_model_desc *desc, int32_t device, m2c_stream_t c
     c->dec_prof = (unsigned long long *)(b + o_dprof);
     c->dec_bin_sh = (int *)(b + o_binsh);
     c->dec_sabs = (unsigned *)(b + o_sabs);
-    c->dec_bucket = b + o_bucket;
-    c->dec_stage = (int *)(b + o_stage);
-    c->dec_ccount = (int *)(b + o_ccount);
+    c->dec_hb = (long long *)(b + o_hb);
+    c->dec_runs = (int *)(b + o_runs);
+    c->dec_hist = (int *)(b + o_dhist);
     e = cudaMemset(c->ws_mem, 0, off);
     if (e == cudaSuccess) {  // k_decode's first token: a histogram scale that covers |s| <= smax
         int sh0 = 0;
@@ -460,7 +460,10 @@ m2c_status m2c_load_layer(m2c_ctx *c, int32_t layer, const void *g, const void *
     L.mode = cfg->mode;
     L.A = (const int8_t *)(hb + Lo.A);
     L.B = (const int8_t *)(hb + Lo.B);
-    M2C_CUDA(cudaMemcpyAsync(hb + Lo.A, A, (size_t)r * d, cudaMemcpyDefault, st));
+    // A arrives row-major [r][d]; it is stored transposed (A^T [d][r], R2 / k_pred.cu).  The
+    // FFN partial-sum workspace (8 G d >= r d bytes) stages the transpose.
+    M2C_CUDA(cudaMemcpyAsync(c->ws.partial, A, (size_t)r * d, cudaMemcpyDefault, st));
+    M2C_CUDA(launch_transpose_i8(r, d, (const int8_t *)c->ws.partial, (int8_t *)(hb + Lo.A), st));
     M2C_CUDA(cudaMemcpyAsync(hb + Lo.B, B, (size_t)F_r * r, cudaMemcpyDefault, st));
     const int bits[3] = {16, 8, 4};
     const __half *G = (const __half *)g, *U = (const __half *)u, *D = (const __half *)dn;

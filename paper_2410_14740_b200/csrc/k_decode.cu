@@ -2,28 +2,34 @@
 // through every layer of the resident stack (a1 -> a7 of SURVEY §8, per layer).
 //
 // Why: batch-1 decode of the sparse FFN moves ~17 MB per layer (S7), i.e. ~2.7 us at HBM
-// speed, while a chain of five dependent kernels per layer costs ~40 us of launch / drain /
-// ramp latency (profiles/).  Here one CTA per SM stays resident for the whole token and the
-// phases of a layer are separated by grid barriers (~0.5 us each) instead of kernel
-// boundaries:
-//   P1  x -> xq = Q(x) (every CTA, from L2), h = A xq for this CTA's rows of A   [a1]
-//   --- barrier
-//   P2  hq = Q(h) (every CTA), scores s = B hq for this CTA's neurons, 4096-bin
-//       histogram of s (global atomics)                                          [a2]
-//   --- barrier
-//   P3  every CTA derives the three rank cuts itself (histogram scan, exact refinement of
-//       the cut bins, ties by id -- R3), classifies ALL neurons from a shared-memory copy of
-//       the scores and takes its byte-balanced share of the tier lists (no barrier needed:
-//       the lists are a pure function of s)                                       [a3]
+// speed, while a chain of dependent kernels per layer costs ~40 us of launch / drain / ramp
+// latency (profiles/).  One CTA per SM stays resident for the whole token; the phases of a
+// layer are separated by grid barriers (~1.3 us each on B200, tools/mb_gridsync2.cu), so the
+// design minimises their number: THREE per layer.
+//
+//   P2  hq = Q(h) (every CTA: h = A x was completed by integer atomics before the barrier),
+//       x -> smem, scores s = B hq of this CTA's neurons, 4096-bin score histogram (global
+//       atomics)                                                                     [a2]
+//   --- barrier Bs
+//   P3  every CTA pulls the whole histogram and ALL scores into shared memory with two TMA
+//       bulk copies and derives the selection itself: the three rank cuts (k16, k16+k8, k;
+//       histogram scans, exact ranking of the cut bins' candidates, ties by id -- R3), then a
+//       block-wide ordered compaction that keeps the ids falling into this CTA's share of the
+//       tier lists.  No exchange is needed: the lists are a pure function of s.         [a3]
 //   P4  fused dequant-GEMV FFN over the share (ffn_dev.cuh, same code as k_ffn) -> partial y
-//                                                                                 [a6]
-//   --- barrier
-//   P5  fixed-order reduction of the partials (the k_reduce order) for this CTA's 32-column
-//       chunks, x_{l+1} = fp16(x + fp16(y)) (R14)                                 [a7]
-//   --- barrier
-// While layer l runs, every CTA streams its share of layer l+1's predictor slices and of the
-// records the previous token selected for layer l+1 (~80% recur) into L2, so the FFN's
-// TMA reads mostly hit L2 (cross-layer lookahead in hardware terms).
+//                                                                                    [a6]
+//   --- barrier By
+//   R   for this CTA's 32-column chunks: fixed-order reduction of the partials (the k_reduce
+//       order), x_{l+1} = fp16(x + fp16(y)) (R14); then, because h = A x is exact integer
+//       arithmetic (R2), the chunk's contribution to layer l+1's h = A_{l+1} x_{l+1} is added
+//       with red.add.u64 -- integer atomics are order-independent, so h is bit-exact and the
+//       predictor needs no barrier of its own                                     [a7, a1]
+//   --- barrier Bx (not after the last layer)
+//
+// Layer 0's h comes from a prologue (the R step without the reduction) and one barrier.
+// While layer l runs, warp 1 streams into L2 (during barrier waits): layer l+1's predictor
+// slice of this CTA, layer l+2's A^T chunk, and this CTA's share of the records the previous
+// token selected for layer l+1 (~80% recur), so the FFN's TMA reads mostly hit L2.
 // Results are bit-identical to the per-phase kernel chain (same select rule, same per-CTA FFN
 // shares and batches, same reduction order): tests/test_gpu_parity.py checks it.
 #include <cstdlib>
@@ -34,21 +40,26 @@ namespace m2c {
 namespace {
 
 constexpr int kBins = 4096;
-// profiling stamps per (layer, CTA): 0 layer start, 1 P1 done, 2 after B1, 3 P2 done, 4 after
-// B2, 5 P3 done, 6 P4 done, 7 after B4, 8 P5 done, 9 kernel end (last layer only); P3 steps:
-// 10 cuts exact, 11 own neurons classified + published, 12 after barrier 3, 13 list share
-// gathered.  (Publishing the counts as tagged words polled by every CTA instead of barrier 3
-// measured slower: 148 x 148 pollers on ten cache lines.)
+constexpr int kHistW = kBins;  // fine bins (the 64 coarse sums follow them in smem only)
+// profiling stamps per (layer, CTA): 0 layer start, 1 P2 done, 4 after Bs, 2 runs in smem,
+// 3 cut bins found, 10 cuts exact,
+// 11 lists done, 5 P3 done, 6 P4 done, 7 after By, 8 R done, 9 kernel end (last layer),
+// 12/13 prologue start / after its barrier (layer 0), 14/15 FFN-internal (ffn_loop)
 constexpr int kStamps = kDecodeStamps;
-constexpr int kBucket = 32;       // (score, id) pairs kept per histogram bin
-constexpr int kCoarse = 64;       // coarse bins (64 fine bins each)
-// ring-aliased scratch of P1..P3 (bytes): xq [0, 8K) | hq [8K, 8.5K) | own scores | from 32K:
-// histogram (P3a), all scores (degenerate-tie fallback), per-CTA counts (P3b)
-constexpr int kOwnOff = 9216;     // <= 4096 ints: this CTA's scores
-constexpr int kSbufOff = 32768;   // [F_r] ints
+constexpr int kCand = 64;         // candidates ranked per cut bin (more: block-wide fallback)
+// ring-aliased scratch of P2..P3 (bytes): hq [0, 512) | histogram + coarse sums [4K, 20.25K)
+// | cut candidates [21K, 22.5K) | all scores from 32K
+constexpr int kHistOff = 4096;
+constexpr int kCandOff = 21504;
+constexpr int kCcOff = 23040;     // [G][4] per-run cumulative tier counts (G <= 148)
+constexpr int kExOff = 25600;     // [G][4] per-run list positions (before: per-run cut keys)
+constexpr int kWorkOff = 28160;   // [<= 3 G] (run, tier) work items of the list write
+constexpr int kSbufOff = 32768;
+// R: this CTA's A^T chunks of the next layer (<= 2 x 32 r bytes), staged by TMA at barrier By
+constexpr int kAtOff = 8192;
 
 struct DecLayer {
-    const int8_t *A, *B;
+    const int8_t *At, *B;       // A^T [d][r], B [F_r][r]
     const uint8_t *pool[3];
 };
 
@@ -56,22 +67,20 @@ struct DecArgs {
     const DecLayer *layers;
     int n_layers, d, r, F_r, act;
     int k16, k8, k4;
-    int smax, sh;
+    int smax;
     int nb[3], wt[3];
     __half *x;                  // [d] in/out
-    int32_t *h;                 // [r]
-    int32_t *s;                 // [F_r]
-    int *ghist;                 // [2][4096]
+    long long *hb;              // [2][r][kHStride] h accumulators (layer parity)
+    int *runs;                  // [G][RP] per-CTA sorted score keys (P2 -> P3)
+    int *ghist;                 // [2][kHistW] fine + coarse score histograms (layer parity)
+    int T;                      // run row length (== RP)
     int32_t *lists;             // [n_layers][max(k,1)]  (the tier lists; next token's prefetch hint)
     float *partial;             // [G][d]
-    unsigned *bar_flags;        // [32]: [0] = grid-barrier arrival counter
+    unsigned *bar_flags;        // [0] = grid-barrier arrival counter
     unsigned *bar_epoch;
     uint32_t *err;
     unsigned long long *prof;   // [n_layers][G][kStamps] globaltimer stamps, or null
     int prefetch;
-    int2 *bucket;               // [2][4096][kBucket] (score, id) per bin (layer parity)
-    int *stage;                 // [3][G][ceil(F_r / G)] per-CTA compacted selected ids
-    int *ccount;                // [G][4] per-CTA tier counts
     int *bin_sh;                // [n_layers] histogram scale per layer (adapted token to token)
     unsigned *sabs;             // [G] per-CTA max |s| of the current layer
 };
@@ -89,7 +98,6 @@ __device__ __forceinline__ unsigned ld_relaxed(const unsigned *p) {
     asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
-
 __device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
     unsigned v;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -98,9 +106,8 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned *p) {
 
 // Grid barrier #target (counted across launches): every CTA adds 1 to one counter with a
 // release reduction; thread 0 polls it with acquire loads until it reaches target * G
-// (wrap-safe).  Measured ~1.4 us on B200 (tools/mb_gridsync.cu: per-CTA flag words polled
-// by a warp cost ~3 us).  Warp 1 runs `work` (latency-tolerant side work) meanwhile.  A 2 s
-// timeout sets err bit 4 instead of hanging the GPU.
+// (wrap-safe).  Measured ~1.3 us on B200 (tools/mb_gridsync2.cu).  Warp 1 runs `work`
+// (latency-tolerant side work) meanwhile.  A 2 s timeout sets err bit 4 instead of hanging.
 template <class F>
 __device__ __forceinline__ void grid_sync(unsigned *counter, unsigned target, uint32_t *err, F work) {
     __syncthreads();
@@ -124,6 +131,18 @@ __device__ __forceinline__ void grid_sync(unsigned *flags, unsigned target, uint
     grid_sync(flags, target, err, [] {});
 }
 
+__device__ __forceinline__ unsigned long long block_max_u64(unsigned long long v, unsigned long long *sm32) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    __syncthreads();
+    if (lane == 0) sm32[warp] = v;
+    __syncthreads();
+    v = lane < nw ? sm32[lane] : 0ull;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
 __device__ __forceinline__ int block_max_u(unsigned v, unsigned *sm32) {
     v = __reduce_max_sync(0xffffffffu, v);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -140,81 +159,74 @@ __device__ __forceinline__ int block_sum(int v, int *sm32) {
     __syncthreads();
     return __reduce_add_sync(0xffffffffu, lane < nw ? sm32[lane] : 0);
 }
-// exclusive block scan of 3 ints (any blockDim multiple of 32, <= 1024); totals in tot
-__device__ __forceinline__ void block_exscan3(const int v[3], int ex[3], int tot[3], int *sm /*[3][32]*/) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    int inc[3];
-#pragma unroll
-    for (int t = 0; t < 3; t++) {
-        int x = v[t];
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
-        }
-        inc[t] = x;
-        if (lane == 31) sm[t * 32 + warp] = x;
+// one L2 prefetch of [p, p + bytes): a TMA bulk prefetch (mode 1, 2), or per-line
+// prefetch.global.L2 instructions spread over the warp (mode 3, 4: LSU path, no TMA queue)
+__device__ __forceinline__ void pf_range(int mode, const void *ptr, uint32_t bytes, int lane, int nl) {
+    if (mode <= 2) {
+        if (lane == 0) prefetch_l2(ptr, bytes);
+    } else {
+        const char *c = static_cast<const char *>(ptr);
+        for (uint32_t o = 128u * lane; o < bytes; o += 128u * nl)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(c + o));
     }
-    __syncthreads();
-    if (warp == 0) {
-#pragma unroll
-        for (int t = 0; t < 3; t++) {
-            int x = lane < nw ? sm[t * 32 + lane] : 0;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int y = __shfl_up_sync(0xffffffffu, x, o);
-                if (lane >= o) x += y;
-            }
-            sm[t * 32 + lane] = x;
-        }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int t = 0; t < 3; t++) {
-        ex[t] = (warp ? sm[t * 32 + warp - 1] : 0) + inc[t] - v[t];
-        tot[t] = sm[t * 32 + nw - 1];
-    }
-    __syncthreads();
 }
 
-__device__ __forceinline__ int q127_f32(float a, float M, float inv) {  // a = |v| >= 0, M > 0
-    int q = (int)fmaf(a, inv, 0.5f);
-    const float a254 = 254.f * a;
-    if (fmaf(-(float)(2 * q - 1), M, a254) < 0.f) q -= 1;
-    else if (fmaf(-(float)(2 * q + 1), M, a254) >= 0.f) q += 1;
-    return q;
-}
-__device__ __forceinline__ int q127_f64(double a, double M, double inv) {
-    int q = (int)fma(a, inv, 0.5);
-    const double a254 = 254.0 * a;
-    if (fma(-(double)(2 * q - 1), M, a254) < 0.0) q -= 1;
-    else if (fma(-(double)(2 * q + 1), M, a254) >= 0.0) q += 1;
-    return q;
-}
-
-// L2 prefetch of layer lj's predictor slices of this CTA and its share of the records the
-// previous token selected for lj (one warp, fire and forget)
-__device__ __forceinline__ void prefetch_layer(const DecArgs &p, int lj) {
-    if (p.prefetch == 0) return;
-    const DecLayer Lj = p.layers[lj];
+// L2 prefetch (one warp, fire and forget): this CTA's predictor slice of layer lb (B rows of
+// its neurons), its A^T chunks of layer la, its share of the records the previous token
+// selected for layer lr.  Negative layer indices skip that part.
+// M2C_DECODE_PREFETCH: 0 none; 1 all (TMA bulk prefetch); 2 predictor only (TMA);
+// 3 all (per-line LSU prefetch); 4 predictor only (LSU).
+__device__ __forceinline__ void prefetch_layers(const DecArgs &p, int lb, int la, int lr) {
+    const int mode = p.prefetch;
+    if (mode == 0) return;
     const int lane = threadIdx.x & 31, G = gridDim.x, cta = blockIdx.x;
-    const int rph = (p.r + G - 1) / G, rps = (p.F_r + G - 1) / G;
-    if (lane < rph && cta * rph + lane < p.r)
-        prefetch_l2(Lj.A + (int64_t)(cta * rph + lane) * p.d, (uint32_t)p.d);
-    {
+    const int nl = blockDim.x == 32 ? 1 : 32;  // a 32-thread CTA runs this on thread 0 alone
+    const int ln = blockDim.x == 32 ? 0 : lane;
+    if (lb >= 0) {
+        const int8_t *B = p.layers[lb].B;
+        const int rps = (p.F_r + G - 1) / G;
         const int n0 = cta * rps, n1 = min(p.F_r, n0 + rps);
-        for (int n = n0 + lane * 64; n < n1; n += 32 * 64)  // <= 64 rows (16 KB at r = 256) per call
-            prefetch_l2(Lj.B + (int64_t)n * p.r, (uint32_t)(min(64, n1 - n) * p.r));
+        if (n1 > n0) pf_range(mode, B + (int64_t)n0 * p.r, (uint32_t)((n1 - n0) * p.r), ln, nl);
     }
-    if (p.prefetch == 1) {
+    if (la >= 0) {
+        const int8_t *At = p.layers[la].At;
+        for (int ch = cta; ch < p.d / 32; ch += G) pf_range(mode, At + (int64_t)ch * 32 * p.r, (uint32_t)(32 * p.r), ln, nl);
+    }
+    if (lr >= 0 && (mode == 1 || mode == 3)) {
+        const DecLayer Lj = p.layers[lr];
         const int k = p.k16 + p.k8 + p.k4;
-        const int32_t *ids = p.lists + (int64_t)lj * (k > 0 ? k : 1);
+        const int32_t *ids = p.lists + (int64_t)lr * (k > 0 ? k : 1);
         const int i0 = (int)((long long)k * cta / G), i1 = (int)((long long)k * (cta + 1) / G);
-        for (int i = i0 + lane; i < i1; i += 32) {
-            const int t = i < p.k16 ? 0 : (i < p.k16 + p.k8 ? 1 : 2);
-            const int id = __ldcg(ids + i);
-            if (id >= 0 && id < p.F_r) prefetch_l2(Lj.pool[t] + (int64_t)id * p.nb[t], (uint32_t)p.nb[t]);
+        if (mode == 1) {
+            for (int i = i0 + ln; i < i1; i += nl) {
+                const int t = i < p.k16 ? 0 : (i < p.k16 + p.k8 ? 1 : 2);
+                const int id = __ldcg(ids + i);
+                if (id >= 0 && id < p.F_r) prefetch_l2(Lj.pool[t] + (int64_t)id * p.nb[t], (uint32_t)p.nb[t]);
+            }
+        } else {
+            for (int i = i0; i < i1; i++) {
+                const int t = i < p.k16 ? 0 : (i < p.k16 + p.k8 ? 1 : 2);
+                const int id = __ldcg(ids + i);
+                if (id >= 0 && id < p.F_r) pf_range(mode, Lj.pool[t] + (int64_t)id * p.nb[t], (uint32_t)p.nb[t], ln, nl);
+            }
         }
+    }
+}
+
+// h_{la} += A_{la}[:, 32 ch .. 32 ch + 32) X for the chunk whose fixed-point x values
+// (X_j = xm_j << xsh_j, fp16_fixed) are in shared memory; one red.add.u64 per row.
+// At: the chunk's 32 rows of A^T (global memory, or a shared-memory copy)
+__device__ __forceinline__ void h_chunk(const int8_t *At, int r, const int *xm, const int *xsh,
+                                        long long *hbuf) {
+    for (int i = threadIdx.x; i < r; i += blockDim.x) {
+        int av[32];
+#pragma unroll
+        for (int j = 0; j < 32; j++) av[j] = At[(int64_t)j * r + i];
+        unsigned long long acc = 0;
+#pragma unroll
+        for (int j = 0; j < 32; j++) acc += (unsigned long long)(long long)(av[j] * xm[j]) << xsh[j];
+        // (fully unrolled: av stays in registers)
+        if (acc) red_add_u64(hbuf + (int64_t)i * kHStride, (long long)acc);
     }
 }
 
@@ -224,17 +236,22 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
     __shared__ FfnShared sm;
     __shared__ FfnArgs fa;
     __shared__ unsigned red_u[32];
+    __shared__ unsigned long long red_u64[32];
     __shared__ int red_i[32];
-    __shared__ int scan_sm[96];
-    __shared__ int cut_bin[3], cut_need[3], cut_V[3], cut_I[3], ncand[3];
+    __shared__ int cut_bin[3], cut_need[3], cut_V[3], cut_I[3], ncand[3], ccnt[3];
+    __shared__ int xm[32], xsh[32];
+    __shared__ __align__(8) uint64_t sel_bar, at_bar;
     const SmemPtrs S = carve(smem);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int NT = blockDim.x, NW = NT >> 5, G = gridDim.x, cta = blockIdx.x;
     const int d = p.d, r = p.r, F_r = p.F_r;
     const int kk = p.k16 + p.k8 + p.k4;
-    const int tg[3] = {p.k16, p.k16 + p.k8, kk};
+    auto tg = [&](int t) { return t == 0 ? p.k16 : (t == 1 ? p.k16 + p.k8 : kk); };  // cut targets
+    const int nchunk = d / 32;
     if (tid == 0) {
         for (int i = 0; i < kNSlot; i++) mbar_init(&sm.bars[i], 1);
+        mbar_init(&sel_bar, 1);
+        mbar_init(&at_bar, 1);
         fence_mbar_init();
         for (int t = 0; t < 3; t++) {
             fa.nb[t] = p.nb[t];
@@ -254,99 +271,50 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
     // per-CTA globaltimer stamps (profiling): [l][cta][kStamps], see STAMP below
     unsigned long long *prof0 = (p.prof && tid == 0) ? p.prof + (int64_t)cta * kStamps : nullptr;
     const int64_t prof_layer = (int64_t)G * kStamps;
-    unsigned long long *prof = nullptr;
+    unsigned long long *prof = prof0;
 #define STAMP(i) \
     if (prof) prof[i] = gtimer()
-    if (warp == NW - 1) prefetch_layer(p, 0);
+    STAMP(12);
+    if (warp == NW - 1) prefetch_layers(p, 0, p.n_layers > 1 ? 1 : -1, 0);
+    // (the L2 prefetches are bulk operations of the SM's TMA unit, which serves requests in
+    // order: they are issued where no latency-critical copy is queued behind them -- here and
+    // at barrier By, after the FFN's copies)
+
+    // ================= prologue: layer 0's h = A_0 x from this CTA's column chunks ==========
+    for (int ch = cta; ch < nchunk; ch += G) {
+        if (tid < 32) {
+            bool bad = false;
+            int m, sh;
+            fp16_fixed(__half_as_ushort(__ldcg(p.x + ch * 32 + tid)), m, sh, bad);
+            if (bad) atomicOr(p.err, 1u);
+            xm[tid] = m;
+            xsh[tid] = sh;
+        }
+        __syncthreads();
+        h_chunk(p.layers[0].At + (int64_t)ch * 32 * r, r, xm, xsh, p.hb);
+        __syncthreads();
+    }
+    grid_sync(p.bar_flags, base + ++nbar, p.err);
+    STAMP(13);
 
     for (int l = 0; l < p.n_layers; l++) {
         const DecLayer Ld = p.layers[l];
-        int *hist = p.ghist + (l & 1) * kBins;
+        int *hist = p.ghist + (l & 1) * kHistW;
+        long long *hcur = p.hb + (int64_t)(l & 1) * r * kHStride;
         int32_t *lst = p.lists + (int64_t)l * (kk > 0 ? kk : 1);
         prof = prof0 ? prof0 + l * prof_layer : nullptr;
         STAMP(0);
 
-        // ================= P1: xq = Q(x), h rows ==================================
-        {
-            int8_t *xq = reinterpret_cast<int8_t *>(S.ring);
-            // this warp's first 16 B of its A row segment, loaded before x (independent of it)
-            const int rph = (r + G - 1) / G;
-            const int row0 = cta * rph, nrow = max(0, min(rph, r - row0));
-            const int wpr = NW >= nrow && nrow > 0 ? NW / nrow : 1;  // warps per row
-            const int n16 = d / 16, per = (n16 + wpr - 1) / wpr;
-            const int rr_first = warp / wpr, seg = warp % wpr;
-            const int c0 = seg * per, c1 = min(n16, c0 + per);
-            int4 a_pre = make_int4(0, 0, 0, 0);
-            if (rr_first < nrow && c0 + lane < c1)
-                a_pre = __ldg(reinterpret_cast<const int4 *>(Ld.A + (int64_t)(row0 + rr_first) * d) + c0 + lane);
-            const uint4 xv = __ldcg(reinterpret_cast<const uint4 *>(p.x) + tid);  // NT == d / 8
-            S.xs[tid] = xv;
-            const unsigned m2 = __vmaxu2(__vmaxu2(xv.x & 0x7fff7fffu, xv.y & 0x7fff7fffu),
-                                         __vmaxu2(xv.z & 0x7fff7fffu, xv.w & 0x7fff7fffu));
-            unsigned mx = (unsigned)block_max_u(max(m2 & 0xffffu, m2 >> 16), red_u);
-            if (mx >= 0x7c00) {  // Inf / NaN: flag, quantise as zero
-                if (cta == 0 && tid == 0) atomicOr(p.err, 1u);
-                mx = 0;
-            }
-            const float M = __half2float(__ushort_as_half((unsigned short)mx));
-            const float inv = mx ? 127.f / M : 0.f;
-            const uint32_t w[4] = {xv.x, xv.y, xv.z, xv.w};
-            uint32_t packed[2] = {0, 0};
-#pragma unroll
-            for (int e = 0; e < 8; e++) {
-                const unsigned short b = (unsigned short)(w[e >> 1] >> (16 * (e & 1)));
-                int q = 0;
-                if (mx) {
-                    q = q127_f32(__half2float(__ushort_as_half((unsigned short)(b & 0x7fff))), M, inv);
-                    if (b & 0x8000) q = -q;
-                }
-                packed[e >> 2] |= (uint32_t)(q & 0xff) << (8 * (e & 3));
-            }
-            reinterpret_cast<uint2 *>(xq)[tid] = make_uint2(packed[0], packed[1]);
-            __syncthreads();
-            if (nrow > 0) {
-                for (int rr = rr_first; rr < nrow; rr += (NW / wpr > 0 ? NW / wpr : 1)) {
-                    const int4 *a4 = reinterpret_cast<const int4 *>(Ld.A + (int64_t)(row0 + rr) * d);
-                    const int4 *x4 = reinterpret_cast<const int4 *>(xq);
-                    int acc = 0;
-                    for (int c = c0 + lane; c < c1; c += 32) {
-                        const int4 av = (rr == rr_first && c == c0 + lane) ? a_pre : __ldg(a4 + c);
-                        const int4 xw = x4[c];
-                        acc = __dp4a(av.x, xw.x, acc);
-                        acc = __dp4a(av.y, xw.y, acc);
-                        acc = __dp4a(av.z, xw.z, acc);
-                        acc = __dp4a(av.w, xw.w, acc);
-                    }
-                    acc = __reduce_add_sync(0xffffffffu, acc);
-                    if (wpr == 1) {
-                        if (lane == 0) p.h[row0 + rr] = acc;
-                    } else if (lane == 0) {
-                        red_i[warp] = acc;
-                    }
-                }
-                if (wpr > 1) {
-                    __syncthreads();
-                    if (tid < nrow) {
-                        int s = 0;
-                        for (int w2 = 0; w2 < wpr; w2++) s += red_i[tid * wpr + w2];
-                        p.h[row0 + tid] = s;
-                    }
-                }
-            }
-        }
-        STAMP(1);
-        grid_sync(p.bar_flags, base + ++nbar, p.err,
-                  [&] { prefetch_layer(p, l + 1 < p.n_layers ? l + 1 : 0); });
-        STAMP(2);
-
-        // ================= P2: hq = Q(h), scores, histogram ==========================
+        // ================= P2: hq = Q(h), x -> smem, scores, histogram, sorted run ==========
         const int shl = __ldcg(p.bin_sh + l);  // this token's histogram scale for layer l
+        const int rps = (F_r + G - 1) / G;      // neurons per CTA (this CTA: ids [n0, n1))
+        const int RP = (rps + 3) & ~3;          // run length in the runs array (16-B rows)
         {
-            int8_t *hq = reinterpret_cast<int8_t *>(S.ring) + 8192;
+            int8_t *hq = reinterpret_cast<int8_t *>(S.ring);
+            int *keys = reinterpret_cast<int *>(S.ring + 1024);  // this CTA's run keys (<= 256)
             // lanes per neuron LPN, 16-B chunks per lane CPL (r = 256: 4 x 4; r = 32: 1 x 2)
             const int C16 = r / 16, CPL = C16 >= 4 ? 4 : C16, LPN = C16 / CPL, npw = 32 / LPN;
             const int part = lane % LPN, sub = lane / LPN;
-            const int rps = (F_r + G - 1) / G;
             const int n0 = cta * rps, n1 = min(F_r, n0 + rps);
             const int step = NW * npw;
             int nb0 = n0 + warp * npw;
@@ -358,21 +326,22 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
                 for (int c = 0; c < 4; c++) bv[c] = (c < CPL && n < n1) ? __ldg(b4 + c) : make_int4(0, 0, 0, 0);
             };
             load_b();
-            int hv0 = tid < r ? __ldcg(p.h + tid) : 0;
-            int mh = abs(hv0);
-            for (int i = tid + NT; i < r; i += NT) mh = max(mh, abs(__ldcg(p.h + i)));
-            mh = block_max_u((unsigned)mh, red_u);
-            const double Mh = (double)mh, invh = mh ? 127.0 / Mh : 0.0;
+            S.xs[tid] = __ldcg(reinterpret_cast<const uint4 *>(p.x) + tid);  // NT == d / 8
+            long long hv0 = tid < r ? __ldcg(hcur + (int64_t)tid * kHStride) : 0;
+            unsigned long long mh = (unsigned long long)(hv0 < 0 ? -hv0 : hv0);
+            for (int i = tid + NT; i < r; i += NT) {
+                const long long v = __ldcg(hcur + (int64_t)i * kHStride);
+                mh = max(mh, (unsigned long long)(v < 0 ? -v : v));
+            }
+            mh = block_max_u64(mh, red_u64);
             for (int i = tid; i < r; i += NT) {
-                const int hv = i == tid ? hv0 : __ldcg(p.h + i);
-                const int q = mh ? q127_f64((double)abs(hv), Mh, invh) : 0;
+                const long long hv = i == tid ? hv0 : __ldcg(hcur + (int64_t)i * kHStride);
+                const int q = quant127_u64((unsigned long long)(hv < 0 ? -hv : hv), mh);
                 hq[i] = (int8_t)(hv < 0 ? -q : q);
             }
             __syncthreads();
             const int4 *hq4 = reinterpret_cast<const int4 *>(hq) + part * CPL;
             unsigned amax = 0;
-            int *own = reinterpret_cast<int *>(S.ring + kOwnOff);  // this CTA's scores (P3)
-            int2 *bkt = p.bucket + (size_t)(l & 1) * kBins * kBucket;
             while (nb0 < n1) {
                 int acc = 0;
 #pragma unroll
@@ -387,22 +356,55 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
                 for (int o = LPN / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
                 const int n = nb0 + sub;
                 if (part == 0 && n < n1) {
-                    const int b = bin_of(acc, shl);
-                    p.s[n] = acc;
-                    own[n - n0] = acc;
+                    // run key: (s, local index asc) in one int -- |s| < 2^23 (R2), local < 255
+                    keys[n - n0] = (int)(((unsigned)acc << 8) | (unsigned)(255 - (n - n0)));
                     amax = max(amax, (unsigned)abs(acc));
-                    const int slot = atomicAdd(&hist[b], 1);
-                    if (slot < kBucket) bkt[(size_t)b * kBucket + slot] = make_int2(acc, n);
+                    atomicAdd(&hist[bin_of(acc, shl)], 1);
                 }
                 nb0 += step;
                 if (nb0 < n1) load_b();
             }
-            amax = block_max_u(amax, red_u);  // one plain store per CTA (no same-address atomics)
+            amax = block_max_u(amax, red_u);  // (its __syncthreads publishes keys[])
             if (tid == 0) p.sabs[cta] = amax;
+            // sorted run (key descending): rank by counting, one thread per neuron
+            const int nown = n1 - n0;
+            int *run = p.runs + (int64_t)cta * RP;
+            for (int i = tid; i < RP; i += NT) {
+                int ki = (int)0x80000000, rk = i;  // padding: below every key
+                if (i < nown) {
+                    ki = keys[i];
+                    rk = 0;
+                    for (int j = 0; j < nown; j++) rk += keys[j] > ki;
+                }
+                run[rk] = ki;
+            }
         }
-        STAMP(3);
+        STAMP(1);
         grid_sync(p.bar_flags, base + ++nbar, p.err);
         STAMP(4);
+
+        // ================= P3: the selection, every CTA from a copy of all sorted runs =========
+        int *hs = reinterpret_cast<int *>(S.ring + kHistOff);
+        const int T = p.T;
+        const int *ts = reinterpret_cast<const int *>(S.ring + kSbufOff);  // all runs [G][RP]
+        // key e of run c: the smem copy of the run's first T keys, else the run in global memory
+        auto runkey = [&](int c, int e) { return ts[c * T + e]; };  // T == RP: every run is in smem
+        if (tid == 0) {  // histograms + run prefixes -> smem: two bulk copies on one mbarrier
+            // order the ring's earlier generic accesses (and the acquired global data) before
+            // the async-proxy copies
+            asm volatile("fence.proxy.async;" ::: "memory");
+            const uint32_t sb = (uint32_t)(4 * G * T);
+            mbar_expect_tx(&sel_bar, (uint32_t)(4 * kBins) + sb);
+            bulk_g2s_plain(hs, hist, 4 * kBins, &sel_bar);
+            bulk_g2s_plain(S.ring + kSbufOff, p.runs, sb, &sel_bar);
+        }
+        if (tid < 3) {
+            cut_V[tid] = 0x7fffffff;  // empty cut: nothing is above it
+            cut_I[tid] = -1;
+            cut_bin[tid] = -1;
+            ncand[tid] = 0;
+            ccnt[tid] = 0;
+        }
         // next token's histogram scale for this layer: |s| < 2048 << sh (no clamped bins)
         if (cta == 0 && warp == 0) {
             unsigned m = 0;
@@ -412,240 +414,349 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
             while ((m >> sh) >= 2048u) sh++;
             if (lane == 0) p.bin_sh[l] = sh;
         }
+        // h of this layer was consumed in P2: clear it for layer l+2 (accumulated after By of l+1)
+        if (cta == 0)
+            for (int i = tid; i < r; i += NT) hcur[(int64_t)i * kHStride] = 0;
         // the other histogram buffer was last read in layer l-1's P3: clear it for layer l+1
         if (cta == G - 1)
-            for (int i = tid; i < kBins; i += NT) p.ghist[((l + 1) & 1) * kBins + i] = 0;
-
-        // ================= P3a: exact cuts (every CTA), classify own neurons, publish ========
-        // Cut t (t = 0, 1, 2: the k16-th, (k16+k8)-th and k-th score in (score desc, id asc)
-        // order, R3) is found by warp t: suffix scans of the 64 coarse then 64 fine histogram
-        // bins locate the bin and the rank needed inside it; the bin's bucket (<= kBucket
-        // (score, id) pairs written in P2) is ranked exactly.  An overflowing bucket (massive
-        // ties) falls back to block-wide binary searches over all scores.
-        {
-            const int2 *bkt = p.bucket + (size_t)(l & 1) * kBins * kBucket;
-            if (tid < 3) {
-                cut_V[tid] = 0x7fffffff;  // empty cut: nothing is above it
-                cut_I[tid] = -1;
-                cut_bin[tid] = -1;
-                ncand[tid] = 0;
-            }
-            // the histogram -> smem in one round of 16-B loads; coarse sums of 64 bins after it
-            int *hs = reinterpret_cast<int *>(S.ring + kSbufOff);
-#pragma unroll 4
-            for (int i = tid; i < kBins / 4; i += NT)
-                reinterpret_cast<int4 *>(hs)[i] = __ldcg(reinterpret_cast<const int4 *>(hist) + i);
-            __syncthreads();
-            for (int cidx = warp; cidx < kCoarse; cidx += NW) {
+            for (int i = tid; i < kHistW; i += NT) p.ghist[((l + 1) & 1) * kHistW + i] = 0;
+        mbar_wait(&sel_bar, (uint32_t)(l & 1));
+        STAMP(2);
+        // coarse sums of 64 bins (all loads first: independent chains)
+        if (NW == 16) {
+            int v[4];
+#pragma unroll
+            for (int j = 0; j < 4; j++) v[j] = hs[64 * (warp + 16 * j) + lane] + hs[64 * (warp + 16 * j) + 32 + lane];
+#pragma unroll
+            for (int j = 0; j < 4; j++) v[j] = __reduce_add_sync(0xffffffffu, v[j]);
+            if (lane == 0)
+#pragma unroll
+                for (int j = 0; j < 4; j++) hs[kBins + warp + 16 * j] = v[j];
+        } else {
+            for (int cidx = warp; cidx < 64; cidx += NW) {
                 const int v = __reduce_add_sync(0xffffffffu, hs[64 * cidx + lane] + hs[64 * cidx + 32 + lane]);
                 if (lane == 0) hs[kBins + cidx] = v;
             }
-            __syncthreads();
-            for (int t = warp; t < 3; t += NW) {
-                if (tg[t] <= 0) continue;
-                // coarse: lane covers descending coarse bins 63 - 2 lane, 62 - 2 lane
-                const int ca = hs[kBins + 63 - 2 * lane], cb = hs[kBins + 62 - 2 * lane];
-                int inc = ca + cb;
+        }
+        __syncthreads();
+        // Cut t (t = 0, 1, 2: the k16-th, (k16+k8)-th and k-th score in (score desc, id asc)
+        // order, R3) is found by warp t: suffix scans of the 64 coarse then 64 fine histogram
+        // bins locate the bin and the rank needed inside it.
+        for (int t = warp; t < 3; t += NW) {
+            if (tg(t) <= 0) continue;
+            const int ca = hs[kBins + 63 - 2 * lane], cb = hs[kBins + 62 - 2 * lane];
+            int inc = ca + cb;
 #pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int y = __shfl_up_sync(0xffffffffu, inc, o);
-                    if (lane >= o) inc += y;
-                }
-                int before = inc - ca - cb;  // count above this lane's first coarse bin
-                int cbin = -1, need = 0;
-                if (before < tg[t] && before + ca >= tg[t]) {
-                    cbin = 63 - 2 * lane;
-                    need = tg[t] - before;
-                } else if (before + ca < tg[t] && before + ca + cb >= tg[t]) {
-                    cbin = 62 - 2 * lane;
-                    need = tg[t] - before - ca;
-                }
-                const unsigned who = __ballot_sync(0xffffffffu, cbin >= 0);
-                if (!who) {  // histogram total < target: cannot happen with a consistent plan
-                    if (lane == 0) atomicOr(p.err, 8u);
-                    continue;
-                }
-                const int src = __ffs(who) - 1;
-                cbin = __shfl_sync(0xffffffffu, cbin, src);
-                need = __shfl_sync(0xffffffffu, need, src);
-                // fine bins of that coarse bin, descending
-                const int fa_ = hs[64 * cbin + 63 - 2 * lane];
-                const int fb_ = hs[64 * cbin + 62 - 2 * lane];
-                inc = fa_ + fb_;
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += y;
+            }
+            int before = inc - ca - cb;  // count above this lane's first coarse bin
+            int cbin = -1, need = 0;
+            if (before < tg(t) && before + ca >= tg(t)) {
+                cbin = 63 - 2 * lane;
+                need = tg(t) - before;
+            } else if (before + ca < tg(t) && before + ca + cb >= tg(t)) {
+                cbin = 62 - 2 * lane;
+                need = tg(t) - before - ca;
+            }
+            const unsigned who = __ballot_sync(0xffffffffu, cbin >= 0);
+            if (!who) {  // histogram total < target: cannot happen with a consistent plan
+                if (lane == 0) atomicOr(p.err, 8u);
+                continue;
+            }
+            const int src = __ffs(who) - 1;
+            cbin = __shfl_sync(0xffffffffu, cbin, src);
+            need = __shfl_sync(0xffffffffu, need, src);
+            const int fa_ = hs[64 * cbin + 63 - 2 * lane];
+            const int fb_ = hs[64 * cbin + 62 - 2 * lane];
+            inc = fa_ + fb_;
 #pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int y = __shfl_up_sync(0xffffffffu, inc, o);
-                    if (lane >= o) inc += y;
-                }
-                before = inc - fa_ - fb_;
-                int fbin = -1, fneed = 0, m = 0;
-                if (before < need && before + fa_ >= need) {
-                    fbin = 64 * cbin + 63 - 2 * lane;
-                    fneed = need - before;
-                    m = fa_;
-                } else if (before + fa_ < need && before + fa_ + fb_ >= need) {
-                    fbin = 64 * cbin + 62 - 2 * lane;
-                    fneed = need - before - fa_;
-                    m = fb_;
-                }
-                const int src2 = __ffs(__ballot_sync(0xffffffffu, fbin >= 0)) - 1;
-                fbin = __shfl_sync(0xffffffffu, fbin, src2);
-                fneed = __shfl_sync(0xffffffffu, fneed, src2);
-                m = __shfl_sync(0xffffffffu, m, src2);
-                if (lane == 0) {
-                    cut_bin[t] = fbin;
-                    cut_need[t] = fneed;
-                    ncand[t] = m;
-                }
-                if (m <= kBucket) {  // exact rank of the bucket's pairs: the fneed-th is the cut
-                    const int2 ci = lane < m ? __ldcg(bkt + (size_t)fbin * kBucket + lane) : make_int2(0, 0);
-                    int rank = 0;
-                    for (int j = 0; j < m; j++) {
-                        const int vj = __shfl_sync(0xffffffffu, ci.x, j), nj = __shfl_sync(0xffffffffu, ci.y, j);
-                        rank += (vj > ci.x) || (vj == ci.x && nj < ci.y);
-                    }
-                    if (lane < m && rank == fneed - 1) {
-                        cut_V[t] = ci.x;
-                        cut_I[t] = ci.y;
-                    }
-                }
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += y;
             }
-            __syncthreads();
-            if ((tg[0] > 0 && ncand[0] > kBucket) || (tg[1] > 0 && ncand[1] > kBucket) ||
-                (tg[2] > 0 && ncand[2] > kBucket)) {
-                // degenerate: all scores -> smem, binary searches with block-wide counts
-                int *sbuf = reinterpret_cast<int *>(S.ring + kSbufOff);
-                for (int n = tid; n < F_r; n += NT) sbuf[n] = __ldcg(p.s + n);
-                __syncthreads();
-                for (int t = 0; t < 3; t++) {
-                    if (tg[t] <= 0 || ncand[t] <= kBucket) continue;
-                    int lo = -p.smax, hi = p.smax;
-                    while (lo < hi) {  // largest V with #{s >= V} >= tg
-                        const int mid = lo + (hi - lo + 1) / 2;
-                        int c = 0;
-                        for (int n = tid; n < F_r; n += NT) c += sbuf[n] >= mid;
-                        if (block_sum(c, red_i) >= tg[t]) lo = mid;
-                        else hi = mid - 1;
-                    }
-                    const int V = lo;
-                    int c = 0;
-                    for (int n = tid; n < F_r; n += NT) c += sbuf[n] > V;
-                    const int R = tg[t] - block_sum(c, red_i);
-                    int ilo = 0, ihi = F_r - 1;
-                    while (ilo < ihi) {  // smallest I with #{n <= I : s == V} >= R
-                        const int mid = (ilo + ihi) >> 1;
-                        int c2_ = 0;
-                        for (int n = tid; n <= mid; n += NT) c2_ += sbuf[n] == V;
-                        if (block_sum(c2_, red_i) >= R) ihi = mid;
-                        else ilo = mid + 1;
-                    }
-                    if (tid == 0) {
-                        cut_V[t] = V;
-                        cut_I[t] = ilo;
-                    }
-                    __syncthreads();
-                }
+            before = inc - fa_ - fb_;
+            int fbin = -1, fneed = 0, m = 0;
+            if (before < need && before + fa_ >= need) {
+                fbin = 64 * cbin + 63 - 2 * lane;
+                fneed = need - before;
+                m = fa_;
+            } else if (before + fa_ < need && before + fa_ + fb_ >= need) {
+                fbin = 64 * cbin + 62 - 2 * lane;
+                fneed = need - before - fa_;
+                m = fb_;
             }
-            STAMP(10);
-            // classify this CTA's own neurons (P2's block, scores kept in smem); compact the
-            // selected ids of each tier in id order into this CTA's staging row
-            const int V0 = cut_V[0], V1 = cut_V[1], V2 = cut_V[2];
-            const int I0 = cut_I[0], I1 = cut_I[1], I2 = cut_I[2];
-            const int *own = reinterpret_cast<const int *>(S.ring + kOwnOff);
-            const int rps = (F_r + G - 1) / G;
-            const int n0 = cta * rps, nown = max(0, min(rps, F_r - n0));
-            int code = 3;
-            if (tid < nown) {
-                const int v = own[tid], n = n0 + tid;
-                const int a0 = (v > V0) | ((v == V0) & (n <= I0));
-                const int a1 = (v > V1) | ((v == V1) & (n <= I1));
-                const int a2 = (v > V2) | ((v == V2) & (n <= I2));
-                code = 3 - a0 - a1 - a2;  // nested cuts
-            }
-            const unsigned lt = (1u << lane) - 1u;
-            unsigned bal[3];
-#pragma unroll
-            for (int t = 0; t < 3; t++) bal[t] = __ballot_sync(0xffffffffu, code == t);
-            if (lane == 0)
-#pragma unroll
-                for (int t = 0; t < 3; t++) scan_sm[t * 32 + warp] = __popc(bal[t]);
-            __syncthreads();
-            if (code < 3) {
-                int pos = __popc(bal[code] & lt);
-                for (int w = 0; w < warp; w++) pos += scan_sm[code * 32 + w];
-                p.stage[((size_t)code * G + cta) * rps + pos] = n0 + tid;
-            }
-            if (tid < 3) {
-                int c = 0;
-                for (int w = 0; w < NW; w++) c += scan_sm[tid * 32 + w];
-                p.ccount[cta * 4 + tid] = c;
+            const int src2 = __ffs(__ballot_sync(0xffffffffu, fbin >= 0)) - 1;
+            fbin = __shfl_sync(0xffffffffu, fbin, src2);
+            fneed = __shfl_sync(0xffffffffu, fneed, src2);
+            m = __shfl_sync(0xffffffffu, m, src2);
+            if (lane == 0) {
+                cut_bin[t] = fbin;
+                cut_need[t] = fneed;
+                ncand[t] = m;
             }
         }
-        STAMP(11);
-        grid_sync(p.bar_flags, base + ++nbar, p.err);
-        STAMP(12);
-
-        // ================= P3b: this CTA's share of the tier lists ============================
+        __syncthreads();
+        STAMP(3);
+        auto id_of = [&](int e, int key) { return (e / RP) * rps + 255 - (key & 255); };  // e: run-array index
+        // The steps below are warp-cooperative and compact (the layer loop's code does not fit
+        // the instruction cache; straight-line single-thread code here is fetch-bound):
+        // warp w takes runs c = w, w + NW, ...; lane j holds key e0 + j of the run.
+        int *pcum = reinterpret_cast<int *>(S.ring + kCcOff);   // [G][4]: #keys >= K0, K1, K2
+        int *pex = reinterpret_cast<int *>(S.ring + kExOff);    // [G][4]: list positions per tier
+        {  // candidates: the (score, id) pairs of each cut bin -- the top of every sorted run
+            int2 *cand = reinterpret_cast<int2 *>(S.ring + kCandOff);
+            // value interval of each cut bin (bins 0 and 4095 are clamped: open-ended)
+            int lo[3], hi[3], LO = 0x7fffffff;
+#pragma unroll
+            for (int t = 0; t < 3; t++) {
+                const int b = cut_bin[t];
+                lo[t] = b <= 0 ? -0x7fffffff : (b - 2048) * (1 << shl);
+                hi[t] = b >= 4095 ? 0x7fffffff : (b - 2047) * (1 << shl) - 1;
+                if (b < 0) {
+                    lo[t] = 0x7fffffff;
+                    hi[t] = (int)0x80000000;
+                }
+                LO = min(LO, lo[t]);
+            }
+            auto cand_add = [&](bool h0, bool h1, bool h2, int v, int n) {
+                if (h0) {
+                    const int at = atomicAdd(&ccnt[0], 1);
+                    if (at < kCand) cand[at] = make_int2(v, n);
+                }
+                if (h1) {
+                    const int at = atomicAdd(&ccnt[1], 1);
+                    if (at < kCand) cand[kCand + at] = make_int2(v, n);
+                }
+                if (h2) {
+                    const int at = atomicAdd(&ccnt[2], 1);
+                    if (at < kCand) cand[2 * kCand + at] = make_int2(v, n);
+                }
+            };
+            const int lo0 = lo[0], hi0 = hi[0], lo1 = lo[1], hi1 = hi[1], lo2 = lo[2], hi2 = hi[2];
+            // thread (run c, cut t): two binary searches in the sorted run give the keys above
+            // cut t's bin (all in cut t's prefix) and the bin's members (the candidates)
+#pragma unroll 1
+            for (int it = tid; it < 3 * G; it += NT) {
+                const int t = it / G, c = it - t * G;
+                if (cut_bin[t] < 0) {
+                    if (t == 0) pcum[4 * c + 3] = 0;
+                    pcum[4 * c + t] = 0;
+                    continue;
+                }
+                const int nown = min(rps, F_r - c * rps);
+                const int lt = t == 0 ? lo0 : (t == 1 ? lo1 : lo2), ht = t == 0 ? hi0 : (t == 1 ? hi1 : hi2);
+                // #keys >= X in run c (keys descend); X as a 64-bit value (bin edges may be open)
+                auto count_ge = [&](long long X) {
+                    int a = 0, b = nown;
+                    while (a < b) {
+                        const int mid = (a + b) >> 1;
+                        if ((long long)runkey(c, mid) >= X) a = mid + 1;
+                        else b = mid;
+                    }
+                    return a;
+                };
+                const int ia = count_ge(((long long)ht + 1) * 256);  // v > ht
+                const int ib = count_ge((long long)lt * 256);        // v >= lt
+                pcum[4 * c + t] = ia;
+                for (int e = ia; e < ib; e++) {  // the bin's members (few)
+                    const int key = runkey(c, e);
+                    cand_add(t == 0, t == 1, t == 2, key >> 8, c * rps + 255 - (key & 255));
+                }
+            }
+            __syncthreads();
+            STAMP(16);
+            // exact rank of the candidates of cut t (warp t): the need-th in (score desc, id asc)
+            for (int t = warp; t < 3; t += NW) {
+                const int m = ncand[t];
+                if (tg(t) <= 0 || m > kCand) continue;
+                if (ccnt[t] != m && lane == 0) atomicOr(p.err, 8u);
+                const int2 c0 = lane < m ? cand[t * kCand + lane] : make_int2(0, 0);
+                const int2 c1 = lane + 32 < m ? cand[t * kCand + lane + 32] : make_int2(0, 0);
+                int r0 = 0, r1 = 0;
+#pragma unroll 1
+                for (int j = 0; j < m; j++) {
+                    const int2 cj = cand[t * kCand + j];
+                    r0 += (cj.x > c0.x) || (cj.x == c0.x && cj.y < c0.y);
+                    r1 += (cj.x > c1.x) || (cj.x == c1.x && cj.y < c1.y);
+                }
+                const int want = cut_need[t] - 1;
+                if (lane < m && r0 == want) {
+                    cut_V[t] = c0.x;
+                    cut_I[t] = c0.y;
+                }
+                if (lane + 32 < m && r1 == want) {
+                    cut_V[t] = c1.x;
+                    cut_I[t] = c1.y;
+                }
+                __syncwarp();
+                // the bin's members ranked at or above the cut belong to its prefix
+                if (lane < m && r0 <= want) atomicAdd(&pcum[4 * (c0.y / rps) + t], 1);
+                if (lane + 32 < m && r1 <= want) atomicAdd(&pcum[4 * (c1.y / rps) + t], 1);
+            }
+            __syncthreads();
+        }
+        const bool degenerate = (tg(0) > 0 && ncand[0] > kCand) || (tg(1) > 0 && ncand[1] > kCand) ||
+                                (tg(2) > 0 && ncand[2] > kCand);
+        if (degenerate) {
+            // degenerate (massive ties in one bin): binary searches with block-wide counts over
+            // all keys (padding entries never count: their score is below -smax)
+            for (int t = 0; t < 3; t++) {
+                if (tg(t) <= 0 || ncand[t] <= kCand) continue;
+                int lo = -p.smax, hi = p.smax;
+                while (lo < hi) {  // largest V with #{s >= V} >= tg
+                    const int mid = lo + (hi - lo + 1) / 2;
+                    int c = 0;
+                    for (int e = tid; e < G * RP; e += NT) c += (__ldcg(p.runs + e) >> 8) >= mid;
+                    if (block_sum(c, red_i) >= tg(t)) lo = mid;
+                    else hi = mid - 1;
+                }
+                const int V = lo;
+                int c = 0;
+                for (int e = tid; e < G * RP; e += NT) c += (__ldcg(p.runs + e) >> 8) > V;
+                const int R = tg(t) - block_sum(c, red_i);
+                int ilo = 0, ihi = F_r - 1;
+                while (ilo < ihi) {  // smallest I with #{n <= I : s == V} >= R
+                    const int mid = (ilo + ihi) >> 1;
+                    int c2_ = 0;
+                    for (int e = tid; e < G * RP; e += NT) {
+                        const int key = __ldcg(p.runs + e);
+                        c2_ += (key >> 8) == V && key != (int)0x80000000 && id_of(e, key) <= mid;
+                    }
+                    if (block_sum(c2_, red_i) >= R) ihi = mid;
+                    else ilo = mid + 1;
+                }
+                if (tid == 0) {
+                    cut_V[t] = V;
+                    cut_I[t] = ilo;
+                }
+                __syncthreads();
+            }
+        }
+        STAMP(10);
+        // classify and compact.  The tier-t members of run c are a contiguous segment of it
+        // (keys >= K_t(c), nested; K_t(c) is cut t's key as seen from c's local ids): ballots
+        // count them per run, warp 0 scans the counts over runs into list positions, and the
+        // few runs meeting this CTA's share of a tier list write its ids (ascending-id order
+        // inside a segment = ascending local index).
         int n_items, c1, c2;
         {
-            // thread-contiguous source CTAs: their counts (one 16-B load each), a block scan of
-            // the three tier counts -> each source's list offsets; every thread copies the part of
-            // its sources' ids that falls into this CTA's share [lo_t, hi_t)
-            constexpr int kMaxCPT = 5;  // G <= 160, blockDim >= 32
-            const int CPT = (G + NT - 1) / NT;
-            const int cA = min(G, tid * CPT), cB = min(G, cA + CPT);
-            int4 *cc = reinterpret_cast<int4 *>(S.ring + kSbufOff);  // this thread's sources' counts
-            int sum3[3] = {0, 0, 0};
-#pragma unroll
-            for (int k = 0; k < kMaxCPT; k++) {
-                const int4 q = (k < CPT && cA + k < cB) ? __ldcg(reinterpret_cast<const int4 *>(p.ccount) + cA + k)
-                                                        : make_int4(0, 0, 0, 0);
-                if (k < CPT && cA + k < cB) cc[cA + k] = q;
-                sum3[0] += q.x;
-                sum3[1] += q.y;
-                sum3[2] += q.z;
-            }            int ex[3], tot[3];
-            block_exscan3(sum3, ex, tot, scan_sm);
-            int rg[6];
-#pragma unroll
-            for (int i = 0; i < 6; i++) rg[i] = sm.rng[i];
-            const int off1 = rg[1] - rg[0], off2 = off1 + rg[3] - rg[2];
+            const int r0 = sm.rng[0], r1 = sm.rng[1], r2 = sm.rng[2], r3 = sm.rng[3], r4 = sm.rng[4],
+                      r5 = sm.rng[5];
+            const int off1 = r1 - r0, off2 = off1 + r3 - r2;
             c1 = off1;
             c2 = off2;
-            n_items = off2 + rg[5] - rg[4];
-            const int rps = (F_r + G - 1) / G;
-            const int offs[3] = {0, off1, off2};
-            const int segs[3] = {0, p.k16, p.k16 + p.k8};
-#pragma unroll
-            for (int k = 0; k < kMaxCPT; k++) {
-                if (k >= CPT || cA + k >= cB) break;
-                const int c = cA + k;
-                const int4 q = cc[c];
-                const int cnt[3] = {q.x, q.y, q.z};
+            n_items = off2 + r5 - r4;
+            if (degenerate) {  // massive ties: exact per-run counts against the cut keys
+            int *pK = pex;  // [G][4] per-run cut keys (pex is written only after they are used)
+            for (int c = tid; c < G; c += NT) {  // cut t's key as seen from run c's local ids:
+                int kq[3];                        // key >= K <=> s > V, or s == V and local <= loc
 #pragma unroll
                 for (int t = 0; t < 3; t++) {
-                    const int s0 = ex[t];
-                    ex[t] += cnt[t];
-                    const int a = max(rg[2 * t], s0), b = min(rg[2 * t + 1], s0 + cnt[t]);
-                    const int *src = p.stage + ((size_t)t * G + c) * rps - s0;
-                    for (int pos0 = a; pos0 < b; pos0 += 8) {
-                        int ids[8];
+                    const int V = cut_V[t], loc = cut_I[t] - c * rps;
+                    kq[t] = cut_I[t] < 0 ? 0x7fffffff : (loc < 0 ? (V + 1) * 256 : V * 256 + 255 - min(loc, 255));
+                }
+                *reinterpret_cast<int4 *>(pK + 4 * c) = make_int4(kq[0], kq[1], kq[2], 0);
+            }
+            __syncthreads();
+#pragma unroll 1
+            for (int c = warp; c < G; c += NW) {
+                const int nown = min(rps, F_r - c * rps);
+                const int4 K = *reinterpret_cast<const int4 *>(pK + 4 * c);
+                const int key = lane < nown ? ts[c * T + lane] : (int)0x80000000;
+                int q2 = __popc(__ballot_sync(0xffffffffu, key >= K.z));
+                int q1 = __popc(__ballot_sync(0xffffffffu, key >= K.y));
+                int q0 = __popc(__ballot_sync(0xffffffffu, key >= K.x));
+                if (q2 == 32 && nown > 32) {  // rare: the k-th cut is past key 32 of this run
+#pragma unroll 1
+                    for (int e0 = 32; e0 < nown; e0 += 32) {
+                        const int e = e0 + lane;
+                        const int k2 = e < nown ? runkey(c, e) : (int)0x80000000;
+                        q2 += __popc(__ballot_sync(0xffffffffu, k2 >= K.z));
+                        q1 += __popc(__ballot_sync(0xffffffffu, k2 >= K.y));
+                        q0 += __popc(__ballot_sync(0xffffffffu, k2 >= K.x));
+                        if (__shfl_sync(0xffffffffu, k2, 31) < K.z) break;
+                    }
+                }
+                if (lane == 0) *reinterpret_cast<int4 *>(pcum + 4 * c) = make_int4(q0, q1, q2, 0);
+            }
+            }
+            __syncthreads();
+            STAMP(18);
+            if (warp == 0) {  // exclusive scan of the per-run tier counts over runs
+                const int SP = (G + 31) / 32, ca = min(G, lane * SP), cz = min(G, ca + SP);
+                int s0 = 0, s1 = 0, s2 = 0;
+                for (int c = ca; c < cz; c++) {
+                    const int4 q = *reinterpret_cast<const int4 *>(pcum + 4 * c);
+                    s0 += q.x;
+                    s1 += q.y - q.x;
+                    s2 += q.z - q.y;
+                }
+                int i0 = s0, i1 = s1, i2 = s2;
 #pragma unroll
-                        for (int u = 0; u < 8; u++) ids[u] = pos0 + u < b ? __ldcg(src + pos0 + u) : 0;
-#pragma unroll
-                        for (int u = 0; u < 8; u++)
-                            if (pos0 + u < b) {
-                                S.loc[offs[t] + pos0 + u - rg[2 * t]] = ids[u];
-                                lst[segs[t] + pos0 + u] = ids[u];
-                            }
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y0 = __shfl_up_sync(0xffffffffu, i0, o), y1 = __shfl_up_sync(0xffffffffu, i1, o),
+                              y2 = __shfl_up_sync(0xffffffffu, i2, o);
+                    if (lane >= o) {
+                        i0 += y0;
+                        i1 += y1;
+                        i2 += y2;
+                    }
+                }
+                int e0 = i0 - s0, e1 = i1 - s1, e2 = i2 - s2;
+                for (int c = ca; c < cz; c++) {
+                    const int4 q = *reinterpret_cast<const int4 *>(pcum + 4 * c);
+                    *reinterpret_cast<int4 *>(pex + 4 * c) = make_int4(e0, e1, e2, 0);
+                    e0 += q.x;
+                    e1 += q.y - q.x;
+                    e2 += q.z - q.y;
+                }
+                if (lane == 31 && (i0 != p.k16 || i1 != p.k8 || i2 != p.k4)) atomicOr(p.err, 8u);
+            }
+            __syncthreads();
+            STAMP(19);
+            const int sg1 = p.k16, sg2 = p.k16 + p.k8;
+            // work items: the (run, tier) segments that meet this CTA's share (thread per run)
+            int *work = reinterpret_cast<int *>(S.ring + kWorkOff);  // [<= 3 G]
+            if (tid == 0) ccnt[0] = 0;
+            __syncthreads();
+            for (int c = tid; c < G; c += NT) {
+                const int4 q = *reinterpret_cast<const int4 *>(pcum + 4 * c);
+                const int4 x = *reinterpret_cast<const int4 *>(pex + 4 * c);
+                if (x.x < r1 && x.x + q.x > r0) work[atomicAdd(&ccnt[0], 1)] = 4 * c;
+                if (x.y < r3 && x.y + q.y - q.x > r2) work[atomicAdd(&ccnt[0], 1)] = 4 * c + 1;
+                if (x.z < r5 && x.z + q.z - q.y > r4) work[atomicAdd(&ccnt[0], 1)] = 4 * c + 2;
+            }
+            __syncthreads();
+            const int nwork = ccnt[0];
+#pragma unroll 1
+            for (int w = warp; w < nwork; w += NW) {
+                const int c = work[w] >> 2, t = work[w] & 3;
+                const int4 q = *reinterpret_cast<const int4 *>(pcum + 4 * c);
+                const int4 x = *reinterpret_cast<const int4 *>(pex + 4 * c);
+                const int seg0 = t == 0 ? 0 : (t == 1 ? q.x : q.y), seg1 = t == 0 ? q.x : (t == 1 ? q.y : q.z);
+                const int pa = t == 0 ? x.x : (t == 1 ? x.y : x.z);
+                const int ra = t == 0 ? r0 : (t == 1 ? r2 : r4), rb = t == 0 ? r1 : (t == 1 ? r3 : r5);
+                const int off = t == 0 ? 0 : (t == 1 ? off1 : off2);
+                const int sg = t == 0 ? 0 : (t == 1 ? sg1 : sg2);
+#pragma unroll 1
+                for (int i0 = seg0; i0 < seg1; i0 += 32) {
+                    const int i = i0 + lane;
+                    const int lc = i < seg1 ? 255 - (runkey(c, i) & 255) : 0x40000000;
+                    int rk = 0;  // members with a smaller id come first
+#pragma unroll 1
+                    for (int j = seg0; j < seg1; j++) rk += (255 - (runkey(c, j) & 255)) < lc;
+                    const int pos = pa + rk;
+                    if (i < seg1 && pos >= ra && pos < rb) {
+                        S.loc[off + pos - ra] = c * rps + lc;
+                        lst[sg + pos] = c * rps + lc;
                     }
                 }
             }
-            if (tid == 0) {
-                if (tot[0] != p.k16 || tot[1] != p.k8 || tot[2] != p.k4) atomicOr(p.err, 8u);
+            if (tid == 0)
                 for (int t = 0; t < 3; t++) fa.pool[t] = Ld.pool[t];
-            }
-            STAMP(13);
+            STAMP(11);
             fence_proxy_async();  // generic smem traffic in the ring precedes the TMA writes
             __syncthreads();
         }
@@ -664,15 +775,34 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
             jb += (unsigned)n_items;
         }
         STAMP(6);
-        grid_sync(p.bar_flags, base + ++nbar, p.err);
+        // barrier By; meanwhile (warp 1, in TMA-queue order): this CTA's A^T chunks of layer
+        // l+1 -> smem for R, then L2 prefetches: layer l+1's B slice and the previous token's
+        // records of layer l+1, layer l+2's A^T chunks (staged at the next By)
+        grid_sync(p.bar_flags, base + ++nbar, p.err, [&] {
+            if (l + 1 < p.n_layers) {
+                if ((threadIdx.x & 31) == 0 && cta < nchunk) {
+                    fence_proxy_async();  // the FFN's generic reads of the ring precede the copy
+                    const int nown = (nchunk - cta + G - 1) / G;
+                    const uint32_t bytes = 32u * (uint32_t)r;
+                    mbar_expect_tx(&at_bar, bytes * nown);
+                    for (int q = 0; q < nown; q++)
+                        bulk_g2s_plain(S.ring + kAtOff + q * bytes,
+                                       p.layers[l + 1].At + (int64_t)(cta + q * G) * bytes, bytes, &at_bar);
+                }
+                prefetch_layers(p, l + 1, l + 2 < p.n_layers ? l + 2 : -1, l + 1);
+            }
+        });
         STAMP(7);
         if (l == p.n_layers - 1 && cta == G - 1)  // leave both histograms clear for the next token
-            for (int i = tid; i < kBins; i += NT) hist[i] = 0;
+            for (int i = tid; i < kHistW; i += NT) hist[i] = 0;
 
-        // ================= P5: fixed-order reduction + residual ==========================
+        // ================= R: fixed-order reduction + residual + next layer's h ==============
         {
+            const bool more = l + 1 < p.n_layers;
+            long long *hnext = p.hb + (int64_t)((l + 1) & 1) * r * kHStride;
             float(*rf)[33] = reinterpret_cast<float(*)[33]>(S.ring);
-            for (int ch = cta; ch < d / 32; ch += G) {
+            const __half *xs_h = reinterpret_cast<const __half *>(S.xs);
+            for (int ch = cta; ch < nchunk; ch += G) {
                 const int e = ch * 32 + lane;
                 // the k_reduce order: virtual warp w sums rows w::32; two per pass, loads in flight
                 for (int w = warp; w < 32; w += 2 * NW) {
@@ -702,10 +832,24 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
                     float y = 0.f;
 #pragma unroll
                     for (int w = 0; w < 32; w++) y += rf[w][lane];
-                    const __half yh = __float2half_rn(y);
-                    p.x[e] = __hadd(__ldcg(p.x + e), yh);
+                    const __half xn = __hadd(xs_h[e], __float2half_rn(y));
+                    p.x[e] = xn;
+                    if (more) {
+                        bool bad = false;
+                        int m, sh;
+                        fp16_fixed(__half_as_ushort(xn), m, sh, bad);
+                        if (bad) atomicOr(p.err, 1u);
+                        xm[lane] = m;
+                        xsh[lane] = sh;
+                    }
                 }
                 __syncthreads();
+                if (more) {
+                    if (ch == cta) mbar_wait(&at_bar, (uint32_t)(l & 1));  // A^T chunks staged at By
+                    h_chunk(reinterpret_cast<const int8_t *>(S.ring + kAtOff) + (ch - cta) / G * 32 * r, r,
+                            xm, xsh, hnext);
+                    __syncthreads();
+                }
             }
         }
         STAMP(8);
@@ -719,9 +863,15 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
 }  // namespace
 
 size_t decode_layer_table_bytes(int n_layers) { return sizeof(DecLayer) * (size_t)n_layers; }
-size_t decode_bucket_bytes() { return (size_t)2 * kBins * kBucket * sizeof(int2); }
-// scores fit the fallback buffer; a CTA's own neurons fit one pass of its threads and kOwnOff
-int decode_max_F() { return (kRing - kSbufOff) / 4; }
+size_t decode_hist_bytes() { return sizeof(int) * 2 * (size_t)kHistW; }
+// run prefix every CTA copies: ~2x a CTA's expected share of the active set, 16-B rows
+// (the whole run: a probe past a partial prefix would stall its warp on an L2 load)
+int decode_top_len(const m2c_ctx *c) {
+    const int G = c->G, rps = (c->F_r + G - 1) / G;
+    return (rps + 3) & ~3;
+}
+// all runs fit the ring behind the histogram scratch; run keys hold local indices < 255
+int decode_max_F() { return 254 * 148 < (kRing - kSbufOff) / 4 - 4 * 148 ? 254 * 148 : (kRing - kSbufOff) / 4 - 4 * 148; }
 
 cudaError_t init_decode_attrs() {
     cudaError_t e = cudaFuncSetAttribute(k_decode<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -736,7 +886,7 @@ cudaError_t decode_write_layer_table(m2c_ctx *c, void *dev_table) {
     std::vector<DecLayer> t(c->desc.n_layers);
     for (int l = 0; l < c->desc.n_layers; l++) {
         const LayerState &L = c->layers[l];
-        t[l].A = L.A;
+        t[l].At = L.A;
         t[l].B = L.B;
         for (int k = 0; k < 3; k++) t[l].pool[k] = L.pool[k];
     }
@@ -756,15 +906,15 @@ cudaError_t launch_decode(m2c_ctx *c, __half *x, unsigned long long *prof, cudaS
     a.k8 = c->plan.k_int8;
     a.k4 = c->plan.k_int4;
     a.smax = c->sel_smax;
-    a.sh = c->sel_sh;
     for (int t = 0; t < 3; t++) {
         a.nb[t] = (int)c->nb[t];
         a.wt[t] = ffn_weight(c->nb[t], d);
     }
     a.x = x;
-    a.h = c->ws.h;
-    a.s = c->ws.s;
-    a.ghist = c->ghist;
+    a.hb = c->dec_hb;
+    a.runs = c->dec_runs;
+    a.T = decode_top_len(c);
+    a.ghist = c->dec_hist;
     a.lists = c->prev_ids;
     a.partial = c->ws.partial;
     a.bar_flags = c->bar_flags;
@@ -772,12 +922,8 @@ cudaError_t launch_decode(m2c_ctx *c, __half *x, unsigned long long *prof, cudaS
     a.err = c->ws.err;
     a.prof = prof;
     a.bin_sh = c->dec_bin_sh;
-    a.bucket = reinterpret_cast<int2 *>(c->dec_bucket);
-    a.stage = c->dec_stage;
-    a.ccount = c->dec_ccount;
     a.sabs = c->dec_sabs;
-    // M2C_DECODE_PREFETCH: 0 none, 1 predictor slices + previous-token records (default),
-    // 2 predictor slices only (tuning / measurement knob; results are identical)
+    // M2C_DECODE_PREFETCH (see prefetch_layers; a tuning / measurement knob, results are identical)
     {
         const char *ev = getenv("M2C_DECODE_PREFETCH");
         a.prefetch = ev ? atoi(ev) : 1;

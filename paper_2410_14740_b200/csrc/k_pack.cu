@@ -102,7 +102,29 @@ __global__ void __launch_bounds__(256) k_pack_f16(int d, const __half *__restric
     }
 }
 
+// predictor factor A [r][d] (row-major, as the caller passes it) -> A^T [d][r]: the decode
+// path forms h = A x from column slices of A, so each slice must be contiguous
+__global__ void __launch_bounds__(256) k_transpose_i8(int r, int d, const int8_t *__restrict__ A,
+                                                      int8_t *__restrict__ At) {
+    __shared__ int8_t tile[32][33];
+    const int j0 = blockIdx.x * 32, i0 = blockIdx.y * 32;
+    for (int e = threadIdx.x; e < 1024; e += blockDim.x) {
+        const int i = e >> 5, j = e & 31;
+        if (i0 + i < r && j0 + j < d) tile[i][j] = A[(int64_t)(i0 + i) * d + j0 + j];
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < 1024; e += blockDim.x) {
+        const int j = e >> 5, i = e & 31;
+        if (i0 + i < r && j0 + j < d) At[(int64_t)(j0 + j) * r + i0 + i] = tile[i][j];
+    }
+}
+
 }  // namespace
+
+cudaError_t launch_transpose_i8(int r, int d, const int8_t *A, int8_t *At, cudaStream_t st) {
+    k_transpose_i8<<<dim3((d + 31) / 32, (r + 31) / 32), 256, 0, st>>>(r, d, A, At);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_pack(int d, int bits, const __half *g, const __half *u, const __half *dn,
                         int64_t n0, int64_t n1, uint8_t *out, cudaStream_t st) {

@@ -28,7 +28,11 @@ m2c_status cuda_fail(cudaError_t e, const char *what);
 
 constexpr int kMaxPoolSlots = 8192;  // LRU / ATU pool limit (single-CTA bitonic victim sort)
 constexpr int kSelectThreads = 1024;
-constexpr int kDecodeStamps = 16;  // k_decode profiling stamps per (layer, CTA)
+constexpr int kDecodeStamps = M2C_DECODE_STAMPS;  // k_decode profiling stamps per (layer, CTA)
+// h = A x accumulators are int64 words kHStride apart (one 256-B L2 line each): every CTA
+// adds its column-slice partial sums with red.add.u64, and a packed [r] array would put all
+// r counters into a handful of L2 slices whose atomic units serialise them
+constexpr int kHStride = 32;
 
 // ----------------------------------------------------------------------------------------
 // context
@@ -37,7 +41,7 @@ struct LayerState {
     bool loaded = false;
     int mode = 0;  // 0 resident, 1 lru, 2 atu
     int cap[3] = {0, 0, 0};
-    const int8_t *A = nullptr;  // [r][d]
+    const int8_t *A = nullptr;  // A^T: [d][r] (column j of the low-rank factor A is row j)
     const int8_t *B = nullptr;  // [F_r][r]
     uint8_t *pool[3] = {nullptr, nullptr, nullptr};
     int32_t *occupant[3] = {nullptr, nullptr, nullptr};
@@ -51,7 +55,7 @@ struct NcclApi;  // dlopen'd NCCL entry points
 
 
 struct Workspace {
-    int32_t *h = nullptr;          // [r]
+    long long *h = nullptr;        // [r][kHStride]: h_i = (A x)_i at h[i * kHStride] (R2)
     int32_t *s = nullptr;          // [F_r]
     int32_t *tier_ids = nullptr;   // [F_r]
     int8_t *tier_of = nullptr;     // [F_r]
@@ -107,9 +111,9 @@ struct m2c_ctx {
     unsigned *bar_epoch = nullptr;
     unsigned long long *dec_prof = nullptr;  // [n_layers][G][kDecodeStamps]
     int *dec_bin_sh = nullptr;       // [n_layers] k_decode histogram scale per layer
-    void *dec_bucket = nullptr;      // [2][4096][32] int2 (score, id) per histogram bin
-    int *dec_stage = nullptr;        // [3][G][ceil(F_r / G)] per-CTA selected ids
-    int *dec_ccount = nullptr;       // [G][4] per-CTA tier counts
+    long long *dec_hb = nullptr;     // [2][r][kHStride] k_decode h accumulators (layer parity)
+    int *dec_runs = nullptr;         // [G][RP] k_decode per-CTA sorted score keys
+    int *dec_hist = nullptr;         // [2][4096 + 64] k_decode score histograms
     unsigned *dec_sabs = nullptr;    // [G] per-CTA max |s| scratch
     bool dec_table_dirty = true;
     bool last_token_fused = false;
@@ -135,6 +139,7 @@ struct PrefetchArgs {
     int k[3] = {0, 0, 0};
     int F_r = 0;
 };
+cudaError_t launch_transpose_i8(int r, int d, const int8_t *A, int8_t *At, cudaStream_t st);
 cudaError_t launch_predict(m2c_ctx *c, const LayerState &L, const __half *x, int32_t *scores,
                            int *hist, const int32_t *prefetch_ids, cudaStream_t st);
 cudaError_t launch_select(m2c_ctx *c, const int32_t *scores, int *hist, const m2c_tier_plan &p,
@@ -157,8 +162,9 @@ cudaError_t launch_decode(m2c_ctx *c, __half *x, unsigned long long *prof, cudaS
 cudaError_t init_decode_attrs();
 cudaError_t decode_write_layer_table(m2c_ctx *c, void *dev_table);
 size_t decode_layer_table_bytes(int n_layers);
-size_t decode_bucket_bytes();
 int decode_max_F();
+size_t decode_hist_bytes();
+int decode_top_len(const m2c_ctx *c);
 cudaError_t init_select_attrs();
 cudaError_t init_cache_attrs();
 cudaError_t init_ffn_attrs();
@@ -236,6 +242,13 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
         "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
         : "memory");
 }
+__device__ __forceinline__ void bulk_g2s_plain(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
 // bulk L2 prefetch (no smem destination); size multiple of 16, address 16-B aligned
 __device__ __forceinline__ void prefetch_l2(const void *p, uint32_t bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes & ~15u) : "memory");
@@ -257,29 +270,40 @@ __device__ __forceinline__ float warp_sum_f(float v) {
     return v;
 }
 
-// exact sgn(v) * floor((254|v| + M) / (2M)) for |v| <= M < 2^45 (R2); double division is
-// correctly rounded and num, den < 2^53 are exact, so the floor is off by at most one and
-// the two integer checks fix it.
-// Same exact result from an fp32 estimate est ~= 127 |v| / M + 0.5 (|error| << 1): the floor
-// of the estimate is within one of the exact value and two int64 checks pin it.
-__device__ __forceinline__ int quant127_est(long long v, long long M, float est) {
+// O3 (R2): exact round-half-up of 127 a / M for 0 <= a <= M < 2^62, i.e.
+// floor((254 a + M) / (2 M)).  The fp64 estimate is within one of the answer; two 128-bit
+// integer checks pin it.
+__device__ __forceinline__ int quant127_u64(unsigned long long a, unsigned long long M) {
     if (M == 0) return 0;
-    const long long a = v < 0 ? -v : v;
-    const long long num = 254 * a + M, den = 2 * M;
-    long long q = (long long)__float2int_rd(est);
-    if (q * den > num) q -= 1;
-    else if ((q + 1) * den <= num) q += 1;
-    return (int)(v < 0 ? -q : q);
+    int q = (int)fma((double)a, 127.0 / (double)M, 0.5);
+    q = q < 0 ? 0 : (q > 127 ? 127 : q);
+    // q is right iff (2q - 1) M <= 254 a < (2q + 1) M; products as (hi, lo) 128-bit pairs
+    const unsigned long long al = a * 254ull, ah = __umul64hi(a, 254ull);
+    auto lt = [&](unsigned long long k) {  // 254 a < k M ?
+        const unsigned long long ml = M * k, mh = __umul64hi(M, k);
+        return ah < mh || (ah == mh && al < ml);
+    };
+    if (!lt((unsigned long long)(2 * q + 1))) q += 1;
+    else if (q > 0 && lt((unsigned long long)(2 * q - 1))) q -= 1;
+    return q;
 }
-
-__device__ __forceinline__ int quant127(long long v, long long M) {
-    if (M == 0) return 0;
-    long long a = v < 0 ? -v : v;
-    long long num = 254 * a + M, den = 2 * M;
-    long long q = (long long)floor((double)num / (double)den);
-    if (q * den > num) q -= 1;
-    if ((q + 1) * den <= num) q += 1;
-    return (int)(v < 0 ? -q : q);
+// x_j 2^24 as an exact integer (O1): mantissa m (signed, |m| < 2^11) and shift sh, X = m << sh.
+// Inf / NaN: m = 0 and *bad set.
+__device__ __forceinline__ void fp16_fixed(unsigned b, int &m, int &sh, bool &bad) {
+    const int e = (b >> 10) & 31;
+    m = b & 1023;
+    sh = 0;
+    if (e == 31) {
+        bad = true;
+        m = 0;
+    } else if (e) {
+        m |= 1024;
+        sh = e - 1;
+    }
+    if (b & 0x8000) m = -m;
+}
+__device__ __forceinline__ void red_add_u64(long long *p, long long v) {
+    asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
 }  // namespace m2c

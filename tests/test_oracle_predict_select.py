@@ -1,7 +1,8 @@
 """Pins for oracle O1-O5 (exact-integer predictor, top-k, tier split).
 
-Pinned against: numpy int64 matmul (library routine) for O2/O4; closed-form special cases
-(x = 0, x = c*e_j, half-up ties) for O1/O3; python ``sorted`` brute force for O5; SPEC's
+Pinned against: python big-integer matmul on exact rationals for O1/O2, numpy int64 matmul
+(library routine) for O4; closed-form special cases (x = 0, x = c*e_j, subnormals, fp16-max
+magnitudes, half-up ties) for O2/O3; python ``sorted`` brute force for O5; SPEC's
 partition example 250/250/500 and the survey's per-config tier counts.
 """
 from fractions import Fraction
@@ -29,36 +30,67 @@ def _rand_pred(d, r, F, seed):
     return x, A, B
 
 
+def _X(x):
+    # x_j * 2^24 as an exact python integer (exact rationals, independent of the C conversion)
+    return [int(Fraction(float(v)) * (1 << 24)) for v in np.asarray(x, np.float16).astype(np.float64)]
+
+
 @pytest.mark.parametrize("seed", range(4))
-def test_predictor_matches_int64_matmul_and_exact_rounding(seed):
+def test_predictor_matches_bigint_matmul_and_exact_rounding(seed):
     d, r, F = 256, 32, 688
     x, A, B = _rand_pred(d, r, F, seed)
     out = orc.predict(x, A, B)
-    X = [int(Fraction(float(v)) * (1 << 24)) for v in x.astype(np.float64)]
-    M = max(abs(v) for v in X)
-    assert [int(q) for q in out["xq"]] == [_exact_q127(v, M) for v in X]
-    h = A.astype(np.int64) @ out["xq"].astype(np.int64)
-    assert np.array_equal(out["h"], h)
-    Mh = int(np.abs(h).max())
-    assert [int(q) for q in out["hq"]] == [_exact_q127(int(v), Mh) for v in h]
+    X = _X(x)
+    h = [sum(int(a) * xv for a, xv in zip(row, X)) for row in A.tolist()]  # python big ints
+    assert [int(v) for v in out["h"]] == h
+    Mh = max(abs(v) for v in h)
+    assert [int(q) for q in out["hq"]] == [_exact_q127(v, Mh) for v in h]
     assert np.array_equal(out["s"], B.astype(np.int64) @ out["hq"].astype(np.int64))
-    assert np.abs(out["xq"]).max() == 127 and np.abs(out["hq"]).max() == 127
+    assert np.abs(out["hq"]).max() == 127
+
+
+def test_predictor_extreme_magnitudes_no_overflow():
+    # |x| = 65504 (fp16 max) everywhere with A = +-127: |h| ~ 2^59.9 must stay exact (int64)
+    d, r, F = 8192, 4, 8
+    A = np.full((r, d), 127, np.int8)
+    A[1] = -127
+    A[2, ::2] = -127
+    A[3, :] = 0
+    A[3, 5] = 1
+    x = np.full(d, 65504.0, np.float16)
+    B = np.eye(F, r, dtype=np.int8)
+    out = orc.predict(x, A, B)
+    X = _X(x)
+    h = [sum(int(a) * xv for a, xv in zip(row, X)) for row in A.tolist()]
+    assert [int(v) for v in out["h"]] == h
+    assert h[0] == 127 * 8192 * 65504 * (1 << 24) and h[2] == 0
+    # hq = Q(h): M = h[0]; h[1] = -M -> -127; h[3] = X_5 -> 127 X_5 / M rounds to 0
+    assert [int(q) for q in out["hq"]] == [127, -127, 0, 0]
 
 
 def test_predictor_special_cases():
     d, r, F = 128, 16, 64
     _, A, B = _rand_pred(d, r, F, 9)
     z = orc.predict(np.zeros(d, np.float16), A, B)
-    assert not z["xq"].any() and not z["s"].any()
+    assert not z["h"].any() and not z["hq"].any() and not z["s"].any()
+    # x = c e_j  =>  h = c 2^24 A[:, j] exactly, hq = Q(A[:, j]) (scale-free)
     x = np.zeros(d, np.float16)
     x[7] = -3.0
     e = orc.predict(x, A, B)
-    assert e["xq"][7] == -127 and np.count_nonzero(e["xq"]) == 1
-    assert np.array_equal(e["h"], -127 * A[:, 7].astype(np.int64))
-    # half-up tie: 127 * 0.5 = 63.5 -> 64 ; -63.5 -> -64
+    assert np.array_equal(e["h"], -3 * (1 << 24) * A[:, 7].astype(np.int64))
+    col = [-int(v) for v in A[:, 7]]
+    M = max(abs(v) for v in col)
+    assert [int(q) for q in e["hq"]] == [_exact_q127(v, M) for v in col]
+    # subnormal x: 2^-24 is X = 1
     x = np.zeros(d, np.float16)
-    x[0], x[1], x[2] = 1.0, 0.5, -0.5
-    assert list(orc.predict(x, A, B)["xq"][:3]) == [127, 64, -64]
+    x[3] = np.float16(2.0 ** -24)
+    assert np.array_equal(orc.predict(x, A, B)["h"], A[:, 3].astype(np.int64))
+    # half-up tie in O3: h = (2, 1, -1) * c  ->  hq = (127, 64, -64)
+    A2 = np.zeros((3, d), np.int8)
+    A2[0, 0], A2[1, 0], A2[2, 0] = 2, 1, -1
+    x = np.zeros(d, np.float16)
+    x[0] = 0.5
+    assert list(orc.predict(x, A2, B[:, :3])["hq"]) == [127, 64, -64]
     bad = np.zeros(d, np.float16)
     bad[3] = np.inf
     with pytest.raises(ValueError):

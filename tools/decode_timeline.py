@@ -28,45 +28,47 @@ for t in range(T):
     s = ctx.profile_stamps().astype(np.int64)  # [L, G, 10]
     rows.append(s)
 ctx.profile(False)
-names = ["P1 h", "B1", "P2 s+hist", "B2", "P3 select", "P4 ffn", "B4", "P5 reduce", "B5"]
+names = ["P2 hq+s+hist", "Bs", "P3 cuts", "P3 lists", "P4 ffn", "By", "R red+h", "Bx"]
 acc = {k: [] for k in names}
 accm = {k: [] for k in names}
 tot = []
+pro = []
 for s in rows:
-    tot.append((s[-1, :, 9].max() - s[0, :, 0].min()) / 1e3)
+    tot.append((s[-1, :, 9].max() - s[0, :, 12].min()) / 1e3)
+    pro.append((s[0, :, 13].max() - s[0, :, 12].min()) / 1e3)
     for l in range(L):
         a = s[l]
         nxt0 = s[l + 1, :, 0] if l + 1 < L else a[:, 9]
-        # phase = (last CTA done) - (first CTA released); barrier = (last release) - (last arrival)
+        # phase = (last CTA done) - (first CTA started); barrier = (last release) - (last arrival)
+        def ph(i, j):
+            return (a[:, j].max() - a[:, i].min(), (a[:, j] - a[:, i]).mean())
+        def br(i, nxt):
+            return (nxt.max() - a[:, i].max(), (nxt - a[:, i].max()).mean())
         spans = {
-            "P1 h": (a[:, 1].max() - a[:, 0].min(), (a[:, 1] - a[:, 0]).mean()),
-            "B1": (a[:, 2].max() - a[:, 1].max(), (a[:, 2] - a[:, 1].max()).mean()),
-            "P2 s+hist": (a[:, 3].max() - a[:, 2].min(), (a[:, 3] - a[:, 2]).mean()),
-            "B2": (a[:, 4].max() - a[:, 3].max(), (a[:, 4] - a[:, 3].max()).mean()),
-            "P3 select": (a[:, 5].max() - a[:, 4].min(), (a[:, 5] - a[:, 4]).mean()),
-            "P4 ffn": (a[:, 6].max() - a[:, 5].min(), (a[:, 6] - a[:, 5]).mean()),
-            "B4": (a[:, 7].max() - a[:, 6].max(), (a[:, 7] - a[:, 6].max()).mean()),
-            "P5 reduce": (a[:, 8].max() - a[:, 7].min(), (a[:, 8] - a[:, 7]).mean()),
-            "B5": (nxt0.max() - a[:, 8].max(), (nxt0 - a[:, 8].max()).mean()),
+            "P2 hq+s+hist": ph(0, 1),
+            "Bs": br(1, a[:, 4]),
+            "P3 cuts": ph(4, 10),
+            "P3 lists": ph(10, 5),
+            "P4 ffn": ph(5, 6),
+            "By": br(6, a[:, 7]),
+            "R red+h": ph(7, 8),
+            "Bx": br(8, nxt0),
         }
         for k, (mx, mn) in spans.items():
             acc[k].append(mx / 1e3)
             accm[k].append(mn / 1e3)
-print(f"{name}: {L} layers, token {np.mean(tot):.1f} us ({np.mean(tot) / L:.2f} us/layer)")
-print(f"{'phase':12s} {'crit us':>8s} {'mean-CTA us':>12s}")
+print(f"{name}: {L} layers, token {np.mean(tot):.1f} us ({np.mean(tot) / L:.2f} us/layer), prologue {np.mean(pro):.2f} us")
+print(f"{'phase':14s} {'crit us':>8s} {'mean-CTA us':>12s}")
 for k in names:
-    print(f"{k:12s} {np.mean(acc[k]):8.2f} {np.mean(accm[k]):12.2f}")
+    print(f"{k:14s} {np.mean(acc[k]):8.2f} {np.mean(accm[k]):12.2f}")
 s = rows[-1][L // 2]
 print("P4 per-CTA us (mid layer): min %.2f median %.2f max %.2f argmax %d" % (
     ((s[:, 6] - s[:, 5]) / 1e3).min(), np.median((s[:, 6] - s[:, 5]) / 1e3),
     ((s[:, 6] - s[:, 5]) / 1e3).max(), int(np.argmax(s[:, 6] - s[:, 5]))))
-print("P3 per-CTA us (mid layer): min %.2f median %.2f max %.2f" % (
-    ((s[:, 5] - s[:, 4]) / 1e3).min(), np.median((s[:, 5] - s[:, 4]) / 1e3), ((s[:, 5] - s[:, 4]) / 1e3).max()))
 G = rows[-1].shape[1]
 p4 = np.mean([(s[:, :, 6] - s[:, :, 5]) / 1e3 for s in rows], axis=(0, 1))  # per CTA
 print("P4 mean per CTA by sixths of the grid:", " ".join(f"{p4[i * G // 6:(i + 1) * G // 6].mean():.2f}" for i in range(6)))
-sub = {"P3a cuts": (4, 10), "P3a classify": (10, 11), "B3": (11, 12), "P3b gather": (12, 13),
-       "P3b tail": (13, 5), "P4 setup": (5, 14), "P4 gate/up": (14, 15), "P4 down": (15, 6)}
+sub = {"P3 load": (4, 2), "P3 cutbins": (2, 3), "P3 cand": (3, 16), "P3 rank": (16, 10), "P3 walk": (10, 18), "P3 exscan": (18, 19), "P3 write": (19, 11), "P3 tail": (11, 5), "P4 setup": (5, 14), "P4 gate/up": (14, 15), "P4 down": (15, 6)}
 for k, (i, j) in sub.items():
     v = np.mean([((s[:, :, j] - s[:, :, i]) / 1e3).mean() for s in rows])
     print(f"{k:12s} mean-CTA {v:.2f} us")
