@@ -216,17 +216,19 @@ __device__ __forceinline__ void prefetch_layers(const DecArgs &p, int lb, int la
 // h_{la} += A_{la}[:, 32 ch .. 32 ch + 32) X for the chunk whose fixed-point x values
 // (X_j = xm_j << xsh_j, fp16_fixed) are in shared memory; one red.add.u64 per row.
 // At: the chunk's 32 rows of A^T (global memory, or a shared-memory copy)
+// Two threads (adjacent lanes) per row, 16 columns each, combined by one shuffle.
 __device__ __forceinline__ void h_chunk(const int8_t *At, int r, const int *xm, const int *xsh,
                                         long long *hbuf) {
-    for (int i = threadIdx.x; i < r; i += blockDim.x) {
-        int av[32];
+    for (int i2 = threadIdx.x; i2 < 2 * r; i2 += blockDim.x) {  // 2 r is a multiple of 32
+        const int i = i2 >> 1, j0 = 16 * (i2 & 1);
+        int av[16];
 #pragma unroll
-        for (int j = 0; j < 32; j++) av[j] = At[(int64_t)j * r + i];
+        for (int j = 0; j < 16; j++) av[j] = At[(int64_t)(j0 + j) * r + i];
         unsigned long long acc = 0;
 #pragma unroll
-        for (int j = 0; j < 32; j++) acc += (unsigned long long)(long long)(av[j] * xm[j]) << xsh[j];
-        // (fully unrolled: av stays in registers)
-        if (acc) red_add_u64(hbuf + (int64_t)i * kHStride, (long long)acc);
+        for (int j = 0; j < 16; j++) acc += (unsigned long long)(long long)(av[j] * xm[j0 + j]) << xsh[j0 + j];
+        acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+        if ((i2 & 1) == 0 && acc) red_add_u64(hbuf + (int64_t)i * kHStride, (long long)acc);
     }
 }
 
@@ -366,17 +368,18 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
             }
             amax = block_max_u(amax, red_u);  // (its __syncthreads publishes keys[])
             if (tid == 0) p.sabs[cta] = amax;
-            // sorted run (key descending): rank by counting, one thread per neuron
+            // sorted run (key descending): rank by counting, four threads per key (a quarter of
+            // the comparisons each, combined by shuffles within the aligned group of four)
             const int nown = n1 - n0;
             int *run = p.runs + (int64_t)cta * RP;
-            for (int i = tid; i < RP; i += NT) {
-                int ki = (int)0x80000000, rk = i;  // padding: below every key
-                if (i < nown) {
-                    ki = keys[i];
-                    rk = 0;
-                    for (int j = 0; j < nown; j++) rk += keys[j] > ki;
-                }
-                run[rk] = ki;
+            for (int i4 = tid; i4 < ((4 * RP + 31) & ~31); i4 += NT) {  // whole warps (shuffles)
+                const int i = i4 >> 2, part4 = i4 & 3;
+                const int ki = i < nown ? keys[i] : (int)0x80000000;
+                int rk = 0;
+                for (int j = part4; j < nown; j += 4) rk += keys[j] > ki;
+                rk += __shfl_xor_sync(0xffffffffu, rk, 1);
+                rk += __shfl_xor_sync(0xffffffffu, rk, 2);
+                if (part4 == 0 && i < RP) run[i < nown ? rk : i] = ki;  // padding keeps its slot
             }
         }
         STAMP(1);
@@ -685,13 +688,18 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
             __syncthreads();
             STAMP(18);
             if (warp == 0) {  // exclusive scan of the per-run tier counts over runs
-                const int SP = (G + 31) / 32, ca = min(G, lane * SP), cz = min(G, ca + SP);
+                constexpr int kSP = 5;  // runs per lane (G <= 160); loads issued together
+                const int ca = lane * kSP;
+                int4 qv[kSP];
+#pragma unroll
+                for (int u = 0; u < kSP; u++)
+                    qv[u] = ca + u < G ? *reinterpret_cast<const int4 *>(pcum + 4 * (ca + u)) : make_int4(0, 0, 0, 0);
                 int s0 = 0, s1 = 0, s2 = 0;
-                for (int c = ca; c < cz; c++) {
-                    const int4 q = *reinterpret_cast<const int4 *>(pcum + 4 * c);
-                    s0 += q.x;
-                    s1 += q.y - q.x;
-                    s2 += q.z - q.y;
+#pragma unroll
+                for (int u = 0; u < kSP; u++) {
+                    s0 += qv[u].x;
+                    s1 += qv[u].y - qv[u].x;
+                    s2 += qv[u].z - qv[u].y;
                 }
                 int i0 = s0, i1 = s1, i2 = s2;
 #pragma unroll
@@ -705,12 +713,12 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
                     }
                 }
                 int e0 = i0 - s0, e1 = i1 - s1, e2 = i2 - s2;
-                for (int c = ca; c < cz; c++) {
-                    const int4 q = *reinterpret_cast<const int4 *>(pcum + 4 * c);
-                    *reinterpret_cast<int4 *>(pex + 4 * c) = make_int4(e0, e1, e2, 0);
-                    e0 += q.x;
-                    e1 += q.y - q.x;
-                    e2 += q.z - q.y;
+#pragma unroll
+                for (int u = 0; u < kSP; u++) {
+                    if (ca + u < G) *reinterpret_cast<int4 *>(pex + 4 * (ca + u)) = make_int4(e0, e1, e2, 0);
+                    e0 += qv[u].x;
+                    e1 += qv[u].y - qv[u].x;
+                    e2 += qv[u].z - qv[u].y;
                 }
                 if (lane == 31 && (i0 != p.k16 || i1 != p.k8 || i2 != p.k4)) atomicOr(p.err, 8u);
             }
