@@ -27,9 +27,11 @@
 //   --- barrier Bx (not after the last layer)
 //
 // Layer 0's h comes from a prologue (the R step without the reduction) and one barrier.
-// While layer l runs, warp 1 streams into L2 (during barrier waits): layer l+1's predictor
-// slice of this CTA, layer l+2's A^T chunk, and this CTA's share of the records the previous
-// token selected for layer l+1 (~80% recur), so the FFN's TMA reads mostly hit L2.
+// At barrier By, warp 1 stages this CTA's A^T chunk of layer l+1 into shared memory (TMA) for
+// R.  An optional L2 lookahead (M2C_DECODE_PREFETCH) streams layer l+1's predictor slice and
+// the records the previous token selected for layer l+1 (~80% recur); it is off by
+// default: the FFN's own reads already run at HBM speed (~1.8 us for 13.75 MB at S7) and the
+// prefetch traffic slows the latency-bound phases more than it saves (tools/exp_prefetch.sh).
 // Results are bit-identical to the per-phase kernel chain (same select rule, same per-CTA FFN
 // shares and batches, same reduction order): tests/test_gpu_parity.py checks it.
 #include <cstdlib>
@@ -934,7 +936,7 @@ cudaError_t launch_decode(m2c_ctx *c, __half *x, unsigned long long *prof, cudaS
     // M2C_DECODE_PREFETCH (see prefetch_layers; a tuning / measurement knob, results are identical)
     {
         const char *ev = getenv("M2C_DECODE_PREFETCH");
-        a.prefetch = ev ? atoi(ev) : 1;
+        a.prefetch = ev ? atoi(ev) : 0;  // off: L2 prefetch traffic slows the latency-bound phases (tools/exp_prefetch.sh)
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(c->G);
