@@ -84,7 +84,7 @@ struct DecArgs {
     unsigned long long *prof;   // [n_layers][G][kStamps] globaltimer stamps, or null
     int prefetch;
     int *bin_sh;                // [n_layers] histogram scale per layer (adapted token to token)
-    unsigned *sabs;             // [G] per-CTA max |s| of the current layer
+    unsigned *sabs;             // [2G] per-CTA |s| of its run's two ends (current layer)
 };
 
 // histogram bin of a raw score: monotone, clamped; 2^sh-wide bins centred on 0
@@ -144,14 +144,6 @@ __device__ __forceinline__ unsigned long long block_max_u64(unsigned long long v
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
     return v;
-}
-__device__ __forceinline__ int block_max_u(unsigned v, unsigned *sm32) {
-    v = __reduce_max_sync(0xffffffffu, v);
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    __syncthreads();
-    if (lane == 0) sm32[warp] = v;
-    __syncthreads();
-    return (int)__reduce_max_sync(0xffffffffu, lane < nw ? sm32[lane] : 0u);
 }
 __device__ __forceinline__ int block_sum(int v, int *sm32) {
     v = __reduce_add_sync(0xffffffffu, v);
@@ -239,7 +231,6 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ FfnShared sm;
     __shared__ FfnArgs fa;
-    __shared__ unsigned red_u[32];
     __shared__ unsigned long long red_u64[32];
     __shared__ int red_i[32];
     __shared__ int cut_bin[3], cut_need[3], cut_V[3], cut_I[3], ncand[3], ccnt[3];
@@ -345,7 +336,6 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
             }
             __syncthreads();
             const int4 *hq4 = reinterpret_cast<const int4 *>(hq) + part * CPL;
-            unsigned amax = 0;
             while (nb0 < n1) {
                 int acc = 0;
 #pragma unroll
@@ -362,14 +352,12 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
                 if (part == 0 && n < n1) {
                     // run key: (s, local index asc) in one int -- |s| < 2^23 (R2), local < 255
                     keys[n - n0] = (int)(((unsigned)acc << 8) | (unsigned)(255 - (n - n0)));
-                    amax = max(amax, (unsigned)abs(acc));
                     atomicAdd(&hist[bin_of(acc, shl)], 1);
                 }
                 nb0 += step;
                 if (nb0 < n1) load_b();
             }
-            amax = block_max_u(amax, red_u);  // (its __syncthreads publishes keys[])
-            if (tid == 0) p.sabs[cta] = amax;
+            __syncthreads();  // keys[] complete
             // sorted run (key descending): rank by counting, four threads per key (a quarter of
             // the comparisons each, combined by shuffles within the aligned group of four)
             const int nown = n1 - n0;
@@ -382,6 +370,9 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
                 rk += __shfl_xor_sync(0xffffffffu, rk, 1);
                 rk += __shfl_xor_sync(0xffffffffu, rk, 2);
                 if (part4 == 0 && i < RP) run[i < nown ? rk : i] = ki;  // padding keeps its slot
+                // max |s| of this CTA (next token's histogram scale): the run's two ends
+                if (part4 == 0 && i < nown && (rk == 0 || rk == nown - 1))
+                    p.sabs[2 * cta + (rk != 0)] = (unsigned)abs(ki >> 8);
             }
         }
         STAMP(1);
@@ -413,7 +404,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
         // next token's histogram scale for this layer: |s| < 2048 << sh (no clamped bins)
         if (cta == 0 && warp == 0) {
             unsigned m = 0;
-            for (int c = lane; c < G; c += 32) m = max(m, __ldcg(p.sabs + c));
+            for (int c = lane; c < 2 * G; c += 32) m = max(m, __ldcg(p.sabs + c));
             m = __reduce_max_sync(0xffffffffu, m);
             int sh = 0;
             while ((m >> sh) >= 2048u) sh++;
