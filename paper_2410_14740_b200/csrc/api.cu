@@ -68,7 +68,7 @@ static NcclApi *load_nccl(const char *path) {
 // ---- per-layer memory layout (hbm_region / host_region) ----
 struct Layout {
     size_t A = 0, B = 0, pool[3] = {0, 0, 0}, occ[3] = {0, 0, 0}, last[3] = {0, 0, 0},
-           slot_of[3] = {0, 0, 0}, hbm = 0;
+           slot_of[3] = {0, 0, 0}, ord[3] = {0, 0, 0}, hbm = 0;
     size_t host_rec[3] = {0, 0, 0}, host = 0;
 };
 static size_t a256(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -95,6 +95,8 @@ static Layout layout_of(const m2c_model_desc &d, const m2c_cache_cfg &cfg) {
             off += a256(4 * (size_t)cfg.cap_slots[t]);
             L.slot_of[t] = off;
             off += a256(4 * (size_t)F_r);
+            L.ord[t] = off;
+            off += a256(4 * (size_t)cfg.cap_slots[t]);
         }
         size_t h = 0;
         for (int t = 0; t < 3; t++) {
@@ -486,6 +488,8 @@ m2c_status m2c_load_layer(m2c_ctx *c, int32_t layer, const void *g, const void *
             L.occupant[t] = (int32_t *)(hb + Lo.occ[t]);
             L.last[t] = (int32_t *)(hb + Lo.last[t]);
             L.slot_of[t] = (int32_t *)(hb + Lo.slot_of[t]);
+            L.ord[t] = (int32_t *)(hb + Lo.ord[t]);
+            M2C_CUDA(launch_iota(L.ord[t], L.cap[t], st));  // all last_use = -1: slot order
             M2C_CUDA(launch_fill_i32(L.occupant[t], -1, L.cap[t], st));
             M2C_CUDA(launch_fill_i32(L.last[t], -1, L.cap[t], st));
             M2C_CUDA(launch_fill_i32(L.slot_of[t], -1, F_r, st));

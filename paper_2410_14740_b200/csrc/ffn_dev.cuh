@@ -30,6 +30,9 @@ namespace m2c {
 namespace {
 
 constexpr int kNBMax = 16;   // records per batch
+#ifndef M2C_FFN_FB_MUL
+#define M2C_FFN_FB_MUL 4     // fast-path batch = M2C_FFN_FB_MUL x (warps / quarter-units per record); 1 measured slower (tools/exp_fb.sh)
+#endif
 constexpr int kNSlot = 32;   // mbarriers (>= records in flight)
 constexpr int kRing = 192 * 1024;
 constexpr int kMaxLocal = 1024;  // records one CTA may own
@@ -314,9 +317,12 @@ __device__ __forceinline__ void ffn_loop(const FfnArgs &a, int d, int act, const
                 mbar_expect_tx(bar, (uint32_t)sz);
                 bulk_g2s(ring + off, src(j), (uint32_t)sz, bar, pol);
             }
-            const int nbt = (n_items + kNBMax - 1) / kNBMax;
+            // batches of one record per warp (P quarter-units each): the down-projection of a
+            // batch overlaps the arrival of the next batch's records
+            const int FB = max(1, min(kNBMax, (nwarp / (nchunk >= 512 ? 4 : 1)) * M2C_FFN_FB_MUL));
+            const int nbt = (n_items + FB - 1) / FB;
             if (j == 0) sm.nbatch = nbt;
-            if (j <= nbt) bst[j] = min(j * kNBMax, n_items);
+            if (j <= nbt) bst[j] = min(j * FB, n_items);
         }
     } else if (threadIdx.x == 0) {
         // thread 0: batches (consecutive records that fit the ring together, with wrap slack)

@@ -21,6 +21,7 @@ struct LruArgs {
     int32_t *occ[3];
     int32_t *last[3];
     int32_t *slot_of[3];
+    int32_t *ord[3];  // slots sorted by (last_use, slot): the LRU order, maintained in place
     int cap[3];
     int seg[3];
     int cnt[3];
@@ -53,6 +54,11 @@ __device__ __forceinline__ int block_scan1(int v, int *tot, int *sm) {
     return r;
 }
 
+// One CTA per tier pool.  The victims are the nm smallest (last_use, slot) among slots with
+// last_use < t (R7).  Instead of sorting every step, the pool keeps its slots in that order
+// (ord): after this step's hits are refreshed, the victims are the first nm non-hit entries of
+// ord, and the new order is [the other non-hit entries, in order] ++ [hits and victims -- all
+// now stamped t -- by slot].  O(C) with four block scans.
 __global__ void __launch_bounds__(NT, 1)
     k_lru(LruArgs a, const int32_t *__restrict__ step_ptr, const int32_t *__restrict__ tier_ids, int32_t *__restrict__ slots,
           uint32_t *__restrict__ hit_bits, int32_t *__restrict__ hit_items,
@@ -60,15 +66,21 @@ __global__ void __launch_bounds__(NT, 1)
           int32_t *__restrict__ miss_log, int32_t *__restrict__ evict_log,
           int32_t *__restrict__ counts, unsigned long long *__restrict__ stats, int P2) {
     extern __shared__ __align__(16) uint8_t smraw[];
-    unsigned long long *ck = reinterpret_cast<unsigned long long *>(smraw);  // [P2]
-    int32_t *mpos = reinterpret_cast<int32_t *>(smraw + 8 * (size_t)P2);     // [cnt]
+    // smem: new order [C] | victims [C] | miss positions [cnt] | slot bitmaps hit, tail [C/32]
+    int32_t *nord = reinterpret_cast<int32_t *>(smraw);
+    int32_t *vict = nord + P2;
+    int32_t *mpos = vict + P2;
+    uint32_t *hmask = reinterpret_cast<uint32_t *>(mpos + P2);
+    uint32_t *tmask = hmask + P2 / 32;
     __shared__ int scan_sm[NW];
-    griddep_wait();
-    const int t = *step_ptr;
     const int tau = blockIdx.x;
     const int n = a.cnt[tau], seg = a.seg[tau], C = a.cap[tau];
-    int32_t *occ = a.occ[tau], *last = a.last[tau], *slot_of = a.slot_of[tau];
+    for (int i = threadIdx.x; i < P2 / 32; i += NT) hmask[i] = tmask[i] = 0u;
+    griddep_wait();
+    const int t = *step_ptr;
+    int32_t *occ = a.occ[tau], *last = a.last[tau], *slot_of = a.slot_of[tau], *ord = a.ord[tau];
     const int32_t *R = tier_ids + seg;
+    __syncthreads();
 
     // 1. hits: refresh their timestamp (a hit never moves slot)
     const int CH = (n + NT - 1) / NT;
@@ -80,54 +92,63 @@ __global__ void __launch_bounds__(NT, 1)
             last[sl] = t;
             slots[seg + i] = sl;
             atomicOr(&hit_bits[(seg + i) >> 5], 1u << ((seg + i) & 31));
+            atomicOr(&hmask[sl >> 5], 1u << (sl & 31));
             nh++;
         }
     }
     int tot_h;
-    int hpos = block_scan1(nh, &tot_h, scan_sm);  // also a barrier: last[] writes visible
-    int mp = (i0 - (hpos)) ;  // misses before this chunk = i0 - hits before it
+    int hpos = block_scan1(nh, &tot_h, scan_sm);  // (a barrier: hmask complete)
+    int mp = i0 - hpos;  // misses before this chunk = i0 - hits before it
     for (int i = i0; i < i1; i++) {
         const int sl = slot_of[R[i]];
         if (sl >= 0) hit_items[seg + hpos++] = sl;
         else mpos[mp++] = i;
     }
     const int nm = n - tot_h;
-    // 3. victims: the nm smallest (last_use, slot) among slots with last_use < t
-    for (int sl = threadIdx.x; sl < P2; sl += NT) {
-        unsigned long long key = ~0ull;
-        if (sl < C) {
-            const int lu = last[sl];
-            if (lu < t) key = ((unsigned long long)(uint32_t)(lu + 1) << 32) | (uint32_t)sl;
+    // 2. victims: the first nm non-hit entries of the LRU order
+    const int OC = (C + NT - 1) / NT;
+    const int o0 = min(C, (int)threadIdx.x * OC), o1 = min(C, o0 + OC);
+    int nk = 0;
+    for (int q = o0; q < o1; q++) {
+        const int sl = ord[q];
+        nk += !((hmask[sl >> 5] >> (sl & 31)) & 1u);
+    }
+    int tot_k;
+    int kpos = block_scan1(nk, &tot_k, scan_sm);  // non-hit rank of this thread's first entry
+    for (int q = o0; q < o1; q++) {
+        const int sl = ord[q];
+        if ((hmask[sl >> 5] >> (sl & 31)) & 1u) continue;
+        if (kpos < nm) {
+            vict[kpos] = sl;
+            atomicOr(&tmask[sl >> 5], 1u << (sl & 31));
+        } else {
+            nord[kpos - nm] = sl;  // kept, order preserved
         }
-        ck[sl] = key;
+        kpos++;
     }
     __syncthreads();
-    for (int size = 2; size <= P2; size <<= 1) {
-        for (int stride = size >> 1; stride > 0; stride >>= 1) {
-            for (int i = threadIdx.x; i < P2 / 2; i += NT) {
-                const int lo = 2 * i - (i & (stride - 1));
-                const int hi = lo + stride;
-                const bool asc = ((lo & size) == 0);
-                const unsigned long long x = ck[lo], y = ck[hi];
-                if ((x > y) == asc) {
-                    ck[lo] = y;
-                    ck[hi] = x;
-                }
-            }
-            __syncthreads();
-        }
-    }
+    // 3. the tail: hits and victims by slot
+    const int front = tot_k - nm;
+    int nt = 0;
+    for (int sl = o0; sl < o1; sl++)
+        nt += ((hmask[sl >> 5] | tmask[sl >> 5]) >> (sl & 31)) & 1u;
+    int tot_t;
+    int tpos = block_scan1(nt, &tot_t, scan_sm) + front;
+    for (int sl = o0; sl < o1; sl++)
+        if (((hmask[sl >> 5] | tmask[sl >> 5]) >> (sl & 31)) & 1u) nord[tpos++] = sl;
+    __syncthreads();
+    for (int q = threadIdx.x; q < C; q += NT) ord[q] = nord[q];
     // 4. install misses[m] in victim[m]; evictions compacted in miss order
     const int MC = (nm + NT - 1) / NT;
     const int m0 = min(nm, (int)threadIdx.x * MC), m1 = min(nm, m0 + MC);
     int ne = 0;
-    for (int m = m0; m < m1; m++) ne += occ[(uint32_t)ck[m]] >= 0;
+    for (int m = m0; m < m1; m++) ne += occ[vict[m]] >= 0;
     int tot_e;
     int epos = block_scan1(ne, &tot_e, scan_sm);
     for (int m = m0; m < m1; m++) {
         const int i = mpos[m];
         const int id = R[i];
-        const int sl = (int)(uint32_t)ck[m];
+        const int sl = vict[m];
         const int old = occ[sl];
         if (old >= 0) {
             slot_of[old] = -1;
@@ -201,7 +222,7 @@ __global__ void __launch_bounds__(256) k_fill(FillArgs a, const int32_t *__restr
 
 }  // namespace
 
-size_t lru_smem_bytes(int P2, int maxcnt) { return 8 * (size_t)P2 + 4 * (size_t)maxcnt; }
+size_t lru_smem_bytes(int P2, int maxcnt) { (void)maxcnt; return 12 * (size_t)P2 + 8 * (size_t)(P2 / 32); }
 
 cudaError_t init_cache_attrs() {
     return cudaFuncSetAttribute(k_lru, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -214,15 +235,16 @@ cudaError_t launch_lru(m2c_ctx *c, LayerState &L, const int32_t *step_dev, const
     LruArgs a;
     const int cnt[3] = {p.k_fp16, p.k_int8, p.k_int4};
     const int seg[3] = {0, p.k_fp16, p.k_fp16 + p.k_int8};
-    int P2 = 2, maxcnt = 1;
+    int P2 = 32, maxcnt = 1;
     for (int t = 0; t < 3; t++) {
         a.occ[t] = L.occupant[t];
         a.last[t] = L.last[t];
         a.slot_of[t] = L.slot_of[t];
+        a.ord[t] = L.ord[t];
         a.cap[t] = L.cap[t];
         a.seg[t] = seg[t];
         a.cnt[t] = cnt[t];
-        while (P2 < L.cap[t]) P2 <<= 1;
+        while (P2 < L.cap[t] || P2 < cnt[t]) P2 <<= 1;
         maxcnt = cnt[t] > maxcnt ? cnt[t] : maxcnt;
     }
     cudaError_t e = cudaMemsetAsync(hit_bits, 0, sizeof(uint32_t) * ((p.k + 31) / 32 + 1), st);

@@ -47,6 +47,7 @@ struct LayerState {
     int32_t *occupant[3] = {nullptr, nullptr, nullptr};
     int32_t *last[3] = {nullptr, nullptr, nullptr};
     int32_t *slot_of[3] = {nullptr, nullptr, nullptr};
+    int32_t *ord[3] = {nullptr, nullptr, nullptr};  // LRU order: slots by (last_use, slot)
     const uint8_t *host_rec[3] = {nullptr, nullptr, nullptr};
     int64_t last_step = INT64_MIN;
 };
