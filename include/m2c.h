@@ -219,6 +219,34 @@ m2c_status m2c_profile_stamps(m2c_ctx *ctx, uint64_t *out, int64_t cap, int64_t 
 
 /* Kernels launched by the last m2c_decode_step (per token), and cumulative cache counters
  * (hits, misses per tier) since the last reset (device counters; synchronises). */
+/* ---- NEXT-1: SSD -> DRAM tier (§5.4) -----------------
+ * The paper keeps the whole model on SSD and stages it into DRAM layer-wise with a two-level
+ * DRAM cache: a FIXED area holding the first n layers and a DYNAMIC area managed FIFO, filled
+ * by I/O threads at least two layers ahead.  Here:
+ *   m2c_store_write(ctx, path): after every layer was loaded in LRU/ATU mode, writes the host
+ *     tier (each layer's three packed tiers, verbatim) to a layer-major file, each layer padded
+ *     to m2c_store_frame_bytes.  Synchronous.
+ *   m2c_store_attach(ctx, path, n_fixed, n_dynamic, lookahead, frames, frames_bytes): from now
+ *     on the miss fills read the file-backed DRAM frames instead of the in-memory host tier
+ *     (the caller may free that after attaching).  frames: caller-owned pinned host memory of
+ *     >= (n_fixed + n_dynamic) x m2c_store_frame_bytes bytes, 4 KiB aligned for O_DIRECT reads.
+ *     Layers [0, n_fixed) are read once into the fixed area; one I/O thread keeps layers up to
+ *     `lookahead` ahead of the decode loop in the dynamic frames (FIFO), and synchronises on
+ *     the GPU's last read of a frame before reusing it.  m2c_decode_step then runs eagerly
+ *     (no CUDA graph) and the host blocks in it while a needed layer is still being read.
+ *     Outputs are identical to the in-memory host tier (same bytes).
+ *   m2c_store_stats: bytes read, layer loads, seconds in reads (I/O thread) and seconds the
+ *     decode loop waited for a layer.  m2c_store_detach: stops the I/O thread.
+ * Errors: M2C_ERR_STATE (layers not loaded in LRU/ATU mode, short file, read failure),
+ * M2C_ERR_CAPACITY (frames too small), M2C_ERR_CONFIG (bad counts). */
+size_t m2c_store_frame_bytes(const m2c_model_desc *desc, const m2c_cache_cfg *cfg);
+m2c_status m2c_store_write(m2c_ctx *ctx, const char *path);
+m2c_status m2c_store_attach(m2c_ctx *ctx, const char *path, int32_t n_fixed, int32_t n_dynamic,
+                            int32_t lookahead, void *frames, size_t frames_bytes);
+m2c_status m2c_store_detach(m2c_ctx *ctx);
+m2c_status m2c_store_stats(m2c_ctx *ctx, int64_t *bytes_read, int64_t *layer_loads, double *io_seconds,
+                           double *stall_seconds);
+
 m2c_status m2c_stats(m2c_ctx *ctx, int64_t *kernels_per_token, int64_t hits[3], int64_t misses[3],
                      int32_t reset);
 

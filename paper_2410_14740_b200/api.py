@@ -143,6 +143,38 @@ class M2CContext:
         self._host_off += (nbytes + 255) // 256 * 256
         return t
 
+    # ---- NEXT-1: SSD -> DRAM store (include/m2c.h) ----
+    def store_write(self, path: str):
+        """Write every layer's host tier to a layer-major file (the paper's SSD copy)."""
+        self._call(lib().m2c_store_write, self._h, path.encode())
+
+    def store_attach(self, path: str, n_fixed: int, n_dynamic: int, lookahead: int = 2,
+                     drop_host_tier: bool = True):
+        """Serve the miss fills from DRAM frames of the file: layers [0, n_fixed) fixed, a FIFO
+        of n_dynamic frames filled `lookahead` layers ahead by an I/O thread."""
+        cfg = next(c for (_, _, c) in self.regions.values())
+        fb = lib().m2c_store_frame_bytes(C.byref(self.desc), C.byref(cfg))
+        nbytes = (n_fixed + n_dynamic) * fb
+        self._frames = torch.empty(nbytes + 4096, dtype=torch.uint8, pin_memory=True)
+        off = (-self._frames.data_ptr()) % 4096
+        self._call(lib().m2c_store_attach, self._h, path.encode(), n_fixed, n_dynamic, lookahead,
+                   C.c_void_p(self._frames.data_ptr() + off), nbytes)
+        self._host_dropped = drop_host_tier
+        if drop_host_tier:  # the fills no longer read it
+            self._host_pool = None
+            self.regions = {l: (hb, None, c) for l, (hb, _, c) in self.regions.items()}
+
+    def store_stats(self):
+        b, n = C.c_int64(), C.c_int64()
+        io, st = C.c_double(), C.c_double()
+        check(lib().m2c_store_stats(self._h, C.byref(b), C.byref(n), C.byref(io), C.byref(st)))
+        return {"bytes_read": b.value, "layer_loads": n.value, "io_s": io.value, "stall_s": st.value}
+
+    def store_detach(self):
+        if getattr(self, "_host_dropped", False):
+            raise M2CError(6, "store_detach: the in-memory host tier was dropped at attach")
+        self._call(lib().m2c_store_detach, self._h)
+
     # ---- a0 + load ----
     def load_layer(self, layer, w_gate, w_up, w_down_t, pred_A, pred_B, cfg: CacheCfg = None):
         cfg = cfg or cache_cfg_resident()

@@ -8,7 +8,7 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SOURCES = ["api.cu", "k_pack.cu", "k_pred.cu", "k_select.cu", "k_cache.cu", "k_ffn.cu",
-           "k_reduce.cu", "k_decode.cu"]
+           "k_reduce.cu", "k_decode.cu", "store.cu"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared"]
 
@@ -21,7 +21,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return out
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
     extra = os.environ.get("M2C_NVCC_EXTRA", "").split()  # measurement builds (tools/) only
-    cmd = [nvcc, *NVCC_FLAGS, *extra, "-o", out + ".tmp", *srcs, "-ldl"]
+    cmd = [nvcc, *NVCC_FLAGS, *extra, "-o", out + ".tmp", *srcs, "-ldl", "-lpthread"]
     if verbose:
         print(" ".join(cmd))
     subprocess.check_call(cmd)

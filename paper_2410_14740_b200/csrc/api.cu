@@ -144,6 +144,20 @@ static cudaError_t mark(m2c_ctx *c, int l, int i) {
     return cudaEventRecordWithFlags(c->prof_ev[5 * l + i], c->compute, cudaEventRecordExternal);
 }
 
+// the miss fill of layer l: from the in-memory host tier, or (NEXT-1) from the layer's DRAM
+// frame of the SSD store -- the host blocks until the preloader has it resident
+static cudaError_t enqueue_fill(m2c_ctx *c, int l, const m2c_tier_plan &p) {
+    const LayerState &L = c->layers[l];
+    if (!c->store) return launch_fill(c, L, p, c->copy);
+    uint8_t *frame = store_acquire(c, l);
+    if (!frame) return cudaErrorUnknown;  // I/O error (m2c_last_error is set by the caller)
+    LayerState F = L;
+    for (int t = 0; t < 3; t++) F.host_rec[t] = frame + L.host_off[t];
+    cudaError_t e = launch_fill(c, F, p, c->copy);
+    store_release(c, l, c->copy);
+    return e;
+}
+
 static cudaError_t enqueue_layer(m2c_ctx *c, int l, __half *x) {
     LayerState &L = c->layers[l];
     const m2c_tier_plan &p = c->plan;
@@ -169,7 +183,7 @@ static cudaError_t enqueue_layer(m2c_ctx *c, int l, __half *x) {
         if (e) return e;
         if ((e = cudaEventRecord(c->ev_lookup, st))) return e;
         if ((e = cudaStreamWaitEvent(c->copy, c->ev_lookup, 0))) return e;
-        if ((e = launch_fill(c, L, p, c->copy))) return e;
+        if ((e = enqueue_fill(c, l, p))) return e;
         if ((e = cudaEventRecord(c->ev_fill, c->copy))) return e;
         e = launch_ffn(c, L, x, c->ws.hit_items, c->ws.counts + 4, p, c->ws.partial, st);
         if (e) return e;
@@ -410,6 +424,10 @@ m2c_status m2c_create(const m2c_model_desc *desc, int32_t device, m2c_stream_t c
 
 m2c_status m2c_destroy(m2c_ctx *c) {
     if (!c) return M2C_OK;
+    if (c->store) {
+        cudaStreamSynchronize(c->copy);
+        store_close(c);
+    }
     if (c->graph) cudaGraphExecDestroy(c->graph);
     for (cudaEvent_t e : c->prof_ev) cudaEventDestroy(e);
     if (c->comm && c->nccl) c->nccl->commDestroy(c->comm);
@@ -485,6 +503,9 @@ m2c_status m2c_load_layer(m2c_ctx *c, int32_t layer, const void *g, const void *
                                          cudaMemcpyDefault, st));
             }
             L.host_rec[t] = dst;
+            L.host_base = hh;
+            L.host_off[t] = Lo.host_rec[t];
+            L.host_bytes = Lo.host;
             L.occupant[t] = (int32_t *)(hb + Lo.occ[t]);
             L.last[t] = (int32_t *)(hb + Lo.last[t]);
             L.slot_of[t] = (int32_t *)(hb + Lo.slot_of[t]);
@@ -566,7 +587,7 @@ m2c_status m2c_cache_lookup_fill(m2c_ctx *c, int32_t layer, int64_t step, const 
         }
         M2C_CUDA(cudaEventRecord(c->ev_lookup, cs));
         M2C_CUDA(cudaStreamWaitEvent(c->copy, c->ev_lookup, 0));
-        M2C_CUDA(launch_fill(c, L, *plan, c->copy));
+        M2C_CUDA(enqueue_fill(c, layer, *plan));
         if (fill_done) M2C_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(fill_done), c->copy));
     }
     L.last_step = step;
@@ -692,7 +713,7 @@ m2c_status m2c_decode_step(m2c_ctx *c, void *x_inout, int64_t step) {
         M2C_CUDA(decode_write_layer_table(c, c->dec_layers));
         c->dec_table_dirty = false;
     }
-    if (c->use_graph) {
+    if (c->use_graph && !c->store) {  // (a store's frames change per token: eager)
         if (c->graph && c->graph_x != x_inout) {
             cudaGraphExecDestroy(c->graph);
             c->graph = nullptr;
@@ -801,6 +822,52 @@ m2c_status m2c_profile_stamps(m2c_ctx *c, uint64_t *out, int64_t cap, int64_t *n
     M2C_CUDA(cudaStreamSynchronize(c->compute));
     M2C_CUDA(cudaMemcpy(out, c->dec_prof, 8 * (size_t)n, cudaMemcpyDeviceToHost));
     return M2C_OK;
+}
+
+m2c_status m2c_store_write(m2c_ctx *c, const char *path) {
+    if (!c || !path) return fail(M2C_ERR_INVALID_ARG, "store_write: null argument");
+    M2C_CUDA(cudaDeviceSynchronize());
+    return store_write(c, path, c->layers.empty() ? 0 : c->layers[0].host_bytes);
+}
+
+m2c_status m2c_store_attach(m2c_ctx *c, const char *path, int32_t n_fixed, int32_t n_dynamic,
+                            int32_t lookahead, void *frames, size_t frames_bytes) {
+    if (!c || !path || !frames) return fail(M2C_ERR_INVALID_ARG, "store_attach: null argument");
+    if (c->store) return fail(M2C_ERR_STATE, "store_attach: a store is attached");
+    const int L = c->desc.n_layers;
+    if (n_fixed < 0 || n_dynamic < 0 || n_fixed > L || (n_fixed < L && n_dynamic < 1) || lookahead < 0)
+        return fail(M2C_ERR_CONFIG, "store_attach: need 0 <= n_fixed <= L, n_dynamic >= 1 unless all layers are fixed");
+    for (const LayerState &ls : c->layers)
+        if (!ls.loaded || ls.mode == 0) return fail(M2C_ERR_STATE, "store_attach: all layers must be loaded in LRU/ATU mode");
+    M2C_CUDA(cudaDeviceSynchronize());
+    if (c->graph) {
+        cudaGraphExecDestroy(c->graph);
+        c->graph = nullptr;
+    }
+    return store_open(c, path, n_fixed, n_dynamic, lookahead, frames, frames_bytes, c->layers[0].host_bytes);
+}
+
+m2c_status m2c_store_detach(m2c_ctx *c) {
+    if (!c) return fail(M2C_ERR_INVALID_ARG, "null ctx");
+    if (!c->store) return M2C_OK;
+    M2C_CUDA(cudaDeviceSynchronize());
+    store_close(c);
+    return M2C_OK;
+}
+
+m2c_status m2c_store_stats(m2c_ctx *c, int64_t *bytes_read, int64_t *layer_loads, double *io_seconds,
+                           double *stall_seconds) {
+    if (!c || !bytes_read || !layer_loads || !io_seconds || !stall_seconds)
+        return fail(M2C_ERR_INVALID_ARG, "store_stats: null argument");
+    if (!c->store) return fail(M2C_ERR_STATE, "store_stats: no store attached");
+    store_stats(c, bytes_read, layer_loads, io_seconds, stall_seconds);
+    return M2C_OK;
+}
+
+size_t m2c_store_frame_bytes(const m2c_model_desc *desc, const m2c_cache_cfg *cfg) {
+    if (!desc || !cfg || cfg->mode == 0) return 0;
+    const size_t h = layout_of(*desc, *cfg).host;
+    return (h + 4095) / 4096 * 4096;
 }
 
 m2c_status m2c_stats(m2c_ctx *c, int64_t *kpt, int64_t hits[3], int64_t misses[3], int32_t reset) {

@@ -49,6 +49,9 @@ struct LayerState {
     int32_t *slot_of[3] = {nullptr, nullptr, nullptr};
     int32_t *ord[3] = {nullptr, nullptr, nullptr};  // LRU order: slots by (last_use, slot)
     const uint8_t *host_rec[3] = {nullptr, nullptr, nullptr};
+    const uint8_t *host_base = nullptr;  // the layer's host-tier region (the store's unit)
+    size_t host_off[3] = {0, 0, 0};      // tier offsets inside it
+    size_t host_bytes = 0;
     int64_t last_step = INT64_MIN;
 };
 
@@ -119,6 +122,8 @@ struct m2c_ctx {
     bool dec_table_dirty = true;
     bool last_token_fused = false;
     bool decoded = false;            // at least one m2c_decode_step enqueued
+    // NEXT-1: SSD -> DRAM store (store.cu); null = the in-memory pinned host tier
+    void *store = nullptr;
     // multi-GPU
     m2c::NcclApi *nccl = nullptr;
     void *comm = nullptr;
@@ -151,6 +156,14 @@ cudaError_t launch_lru(m2c_ctx *c, LayerState &L, const int32_t *step_dev, const
                        const m2c_tier_plan &p, int32_t *slots, uint32_t *hit_bits,
                        int32_t *miss_log, int32_t *evict_log, cudaStream_t st);
 cudaError_t launch_fill(m2c_ctx *c, const LayerState &L, const m2c_tier_plan &p, cudaStream_t st);
+// store.cu (NEXT-1)
+m2c_status store_open(m2c_ctx *c, const char *path, int n_fixed, int n_dyn, int ahead, void *frames,
+                      size_t frames_bytes, size_t layer_bytes);
+void store_close(m2c_ctx *c);
+uint8_t *store_acquire(m2c_ctx *c, int l);
+void store_release(m2c_ctx *c, int l, cudaStream_t st);
+void store_stats(m2c_ctx *c, int64_t *bytes, int64_t *loads, double *io_s, double *stall_s);
+m2c_status store_write(m2c_ctx *c, const char *path, size_t layer_bytes);
 cudaError_t launch_ffn(m2c_ctx *c, const LayerState &L, const __half *x, const int32_t *items,
                        const int32_t *counts, const m2c_tier_plan &p, float *partial,
                        cudaStream_t st);

@@ -445,3 +445,42 @@ def test_decode_fused_degenerate_ties(m2c, kind):
     for ctx in ctxs:
         ctx.stats()  # raises if the device flagged an error (barrier timeout, count mismatch)
         ctx.close()
+
+
+@pytest.mark.parametrize("n_fixed,n_dyn,ahead", [(1, 2, 1), (0, 1, 0), (2, 3, 2), (4, 0, 0)])
+def test_store_backed_host_tier_matches_in_memory(m2c, tmp_path, n_fixed, n_dyn, ahead):
+    """NEXT-1: miss fills served from the file-backed two-level DRAM cache (fixed area + FIFO
+    frames filled by the I/O thread) give bit-identical tokens, lists and cache statistics."""
+    cfg = get_config("T")
+    L = 4
+    plan = m2c.plan_of(cfg)
+    ws = [layer_weights(cfg, l, device="cuda") for l in range(L)]
+    ctxs = []
+    for _ in range(2):
+        ctx = _ctx(m2c, cfg, plan, n_layers=L)
+        cc = m2c.cache_cfg_capped(ctx.desc, plan, 1, 4, "lru")
+        ctx.reserve_host_tier(L * ctx.layer_footprint(cc)[1])
+        for l, w in enumerate(ws):
+            ctx.load_layer(l, w["w_gate"], w["w_up"], w["w_down_t"], w["pred_A"], w["pred_B"], cc)
+        ctxs.append(ctx)
+    a, b = ctxs
+    path = str(tmp_path / "m2c_store.bin")
+    b.store_write(path)
+    b.store_attach(path, n_fixed, n_dyn, ahead)
+    xs = token_stream(cfg, 10, device="cuda")
+    for t in range(10):
+        xa, xb = xs[t].contiguous().clone(), xs[t].contiguous().clone()
+        a.decode_step(xa, t + 1)
+        b.decode_step(xb, t + 1)
+        torch.cuda.synchronize()
+        assert torch.equal(xa, xb), t
+    sa, sb = a.stats(), b.stats()
+    assert sa["hits"] == sb["hits"] and sa["misses"] == sb["misses"]
+    st = b.store_stats()
+    assert st["layer_loads"] >= min(n_fixed, L) and st["bytes_read"] > 0
+    if n_fixed + n_dyn < L:  # the dynamic area streamed the other layers every token
+        assert st["layer_loads"] >= n_fixed + (L - n_fixed) * 10 - n_dyn
+    else:  # everything fits the DRAM cache: each layer read once
+        assert st["layer_loads"] == L
+    for c in ctxs:
+        c.close()
