@@ -30,6 +30,10 @@ namespace m2c {
 namespace {
 
 constexpr int kNBMax = 16;   // records per batch
+#ifndef M2C_FFN_WS
+#define M2C_FFN_WS 0         // warp-specialised fast path (gate/up warps | down warps): measured
+                             // slower at S7 (gate/up on half the warps is the longer chain)
+#endif
 #ifndef M2C_FFN_FB_MUL
 #define M2C_FFN_FB_MUL 4     // fast-path batch = M2C_FFN_FB_MUL x (warps / quarter-units per record); 1 measured slower (tools/exp_fb.sh)
 #endif
@@ -93,13 +97,34 @@ __device__ __forceinline__ uint32_t zz2_16(uint32_t z) {  // fp16x2 (1024 + 16 z
 }
 
 // ---- warp-local partial dot products of one record over chunks [c0, c1) (8 elements each)
+// (one 8-element chunk c into the accumulators ag, au)
+template <int TIER>
+__device__ __forceinline__ void gu_one(const uint8_t *rec, const uint4 *xs, int d, int c, float &ag, float &au);
+
 template <int TIER>
 __device__ __forceinline__ void gu_chunks(const uint8_t *rec, const uint4 *xs, int d, int c0, int c1,
                                           float &pg, float &pu) {
     const int lane = threadIdx.x & 31;
-    const int G = d >> 7;
+    if (c1 - c0 == 128) {  // the common quarter of d = 4096: 4 chunks per lane, independent chains
+        float g0 = 0.f, u0 = 0.f, g1 = 0.f, u1 = 0.f, g2 = 0.f, u2 = 0.f, g3 = 0.f, u3 = 0.f;
+        gu_one<TIER>(rec, xs, d, c0 + lane, g0, u0);
+        gu_one<TIER>(rec, xs, d, c0 + lane + 32, g1, u1);
+        gu_one<TIER>(rec, xs, d, c0 + lane + 64, g2, u2);
+        gu_one<TIER>(rec, xs, d, c0 + lane + 96, g3, u3);
+        pg = (g0 + g1) + (g2 + g3);
+        pu = (u0 + u1) + (u2 + u3);
+        return;
+    }
     float ag = 0.f, au = 0.f;
-    for (int c = c0 + lane; c < c1; c += 32) {
+    for (int c = c0 + lane; c < c1; c += 32) gu_one<TIER>(rec, xs, d, c, ag, au);
+    pg = ag;
+    pu = au;
+}
+
+template <int TIER>
+__device__ __forceinline__ void gu_one(const uint8_t *rec, const uint4 *xs, int d, int c, float &ag, float &au) {
+    const int G = d >> 7;
+    {
         const uint4 xv = xs[c];
         const uint32_t xw[4] = {xv.x, xv.y, xv.z, xv.w};
         if (TIER == 0) {
@@ -166,8 +191,6 @@ __device__ __forceinline__ void gu_chunks(const uint8_t *rec, const uint4 *xs, i
             au = fmaf(su, tu, au);
         }
     }
-    pg = ag;
-    pu = au;
 }
 
 __device__ __forceinline__ void gu_any(int tier, const uint8_t *rec, const uint4 *xs, int d, int c0,
@@ -259,15 +282,71 @@ __device__ __forceinline__ void cta_ranges(const FfnArgs &a, int n0, int n1, int
 
 struct FfnShared {
     uint64_t bars[kNSlot];
+    uint64_t abar[kNSlot];   // warp-specialised path: record j's activation a_j is ready
+    int acnt[kNSlot];        // quarter-units of record j done
+    float apart[kNSlot][4][2];
     int span[kNSlot];
     float part[kNBMax][4][2];
-    float a_sm[kNBMax];
+    float a_sm[kNSlot];
     int cb[5][5];        // chunk bounds: cb[P][p] = nchunk * p / P
     int rng[8];          // CTA ranges (6)
     int nbatch;
     int scan[96];
     int selv[16];
 };
+
+__device__ __forceinline__ void ffn_init_bars(FfnShared &sm) {  // thread 0, before any use
+    for (int i = 0; i < kNSlot; i++) {
+        mbar_init(&sm.bars[i], 1);
+        mbar_init(&sm.abar[i], 1);
+    }
+    fence_mbar_init();
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// y[0..8) += a * deq(down column)[8 c8 .. 8 c8 + 8) (down_t for an explicit chunk of 8)
+template <int TIER>
+__device__ __forceinline__ void down_c(const uint8_t *rec, int d, float a, int c8, float *y) {
+    if (TIER == 0) {
+        const uint4 v = *reinterpret_cast<const uint4 *>(rec + 4 * d + 16 * c8);
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            y[2 * i] = fmaf(a, h2f_lo(w[i]), y[2 * i]);
+            y[2 * i + 1] = fmaf(a, h2f_hi(w[i]), y[2 * i + 1]);
+        }
+    } else {
+        const int G = d >> 7, grp = c8 >> 4;
+        const uint8_t *scales = rec + (TIER == 1 ? 3 * d : 3 * (d >> 1));
+        const uint32_t z = (scales + 6 * G)[2 * G + grp];
+        const float as = a * half_bits_f(*reinterpret_cast<const uint16_t *>(scales + 2 * (2 * G + grp)));
+        uint32_t p[4];
+        if (TIER == 1) {
+            const uint2 v = *reinterpret_cast<const uint2 *>(rec + 2 * d + 8 * c8);
+            deq8(v.x, v.y, zz2(z), p);
+#pragma unroll
+            for (int i = 0; i < 4; i++) {
+                y[2 * i] = fmaf(as, h2f_lo(p[i]), y[2 * i]);
+                y[2 * i + 1] = fmaf(as, h2f_hi(p[i]), y[2 * i + 1]);
+            }
+        } else {
+            const uint32_t w = *reinterpret_cast<const uint32_t *>(rec + d + 4 * c8);
+            deq4(w, zz2(z), zz2_16(z), p);
+            const float as16 = as * 0.0625f;
+            y[0] = fmaf(as, h2f_lo(p[0]), y[0]);
+            y[4] = fmaf(as, h2f_hi(p[0]), y[4]);
+            y[1] = fmaf(as16, h2f_lo(p[1]), y[1]);
+            y[5] = fmaf(as16, h2f_hi(p[1]), y[5]);
+            y[2] = fmaf(as, h2f_lo(p[2]), y[2]);
+            y[6] = fmaf(as, h2f_hi(p[2]), y[6]);
+            y[3] = fmaf(as16, h2f_lo(p[3]), y[3]);
+            y[7] = fmaf(as16, h2f_hi(p[3]), y[7]);
+        }
+    }
+}
 
 // table: chunk bounds per split into P parts (constant for a launch)
 __device__ __forceinline__ void ffn_tables(FfnShared &sm, int d) {
@@ -375,6 +454,75 @@ __device__ __forceinline__ void ffn_loop(const FfnArgs &a, int d, int act, const
     __syncthreads();
     if (stamps && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(stamps[0]));
 
+    if (fast && nwarp >= 2 && (nwarp & 1) == 0 && M2C_FFN_WS) {
+        // Warp-specialised (all records in flight): warps [0, NG) compute gate/up units in
+        // record order as the copies land; the unit that completes record j combines its
+        // quarters in a fixed order and arrives on abar[j]; warps [NG, nwarp) own 2 x 8 y
+        // elements per thread and accumulate the down-projection record by record as each
+        // a_j becomes ready -- the down-projection overlaps the arrival of later records.
+        // Per element the operations and their order are those of the batched path.
+        const int P = nchunk >= 512 ? 4 : 1;
+        const int NG = nwarp / 2;
+        if (threadIdx.x < kNSlot) sm.acnt[threadIdx.x] = 0;
+        __syncthreads();
+        if (warp < NG) {
+            for (int u = warp; u < n_items * P; u += NG) {
+                const int j = u / P, pp = u - j * P;
+                mbar_wait(&sm.bars[(jb + j) % kNSlot], (uint32_t)(((jb + j) / kNSlot) & 1));
+                const int ds = dsc[j];
+                float pg, pu;
+                gu_any(ds >> 24, ring + (ds & 0xffffff), xs, d, sm.cb[P][pp], sm.cb[P][pp + 1], pg, pu);
+                pg = warp_sum_f(pg);
+                pu = warp_sum_f(pu);
+                if (lane == 0) {
+                    sm.apart[j][pp][0] = pg;
+                    sm.apart[j][pp][1] = pu;
+                    __threadfence_block();
+                    if (atomicAdd(&sm.acnt[j], 1) == P - 1) {  // last quarter: combine, publish
+                        __threadfence_block();
+                        float g = 0.f, uu = 0.f;
+                        for (int q = 0; q < P; q++) {
+                            g += sm.apart[j][q][0];
+                            uu += sm.apart[j][q][1];
+                        }
+                        sm.a_sm[j] = (act == 1) ? fmaxf(g, 0.f) * uu : g / (1.f + expf(-g)) * uu;
+                        mbar_arrive(&sm.abar[(jb + j) % kNSlot]);
+                    }
+                }
+            }
+            if (stamps && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(stamps[1]));
+        } else {
+            const int t2 = threadIdx.x - NG * 32;  // 0 .. (nwarp - NG) * 32
+            const int c8a = 2 * t2, c8b = 2 * t2 + 1;
+            float ya[8], yb[8];
+#pragma unroll
+            for (int i = 0; i < 8; i++) ya[i] = yb[i] = 0.f;
+            for (int j = 0; j < n_items; j++) {
+                mbar_wait(&sm.abar[(jb + j) % kNSlot], (uint32_t)(((jb + j) / kNSlot) & 1));
+                const int ds = dsc[j];
+                const uint8_t *rec = ring + (ds & 0xffffff);
+                const float aj = sm.a_sm[j];
+                const int tier = ds >> 24;
+                if (tier == 0) {
+                    down_c<0>(rec, d, aj, c8a, ya);
+                    down_c<0>(rec, d, aj, c8b, yb);
+                } else if (tier == 1) {
+                    down_c<1>(rec, d, aj, c8a, ya);
+                    down_c<1>(rec, d, aj, c8b, yb);
+                } else {
+                    down_c<2>(rec, d, aj, c8a, ya);
+                    down_c<2>(rec, d, aj, c8b, yb);
+                }
+            }
+            float *out = partial + (int64_t)blockIdx.x * d + 16 * t2;
+            reinterpret_cast<float4 *>(out)[0] = make_float4(ya[0], ya[1], ya[2], ya[3]);
+            reinterpret_cast<float4 *>(out)[1] = make_float4(ya[4], ya[5], ya[6], ya[7]);
+            reinterpret_cast<float4 *>(out)[2] = make_float4(yb[0], yb[1], yb[2], yb[3]);
+            reinterpret_cast<float4 *>(out)[3] = make_float4(yb[4], yb[5], yb[6], yb[7]);
+        }
+        __syncthreads();  // the ring's records are consumed
+        return;
+    }
     float y[8];
 #pragma unroll
     for (int i = 0; i < 8; i++) y[i] = 0.f;

@@ -41,6 +41,9 @@
 namespace m2c {
 namespace {
 
+#ifndef M2C_BAR_MODE
+#define M2C_BAR_MODE 1
+#endif
 constexpr int kBins = 4096;
 constexpr int kHistW = kBins;  // fine bins (the 64 coarse sums follow them in smem only)
 // profiling stamps per (layer, CTA): 0 layer start, 1 P2 done, 4 after Bs, 2 runs in smem,
@@ -118,12 +121,19 @@ __device__ __forceinline__ void grid_sync(unsigned *counter, unsigned target, ui
         asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(counter) : "memory");
         const unsigned want = target * gridDim.x;
         const unsigned long long t0 = gtimer();
+#if M2C_BAR_MODE == 2  // relaxed polling, one acquire fence after
+        while ((int)(ld_relaxed(counter) - want) < 0) {
+#else
         while ((int)(ld_acquire(counter) - want) < 0) {
+#endif
             if (gtimer() - t0 > 2000000000ull) {
                 atomicOr(err, 4u);
                 break;
             }
         }
+#if M2C_BAR_MODE == 2
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+#endif
     } else if (threadIdx.x >= 32 && threadIdx.x < 64) {
         work();  // warp 1: e.g. L2 prefetch while thread 0 waits
     }
@@ -244,7 +254,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
     auto tg = [&](int t) { return t == 0 ? p.k16 : (t == 1 ? p.k16 + p.k8 : kk); };  // cut targets
     const int nchunk = d / 32;
     if (tid == 0) {
-        for (int i = 0; i < kNSlot; i++) mbar_init(&sm.bars[i], 1);
+        ffn_init_bars(sm);
         mbar_init(&sel_bar, 1);
         mbar_init(&at_bar, 1);
         fence_mbar_init();

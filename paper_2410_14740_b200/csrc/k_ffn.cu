@@ -13,10 +13,7 @@ __global__ void __launch_bounds__(1024, 1)
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ FfnShared sm;
     const SmemPtrs S = carve(smem);
-    if (threadIdx.x == 0) {
-        for (int i = 0; i < kNSlot; i++) mbar_init(&sm.bars[i], 1);
-        fence_mbar_init();
-    }
+    if (threadIdx.x == 0) ffn_init_bars(sm);
     griddep_launch();
     griddep_wait();
     if (threadIdx.x == 0) {
