@@ -175,6 +175,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--eager", action="store_true", help="no CUDA graph")
     ap.add_argument("--unfused", action="store_true", help="per-phase kernel chain instead of k_decode")
+    ap.add_argument("--lookahead", action="store_true",
+                    help="NEXT-2: stage layer l+1's predicted misses during layer l (LRU/ATU configs)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -220,6 +222,8 @@ def main():
         ctx.set_graph(False)
     if args.unfused:
         ctx.set_fused(False)
+    if args.lookahead and cfg.cache_mode != "resident":
+        ctx.set_lookahead(True)
 
     W, K = args.warmup, args.steps
     if cfg.cache_mode != "resident":
@@ -233,6 +237,8 @@ def main():
         ctx.decode_step(x, step)
         step += 1
     ctx.stats(reset=True)
+    if args.lookahead and cfg.cache_mode != "resident":
+        ctx.lookahead_stats(reset=True)
 
     def barrier():
         if world > 1:
@@ -255,6 +261,7 @@ def main():
     ms = e0.elapsed_time(e1)
     ms = m2c_dist.max_over_ranks(ms, device=dev)
     st = ctx.stats()
+    staged = ctx.lookahead_stats() if args.lookahead and cfg.cache_mode != "resident" else 0
     kpt = st["kernels_per_token"]
     tok_s = K / (ms / 1e3)
     ab = algorithmic_bytes(cfg, plan, P)
@@ -358,7 +365,8 @@ def main():
             "load_s": t_load,
         }
         if cfg.cache_mode != "resident":
-            line["cache"] = {"hits": hits, "misses": miss,
+            line["cache"] = {"hits": hits, "misses": miss, "lookahead": bool(args.lookahead),
+                             "staged_fills": staged,
                              "hit_ratio": [h / max(1, h + m) for h, m in zip(hits, miss)]}
         print(json.dumps(line), flush=True)
     ctx.close()

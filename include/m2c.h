@@ -219,6 +219,19 @@ m2c_status m2c_profile_stamps(m2c_ctx *ctx, uint64_t *out, int64_t cap, int64_t 
 
 /* Kernels launched by the last m2c_decode_step (per token), and cumulative cache counters
  * (hits, misses per tier) since the last reset (device counters; synchronises). */
+/* ---- NEXT-2: cross-layer lookahead ("the next one layer ... almost 100%") ---------
+ * m2c_set_lookahead(ctx, 1): in the LRU/ATU decode chain, after layer l's cache lookup the
+ * library also runs layer l+1's predictor and select on x_l (a prediction of layer l+1's
+ * selection), marks the predicted neurons that would miss in layer l+1's pools now, and copies
+ * their records from the host tier into device staging buffers on the copy stream, overlapped
+ * with the rest of layer l.  At layer l+1 a miss whose record was staged is filled device to
+ * device.  The selection, the cache state and every output are unchanged (the staging only
+ * moves the PCIe transfer earlier); mispredicted records cost extra PCIe traffic.  Not used
+ * with an SSD store attached.  Allocates the staging buffers (2 x sum_t k_t nb_t + O(F_r)).
+ * m2c_lookahead_stats: misses filled from staging so far (reset: zero it). */
+m2c_status m2c_set_lookahead(m2c_ctx *ctx, int32_t enable);
+m2c_status m2c_lookahead_stats(m2c_ctx *ctx, int64_t *staged_fills, int32_t reset);
+
 /* ---- NEXT-1: SSD -> DRAM tier (§5.4) -----------------
  * The paper keeps the whole model on SSD and stages it into DRAM layer-wise with a two-level
  * DRAM cache: a FIXED area holding the first n layers and a DYNAMIC area managed FIFO, filled

@@ -143,6 +143,15 @@ class M2CContext:
         self._host_off += (nbytes + 255) // 256 * 256
         return t
 
+    # ---- NEXT-2: cross-layer lookahead staging (include/m2c.h) ----
+    def set_lookahead(self, enable: bool):
+        self._call(lib().m2c_set_lookahead, self._h, 1 if enable else 0)
+
+    def lookahead_stats(self, reset=False):
+        v = C.c_int64()
+        check(lib().m2c_lookahead_stats(self._h, C.byref(v), 1 if reset else 0))
+        return v.value
+
     # ---- NEXT-1: SSD -> DRAM store (include/m2c.h) ----
     def store_write(self, path: str):
         """Write every layer's host tier to a layer-major file (the paper's SSD copy)."""

@@ -146,9 +146,9 @@ static cudaError_t mark(m2c_ctx *c, int l, int i) {
 
 // the miss fill of layer l: from the in-memory host tier, or (NEXT-1) from the layer's DRAM
 // frame of the SSD store -- the host blocks until the preloader has it resident
-static cudaError_t enqueue_fill(m2c_ctx *c, int l, const m2c_tier_plan &p) {
+static cudaError_t enqueue_fill(m2c_ctx *c, int l, const m2c_tier_plan &p, int stage_par = -1) {
     const LayerState &L = c->layers[l];
-    if (!c->store) return launch_fill(c, L, p, c->copy);
+    if (!c->store) return launch_fill(c, L, p, c->copy, stage_par);
     uint8_t *frame = store_acquire(c, l);
     if (!frame) return cudaErrorUnknown;  // I/O error (m2c_last_error is set by the caller)
     LayerState F = L;
@@ -170,6 +170,20 @@ static cudaError_t enqueue_layer(m2c_ctx *c, int l, __half *x) {
     const bool prefetch = L.mode == 0 && c->use_fused;
     int32_t *ids = L.mode == 0 ? lists : c->ws.tier_ids;
     if ((e = mark(c, l, 0))) return e;
+    if (L.mode != 0 && c->lookahead && !c->store && l + 1 < c->desc.n_layers) {
+        // NEXT-2: predict layer l+1's selection from x_l first, and stage its would-be
+        // misses on the staging stream (its own PCIe transfer, concurrent with this layer's)
+        const LayerState &Ln = c->layers[l + 1];
+        if ((e = launch_predict(c, Ln, x, c->ws.s, c->ghist, nullptr, st))) return e;
+        if ((e = launch_select(c, c->ws.s, c->ghist, p, nullptr, nullptr, c->spec_ids, st))) return e;
+        // the staging buffers of this parity were last read by layer l-1's fill (copy stream)
+        if (l > 0 && (e = cudaStreamWaitEvent(st, c->ev_fill, 0))) return e;
+        if ((e = launch_stage_plan(c, Ln, (l + 1) & 1, c->spec_ids, st))) return e;
+        if ((e = cudaEventRecord(c->ev_stage, st))) return e;
+        if ((e = cudaStreamWaitEvent(c->stage_stream, c->ev_stage, 0))) return e;
+        if ((e = launch_stage_fill(c, Ln, (l + 1) & 1, c->stage_stream))) return e;
+        if ((e = cudaEventRecord(c->ev_staged[(l + 1) & 1], c->stage_stream))) return e;
+    }
     if ((e = launch_predict(c, L, x, c->ws.s, c->ghist, prefetch ? lists : nullptr, st))) return e;
     if ((e = mark(c, l, 1))) return e;
     if ((e = launch_select(c, c->ws.s, c->ghist, p, nullptr, nullptr, ids, st))) return e;
@@ -183,7 +197,11 @@ static cudaError_t enqueue_layer(m2c_ctx *c, int l, __half *x) {
         if (e) return e;
         if ((e = cudaEventRecord(c->ev_lookup, st))) return e;
         if ((e = cudaStreamWaitEvent(c->copy, c->ev_lookup, 0))) return e;
-        if ((e = enqueue_fill(c, l, p))) return e;
+        // NEXT-2: layer l's records staged during layer l-1 (parity l & 1) fill device-side
+        const bool la = c->lookahead && !c->store;
+        if (la && l > 0 && (e = cudaStreamWaitEvent(c->copy, c->ev_staged[l & 1], 0))) return e;
+        if ((e = enqueue_fill(c, l, p, la && l > 0 ? (l & 1) : -1))) return e;
+        if (la && l > 0 && (e = launch_stage_clear(c, L, l & 1, c->copy))) return e;
         if ((e = cudaEventRecord(c->ev_fill, c->copy))) return e;
         e = launch_ffn(c, L, x, c->ws.hit_items, c->ws.counts + 4, p, c->ws.partial, st);
         if (e) return e;
@@ -342,7 +360,7 @@ m2c_status m2c_create(const m2c_model_desc *desc, int32_t device, m2c_stream_t c
                  o_hit = take(4 * (size_t)F_r), o_miss = take(4 * (size_t)F_r),
                  o_mid = take(4 * (size_t)F_r), o_cnt = take(4 * 16),
                  o_part = take(4 * (size_t)2 * c->G * d), o_y = take(4 * (size_t)d),
-                 o_x = take(2 * (size_t)d), o_stats = take(8 * 6), o_err = take(4),
+                 o_x = take(2 * (size_t)d), o_stats = take(8 * 8), o_err = take(4),
                  o_hist = take(4 * 2 * 4096), o_sst = take(8 * (size_t)select_blocks(F_r)),
                  o_sdone = take(4), o_sepoch = take(4), o_bflags = take(4 * (size_t)c->G),
                  o_bepoch = take(4), o_dlay = take(decode_layer_table_bytes(desc->n_layers)),
@@ -414,6 +432,7 @@ m2c_status m2c_create(const m2c_model_desc *desc, int32_t device, m2c_stream_t c
     }
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_lookup, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_fill, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_stage, cudaEventDisableTiming);
     if (e != cudaSuccess) {
         m2c_destroy(c);
         return cuda_fail(e, "m2c_create");
@@ -433,6 +452,13 @@ m2c_status m2c_destroy(m2c_ctx *c) {
     if (c->comm && c->nccl) c->nccl->commDestroy(c->comm);
     if (c->ev_lookup) cudaEventDestroy(c->ev_lookup);
     if (c->ev_fill) cudaEventDestroy(c->ev_fill);
+    if (c->ev_stage) cudaEventDestroy(c->ev_stage);
+    if (c->stage_mem) {
+        cudaStreamSynchronize(c->stage_stream);
+        cudaStreamDestroy(c->stage_stream);
+        for (int p = 0; p < 2; p++) cudaEventDestroy(c->ev_staged[p]);
+        cudaFree(c->stage_mem);
+    }
     if (c->ws_mem) cudaFree(c->ws_mem);
     delete c;
     return M2C_OK;
@@ -821,6 +847,59 @@ m2c_status m2c_profile_stamps(m2c_ctx *c, uint64_t *out, int64_t cap, int64_t *n
         return fail(M2C_ERR_STATE, "profile_stamps: profiling off or last token not on k_decode");
     M2C_CUDA(cudaStreamSynchronize(c->compute));
     M2C_CUDA(cudaMemcpy(out, c->dec_prof, 8 * (size_t)n, cudaMemcpyDeviceToHost));
+    return M2C_OK;
+}
+
+m2c_status m2c_set_lookahead(m2c_ctx *c, int32_t enable) {
+    if (!c) return fail(M2C_ERR_INVALID_ARG, "null ctx");
+    M2C_CUDA(cudaStreamSynchronize(c->compute));
+    M2C_CUDA(cudaStreamSynchronize(c->copy));
+    if (c->stage_stream) M2C_CUDA(cudaStreamSynchronize(c->stage_stream));
+    if (enable && !c->stage_mem) {
+        const int F = c->F_r, k = c->plan.k > 0 ? c->plan.k : 1;
+        const int kt[3] = {c->plan.k_fp16, c->plan.k_int8, c->plan.k_int4};
+        size_t off = 0;
+        auto take = [&](size_t b) {
+            const size_t o = off;
+            off += a256(b);
+            return o;
+        };
+        size_t o_of[2], o_buf[2][3], o_sid[2];
+        for (int p = 0; p < 2; p++) {
+            o_of[p] = take(4 * 3 * (size_t)F);
+            for (int t = 0; t < 3; t++) o_buf[p][t] = take((size_t)(kt[t] > 0 ? kt[t] : 1) * c->nb[t]);
+            o_sid[p] = take(4 * (size_t)k);
+        }
+        const size_t o_spec = take(4 * (size_t)k);
+        M2C_CUDA(cudaMalloc(&c->stage_mem, off));
+        uint8_t *b = static_cast<uint8_t *>(c->stage_mem);
+        for (int p = 0; p < 2; p++) {
+            c->stage_of[p] = (int32_t *)(b + o_of[p]);
+            for (int t = 0; t < 3; t++) c->stage_buf[p][t] = b + o_buf[p][t];
+            c->stage_sid[p] = (int32_t *)(b + o_sid[p]);
+            M2C_CUDA(cudaMemset(c->stage_of[p], 0xff, 4 * 3 * (size_t)F));  // -1: nothing staged
+        }
+        c->spec_ids = (int32_t *)(b + o_spec);
+        M2C_CUDA(cudaStreamCreateWithFlags(&c->stage_stream, cudaStreamNonBlocking));
+        for (int p = 0; p < 2; p++) M2C_CUDA(cudaEventCreateWithFlags(&c->ev_staged[p], cudaEventDisableTiming));
+    }
+    c->lookahead = enable != 0;
+    if (c->graph) {
+        cudaGraphExecDestroy(c->graph);
+        c->graph = nullptr;
+    }
+    return M2C_OK;
+}
+
+m2c_status m2c_lookahead_stats(m2c_ctx *c, int64_t *staged_fills, int32_t reset) {
+    if (!c || !staged_fills) return fail(M2C_ERR_INVALID_ARG, "null argument");
+    M2C_CUDA(cudaStreamSynchronize(c->compute));
+    M2C_CUDA(cudaStreamSynchronize(c->copy));
+    if (c->stage_stream) M2C_CUDA(cudaStreamSynchronize(c->stage_stream));
+    unsigned long long v = 0;
+    M2C_CUDA(cudaMemcpy(&v, c->ws.stats + 6, 8, cudaMemcpyDeviceToHost));
+    *staged_fills = (int64_t)v;
+    if (reset) M2C_CUDA(cudaMemset(c->ws.stats + 6, 0, 8));
     return M2C_OK;
 }
 

@@ -178,11 +178,25 @@ __global__ void __launch_bounds__(NT, 1)
     }
 }
 
+struct StageArgs {
+    const uint8_t *host[3];   // layer l+1's host tier
+    const int32_t *slot_of[3];  // layer l+1's pools (read before layer l+1's lookup)
+    int32_t *stage_of[3];     // [F_r] per tier (this parity)
+    uint8_t *stage[3];        // [k_t][nb_t] per tier (this parity)
+    int32_t *sid;             // [k] staged id per list entry (-1 none)
+    int64_t nb[3];
+    int seg[3], cnt[3];
+};
+
 struct FillArgs {
     const uint8_t *host[3];
     uint8_t *pool[3];
     int64_t nb[3];
     int seg[3];
+    // NEXT-2 lookahead: records staged one layer ahead (device), stage_of[t][id] = index or -1
+    const int32_t *stage_of[3];
+    const uint8_t *stage[3];
+    unsigned long long *staged;  // count of misses filled from the staging buffers
 };
 
 // a5: SM-driven gather of the missed records from the pinned host tier (UVA-mapped) into
@@ -202,7 +216,10 @@ __global__ void __launch_bounds__(256) k_fill(FillArgs a, const int32_t *__restr
         const int id = miss_ids[a.seg[tau] + m];
         const int sl = miss_items[a.seg[tau] + m];
         const int64_t nv = a.nb[tau] / 16;
-        const uint4 *src = reinterpret_cast<const uint4 *>(a.host[tau] + (int64_t)id * a.nb[tau]);
+        const int si = a.stage_of[tau] ? a.stage_of[tau][id] : -1;  // staged by the lookahead?
+        if (si >= 0 && lane == 0) atomicAdd(a.staged, 1ull);
+        const uint4 *src = reinterpret_cast<const uint4 *>(
+            si >= 0 ? a.stage[tau] + (int64_t)si * a.nb[tau] : a.host[tau] + (int64_t)id * a.nb[tau]);
         uint4 *dst = reinterpret_cast<uint4 *>(a.pool[tau] + (int64_t)sl * a.nb[tau]);
         for (int64_t base = 0; base < nv; base += 32 * 8) {
             uint4 v[8];
@@ -218,6 +235,64 @@ __global__ void __launch_bounds__(256) k_fill(FillArgs a, const int32_t *__restr
             }
         }
     }
+}
+
+// NEXT-2 (the next layer's neurons are predictable from the current layer's input):
+// the predicted tier lists of layer l+1 (from x_l) -> the entries that would miss in layer
+// l+1's pools now are marked in stage_of (index = position in the tier segment) and copied
+// from the host tier into the staging buffers on the copy stream, overlapped with layer l.
+// The selection, the cache state and the outputs are unchanged: a miss at layer l+1 whose
+// record was staged is filled device-to-device instead of over PCIe.
+__global__ void __launch_bounds__(256) k_stage_plan(StageArgs a, const int32_t *__restrict__ spec_ids) {
+    griddep_wait();
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int k = a.seg[2] + a.cnt[2];
+    if (i >= k) return;
+    const int tau = i < a.seg[1] ? 0 : (i < a.seg[2] ? 1 : 2);
+    const int id = spec_ids[i];
+    const bool stage = a.slot_of[tau][id] < 0;
+    a.sid[i] = stage ? id : -1;
+    if (stage) a.stage_of[tau][id] = i - a.seg[tau];
+}
+
+// the staged records: host tier of layer l+1 -> staging buffers (warp per record)
+__global__ void __launch_bounds__(256) k_stage_fill(StageArgs a) {
+    griddep_wait();
+    const int k = a.seg[2] + a.cnt[2];
+    const int lane = threadIdx.x & 31;
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
+    for (int i = gw; i < k; i += nwarps) {
+        const int id = a.sid[i];
+        if (id < 0) continue;
+        const int tau = i < a.seg[1] ? 0 : (i < a.seg[2] ? 1 : 2);
+        const int64_t nv = a.nb[tau] / 16;
+        const uint4 *src = reinterpret_cast<const uint4 *>(a.host[tau] + (int64_t)id * a.nb[tau]);
+        uint4 *dst = reinterpret_cast<uint4 *>(a.stage[tau] + (int64_t)(i - a.seg[tau]) * a.nb[tau]);
+        for (int64_t base = 0; base < nv; base += 32 * 8) {
+            uint4 v[8];
+#pragma unroll
+            for (int j = 0; j < 8; j++) {
+                const int64_t c = base + lane + 32 * j;
+                if (c < nv) v[j] = src[c];
+            }
+#pragma unroll
+            for (int j = 0; j < 8; j++) {
+                const int64_t c = base + lane + 32 * j;
+                if (c < nv) dst[c] = v[j];
+            }
+        }
+    }
+}
+
+// after layer l+1's fill consumed them: the staging marks are cleared for reuse
+__global__ void __launch_bounds__(256) k_stage_clear(StageArgs a) {
+    griddep_wait();
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int k = a.seg[2] + a.cnt[2];
+    if (i >= k) return;
+    const int tau = i < a.seg[1] ? 0 : (i < a.seg[2] ? 1 : 2);
+    const int id = a.sid[i];
+    if (id >= 0) a.stage_of[tau][id] = -1;
 }
 
 }  // namespace
@@ -257,8 +332,46 @@ cudaError_t launch_lru(m2c_ctx *c, LayerState &L, const int32_t *step_dev, const
     return e;
 }
 
+static StageArgs stage_args(m2c_ctx *c, const LayerState &Ln, int par) {
+    StageArgs a;
+    const m2c_tier_plan &p = c->plan;
+    const int seg[3] = {0, p.k_fp16, p.k_fp16 + p.k_int8}, cnt[3] = {p.k_fp16, p.k_int8, p.k_int4};
+    for (int t = 0; t < 3; t++) {
+        a.host[t] = Ln.host_rec[t];
+        a.slot_of[t] = Ln.slot_of[t];
+        a.stage_of[t] = c->stage_of[par] + (size_t)t * c->F_r;
+        a.stage[t] = c->stage_buf[par][t];
+        a.nb[t] = c->nb[t];
+        a.seg[t] = seg[t];
+        a.cnt[t] = cnt[t];
+    }
+    a.sid = c->stage_sid[par];
+    return a;
+}
+
+cudaError_t launch_stage_plan(m2c_ctx *c, const LayerState &Ln, int par, const int32_t *spec_ids,
+                              cudaStream_t st) {
+    const int k = c->plan.k;
+    if (k <= 0) return cudaSuccess;
+    cudaError_t e = launch_k(k_stage_plan, dim3((k + 255) / 256), dim3(256), 0, st, stage_args(c, Ln, par), spec_ids);
+    c->launch_counter++;
+    return e;
+}
+cudaError_t launch_stage_fill(m2c_ctx *c, const LayerState &Ln, int par, cudaStream_t st) {
+    cudaError_t e = launch_k(k_stage_fill, dim3(64), dim3(256), 0, st, stage_args(c, Ln, par));
+    c->launch_counter++;
+    return e;
+}
+cudaError_t launch_stage_clear(m2c_ctx *c, const LayerState &Ln, int par, cudaStream_t st) {
+    const int k = c->plan.k;
+    if (k <= 0) return cudaSuccess;
+    cudaError_t e = launch_k(k_stage_clear, dim3((k + 255) / 256), dim3(256), 0, st, stage_args(c, Ln, par));
+    c->launch_counter++;
+    return e;
+}
+
 cudaError_t launch_fill(m2c_ctx *c, const LayerState &L, const m2c_tier_plan &p,
-                        cudaStream_t st) {
+                        cudaStream_t st, int stage_par) {
     FillArgs a;
     const int seg[3] = {0, p.k_fp16, p.k_fp16 + p.k_int8};
     for (int t = 0; t < 3; t++) {
@@ -266,7 +379,10 @@ cudaError_t launch_fill(m2c_ctx *c, const LayerState &L, const m2c_tier_plan &p,
         a.pool[t] = L.pool[t];
         a.nb[t] = c->nb[t];
         a.seg[t] = seg[t];
+        a.stage_of[t] = stage_par >= 0 ? c->stage_of[stage_par] + (size_t)t * c->F_r : nullptr;
+        a.stage[t] = stage_par >= 0 ? c->stage_buf[stage_par][t] : nullptr;
     }
+    a.staged = c->ws.stats + 6;
     cudaError_t e = launch_k(k_fill, dim3(64), dim3(256), 0, st, a, c->ws.counts, c->ws.miss_ids,
                              c->ws.miss_items);
     c->launch_counter++;

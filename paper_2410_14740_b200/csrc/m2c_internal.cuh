@@ -72,7 +72,7 @@ struct Workspace {
     float *partial = nullptr;      // [2][G][d]
     float *y32 = nullptr;          // [d]
     __half *xbuf = nullptr;        // [d]
-    unsigned long long *stats = nullptr;  // [6] hits[3], misses[3] cumulative
+    unsigned long long *stats = nullptr;  // [8] hits[3], misses[3], staged fills, - (cumulative)
     uint32_t *err = nullptr;       // device error flag
 };
 
@@ -91,7 +91,7 @@ struct m2c_ctx {
     size_t ws_bytes = 0;
     m2c::Workspace ws;
     int G = 148;              // FFN grid (persistent CTAs)
-    cudaEvent_t ev_lookup = nullptr, ev_fill = nullptr;
+    cudaEvent_t ev_lookup = nullptr, ev_fill = nullptr, ev_stage = nullptr;
     // decode graph
     bool use_graph = true;
     cudaGraphExec_t graph = nullptr;
@@ -124,6 +124,15 @@ struct m2c_ctx {
     bool decoded = false;            // at least one m2c_decode_step enqueued
     // NEXT-1: SSD -> DRAM store (store.cu); null = the in-memory pinned host tier
     void *store = nullptr;
+    // NEXT-2: cross-layer lookahead staging (LRU/ATU decode chain); buffers by layer parity
+    bool lookahead = false;
+    void *stage_mem = nullptr;
+    int32_t *stage_of[2] = {nullptr, nullptr};   // [3][F_r]
+    uint8_t *stage_buf[2][3] = {{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}};
+    int32_t *stage_sid[2] = {nullptr, nullptr};  // [k]
+    int32_t *spec_ids = nullptr;                 // [k] predicted tier lists of the next layer
+    cudaStream_t stage_stream = nullptr;          // staging copies (own stream: concurrent with fills)
+    cudaEvent_t ev_staged[2] = {nullptr, nullptr};  // layer parity: staging complete
     // multi-GPU
     m2c::NcclApi *nccl = nullptr;
     void *comm = nullptr;
@@ -155,7 +164,12 @@ int select_blocks(int F_r);
 cudaError_t launch_lru(m2c_ctx *c, LayerState &L, const int32_t *step_dev, const int32_t *tier_ids,
                        const m2c_tier_plan &p, int32_t *slots, uint32_t *hit_bits,
                        int32_t *miss_log, int32_t *evict_log, cudaStream_t st);
-cudaError_t launch_fill(m2c_ctx *c, const LayerState &L, const m2c_tier_plan &p, cudaStream_t st);
+cudaError_t launch_fill(m2c_ctx *c, const LayerState &L, const m2c_tier_plan &p, cudaStream_t st,
+                        int stage_par = -1);
+// NEXT-2 lookahead staging (k_cache.cu): Ln = layer l+1, par = (l+1) & 1
+cudaError_t launch_stage_plan(m2c_ctx *c, const LayerState &Ln, int par, const int32_t *spec_ids, cudaStream_t st);
+cudaError_t launch_stage_fill(m2c_ctx *c, const LayerState &Ln, int par, cudaStream_t st);
+cudaError_t launch_stage_clear(m2c_ctx *c, const LayerState &Ln, int par, cudaStream_t st);
 // store.cu (NEXT-1)
 m2c_status store_open(m2c_ctx *c, const char *path, int n_fixed, int n_dyn, int ahead, void *frames,
                       size_t frames_bytes, size_t layer_bytes);

@@ -484,3 +484,37 @@ def test_store_backed_host_tier_matches_in_memory(m2c, tmp_path, n_fixed, n_dyn,
         assert st["layer_loads"] == L
     for c in ctxs:
         c.close()
+
+
+@pytest.mark.parametrize("mode", ["lru", "atu"])
+def test_lookahead_staging_is_transparent(m2c, mode):
+    """NEXT-2: staging layer l+1's predicted misses during layer l changes no token or cache
+    statistic, and serves a share of the misses device-side."""
+    cfg = get_config("T")
+    L = 4
+    plan = m2c.plan_of(cfg)
+    ws = [layer_weights(cfg, l, device="cuda") for l in range(L)]
+    ctxs = []
+    for la in (False, True):
+        ctx = _ctx(m2c, cfg, plan, n_layers=L)
+        cc = m2c.cache_cfg_capped(ctx.desc, plan, 1, 4, mode)
+        ctx.reserve_host_tier(L * ctx.layer_footprint(cc)[1])
+        for l, w in enumerate(ws):
+            ctx.load_layer(l, w["w_gate"], w["w_up"], w["w_down_t"], w["pred_A"], w["pred_B"], cc)
+        ctx.set_lookahead(la)
+        ctxs.append(ctx)
+    a, b = ctxs
+    xs = token_stream(cfg, 12, device="cuda")
+    for t in range(12):
+        xa, xb = xs[t].contiguous().clone(), xs[t].contiguous().clone()
+        a.decode_step(xa, t + 1)
+        b.decode_step(xb, t + 1)
+        torch.cuda.synchronize()
+        assert torch.equal(xa, xb), t
+    sa, sb = a.stats(), b.stats()
+    assert sa["hits"] == sb["hits"] and sa["misses"] == sb["misses"]
+    staged = b.lookahead_stats()
+    assert 0 < staged <= sum(sb["misses"])
+    assert a.lookahead_stats() == 0
+    for c in ctxs:
+        c.close()
