@@ -175,6 +175,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--eager", action="store_true", help="no CUDA graph")
     ap.add_argument("--unfused", action="store_true", help="per-phase kernel chain instead of k_decode")
+    ap.add_argument("--global-topk", action="store_true",
+                    help="NEXT-3: exact global top-k across the d_ff shards (P > 1)")
     ap.add_argument("--lookahead", action="store_true",
                     help="NEXT-2: stage layer l+1's predicted misses during layer l (LRU/ATU configs)")
     args = ap.parse_args()
@@ -224,6 +226,9 @@ def main():
         ctx.set_fused(False)
     if args.lookahead and cfg.cache_mode != "resident":
         ctx.set_lookahead(True)
+    if args.global_topk and P > 1:
+        from paper_2410_14740_b200 import tier_plan_make
+        ctx.set_global_topk(tier_plan_make(cfg.d_ff, cfg.active_pct, cfg.a16, cfg.a8, cfg.den))
 
     W, K = args.warmup, args.steps
     if cfg.cache_mode != "resident":
@@ -349,6 +354,7 @@ def main():
                        "active_pct": cfg.active_pct, "tier_plan": list(plan.as_tuple()),
                        "cache": cfg.cache_mode, "global_batch": 1, "seq_len": 1,
                        "parallelism": f"dff-shard{P}" if P > 1 else "single",
+                       "topk": ("global" if args.global_topk else "shard-local") if P > 1 else "global",
                        "l2": "inputs larger than L2 (%.0f MB touched per token)" % (ab["token"] / 1e6),
                        "graph": not args.eager, "persistent_kernel": fused},
             "hbm_gbs": gbs, "hbm_frac": gbs / peak,

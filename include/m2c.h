@@ -219,6 +219,31 @@ m2c_status m2c_profile_stamps(m2c_ctx *ctx, uint64_t *out, int64_t cap, int64_t 
 
 /* Kernels launched by the last m2c_decode_step (per token), and cumulative cache counters
  * (hits, misses per tier) since the last reset (device counters; synchronises). */
+/* ---- NEXT-3: exact global top-k under d_ff sharding --------------
+ * Shard-local top-k (R13) keeps k_r per rank; the paper's semantics is one global top-k over
+ * all F neurons.  m2c_predict_candidates(ctx, layer, x, n_cand, keys_out): this rank's scores
+ * and its top n_cand neurons as int64 keys (score << 32 | ~global id) sorted descending, i.e.
+ * (score desc, global id asc) order (R3); device [n_cand].  After an all-gather of every rank's
+ * keys into keys_all [P][n_cand] (rank order), m2c_select_global(ctx, keys_all, n_cand,
+ * global_plan, tier_ids_out, counts_out) finds the three global cuts (k16, k16+k8, k of the
+ * global plan) and writes THIS rank's selected neurons: tier_ids_out [global k] in three
+ * segments at the global plan's offsets (0, k16, k16+k8), local ids ascending in each, and
+ * counts_out [3] (device) = how many of each tier this rank owns.  Exact (the union over ranks
+ * equals the unsharded selection) when n_cand >= min(F_r, k); else M2C_ERR_CONFIG.  P x n_cand
+ * x 8 B must fit 200 KiB (M2C_ERR_CAPACITY).  Both calls are asynchronous on the compute
+ * stream; the all-gather is the caller's (ncclAllGather over the torch process group). */
+m2c_status m2c_predict_candidates(m2c_ctx *ctx, int32_t layer, const void *x, int32_t n_cand,
+                                  int64_t *keys_out);
+m2c_status m2c_select_global(m2c_ctx *ctx, const int64_t *keys_all, int32_t n_cand,
+                             const m2c_tier_plan *global_plan, int32_t *tier_ids_out, int32_t *counts_out);
+/* m2c_set_global_topk(ctx, global_plan): the resident, d_ff-sharded m2c_decode_step uses the
+ * global selection per layer (the two calls above with ncclAllGather of P x min(F_r, k) int64
+ * keys on the compute stream, then the FFN over this rank's part, the all-reduce as before);
+ * NULL restores shard-local top-k (R13).  Needs m2c_comm_init with an NCCL that exports
+ * ncclAllGather.  (Validated on one GPU through the two calls with emulated all-gathers; the
+ * NCCL wiring itself needs >= 2 GPUs.) */
+m2c_status m2c_set_global_topk(m2c_ctx *ctx, const m2c_tier_plan *global_plan);
+
 /* ---- NEXT-2: cross-layer lookahead ("the next one layer ... almost 100%") ---------
  * m2c_set_lookahead(ctx, 1): in the LRU/ATU decode chain, after layer l's cache lookup the
  * library also runs layer l+1's predictor and select on x_l (a prediction of layer l+1's

@@ -143,6 +143,27 @@ class M2CContext:
         self._host_off += (nbytes + 255) // 256 * 256
         return t
 
+    # ---- NEXT-3: exact global top-k under sharding (include/m2c.h) ----
+    def predict_candidates(self, layer, x, n_cand):
+        _require_cuda(x)
+        keys = torch.empty(max(n_cand, 1), dtype=torch.int64, device=self.device)
+        self._call(lib().m2c_predict_candidates, self._h, layer, _ptr(x), n_cand, _ptr(keys))
+        return keys[:n_cand]
+
+    def select_global(self, keys_all, n_cand, global_plan: TierPlan):
+        """keys_all: [P * n_cand] int64 (every rank's candidates, rank order) -> this rank's
+        (tier_ids [global k] in segments at the global plan's offsets, counts [3])."""
+        _require_cuda(keys_all)
+        ids = torch.full((max(global_plan.k, 1),), -1, dtype=torch.int32, device=self.device)
+        cnt = torch.zeros(3, dtype=torch.int32, device=self.device)
+        self._call(lib().m2c_select_global, self._h, _ptr(keys_all.contiguous()), n_cand,
+                   C.byref(global_plan), _ptr(ids), _ptr(cnt))
+        return ids[:global_plan.k], cnt
+
+    def set_global_topk(self, global_plan: TierPlan = None):
+        """Sharded decode with the exact global selection (NEXT-3); None: shard-local (R13)."""
+        check(lib().m2c_set_global_topk(self._h, C.byref(global_plan) if global_plan else None))
+
     # ---- NEXT-2: cross-layer lookahead staging (include/m2c.h) ----
     def set_lookahead(self, enable: bool):
         self._call(lib().m2c_set_lookahead, self._h, 1 if enable else 0)

@@ -40,6 +40,7 @@ struct NcclApi {
                               cudaStream_t) = nullptr;
     ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
     const char *(*errStr)(ncclResult_t) = nullptr;
+    ncclResult_t (*allGather)(const void *, void *, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
 };
 
 static NcclApi *load_nccl(const char *path) {
@@ -57,6 +58,7 @@ static NcclApi *load_nccl(const char *path) {
     api.allReduce = (decltype(api.allReduce))dlsym(api.h, "ncclAllReduce");
     api.commDestroy = (decltype(api.commDestroy))dlsym(api.h, "ncclCommDestroy");
     api.errStr = (decltype(api.errStr))dlsym(api.h, "ncclGetErrorString");
+    api.allGather = (decltype(api.allGather))dlsym(api.h, "ncclAllGather");
     if (!api.getUniqueId || !api.commInitRank || !api.allReduce || !api.commDestroy) {
         dlclose(api.h);
         api.h = nullptr;
@@ -183,6 +185,29 @@ static cudaError_t enqueue_layer(m2c_ctx *c, int l, __half *x) {
         if ((e = cudaStreamWaitEvent(c->stage_stream, c->ev_stage, 0))) return e;
         if ((e = launch_stage_fill(c, Ln, (l + 1) & 1, c->stage_stream))) return e;
         if ((e = cudaEventRecord(c->ev_staged[(l + 1) & 1], c->stage_stream))) return e;
+    }
+    if (L.mode == 0 && c->nranks > 1 && c->global_topk) {
+        // NEXT-3: exact global top-k -- local candidates (top min(F_r, k) by (score desc,
+        // global id asc)), an all-gather of the keys, the global cuts, this rank's share
+        const m2c_tier_plan &g = c->gplan;
+        const int n = g.k < c->F_r ? g.k : c->F_r;
+        if (!c->nccl || !c->nccl->allGather) return cudaErrorNotSupported;  // NCCL without ncclAllGather
+        const m2c_tier_plan pc{n, n, 0, 0};
+        if ((e = launch_predict(c, L, x, c->ws.s, c->ghist, nullptr, st))) return e;
+        if ((e = mark(c, l, 1))) return e;
+        if ((e = launch_select(c, c->ws.s, c->ghist, pc, c->ws.slots, nullptr, c->ws.tier_ids, st))) return e;
+        if ((e = launch_cand_keys(c, c->ws.s, c->ws.slots, n, c->gkeys, st))) return e;
+        if (c->nccl->allGather(c->gkeys, c->gkeys + n, (size_t)n, 4 /*int64*/, c->comm, st) != 0)
+            return cudaErrorUnknown;
+        if ((e = launch_select_global(c, c->gkeys + n, n, g, c->gids, c->ws.counts, st))) return e;
+        if ((e = mark(c, l, 2))) return e;
+        if ((e = launch_ffn(c, L, x, c->gids, c->ws.counts, g, c->ws.partial, st))) return e;
+        if ((e = mark(c, l, 3))) return e;
+        if ((e = launch_reduce(c, c->G, c->ws.partial, x, c->ws.y32, nullptr, nullptr, nullptr, st))) return e;
+        if (c->nccl->allReduce(c->ws.y32, c->ws.y32, (size_t)c->desc.d_model, 7 /*f32*/, 0 /*sum*/, c->comm, st) != 0)
+            return cudaErrorUnknown;
+        if ((e = launch_finalize(c, c->ws.y32, x, nullptr, x, st))) return e;
+        return mark(c, l, 4);
     }
     if ((e = launch_predict(c, L, x, c->ws.s, c->ghist, prefetch ? lists : nullptr, st))) return e;
     if ((e = mark(c, l, 1))) return e;
@@ -453,6 +478,7 @@ m2c_status m2c_destroy(m2c_ctx *c) {
     if (c->ev_lookup) cudaEventDestroy(c->ev_lookup);
     if (c->ev_fill) cudaEventDestroy(c->ev_fill);
     if (c->ev_stage) cudaEventDestroy(c->ev_stage);
+    if (c->gkeys) cudaFree(c->gkeys);
     if (c->stage_mem) {
         cudaStreamSynchronize(c->stage_stream);
         cudaStreamDestroy(c->stage_stream);
@@ -847,6 +873,68 @@ m2c_status m2c_profile_stamps(m2c_ctx *c, uint64_t *out, int64_t cap, int64_t *n
         return fail(M2C_ERR_STATE, "profile_stamps: profiling off or last token not on k_decode");
     M2C_CUDA(cudaStreamSynchronize(c->compute));
     M2C_CUDA(cudaMemcpy(out, c->dec_prof, 8 * (size_t)n, cudaMemcpyDeviceToHost));
+    return M2C_OK;
+}
+
+m2c_status m2c_predict_candidates(m2c_ctx *c, int32_t layer, const void *x, int32_t n_cand,
+                                  int64_t *keys_out) {
+    if (!c || !x || !keys_out) return fail(M2C_ERR_INVALID_ARG, "predict_candidates: null argument");
+    if (layer < 0 || layer >= c->desc.n_layers || !c->layers[layer].loaded)
+        return fail(M2C_ERR_STATE, "predict_candidates: layer not loaded");
+    if (n_cand < 0 || n_cand > c->F_r || n_cand > 16384)
+        return fail(M2C_ERR_CONFIG, "predict_candidates: need 0 <= n_cand <= min(F_r, 16384)");
+    if (!al16(x)) return fail(M2C_ERR_INVALID_ARG, "x must be 16-B aligned");
+    m2c_tier_plan p{n_cand, n_cand, 0, 0};
+    M2C_CUDA(launch_predict(c, c->layers[layer], (const __half *)x, c->ws.s, c->ghist, nullptr, c->compute));
+    M2C_CUDA(launch_select(c, c->ws.s, c->ghist, p, c->ws.slots /*rank order*/, nullptr, c->ws.tier_ids,
+                           c->compute));
+    M2C_CUDA(launch_cand_keys(c, c->ws.s, c->ws.slots, n_cand, reinterpret_cast<long long *>(keys_out), c->compute));
+    return M2C_OK;
+}
+
+m2c_status m2c_select_global(m2c_ctx *c, const int64_t *keys_all, int32_t n_cand,
+                             const m2c_tier_plan *global_plan, int32_t *tier_ids_out, int32_t *counts_out) {
+    if (!c || !keys_all || !global_plan || !tier_ids_out || !counts_out)
+        return fail(M2C_ERR_INVALID_ARG, "select_global: null argument");
+    const int P = c->desc.shard_count;
+    if (P > 32) return fail(M2C_ERR_CONFIG, "select_global: at most 32 ranks");
+    const int64_t F = (int64_t)c->F_r * P;
+    m2c_status st = check_plan(global_plan, (int32_t)(F < INT32_MAX ? F : INT32_MAX));
+    if (st) return st;
+    if (n_cand < (global_plan->k < c->F_r ? global_plan->k : c->F_r))
+        return fail(M2C_ERR_CONFIG, "select_global: n_cand < min(F_r, k): the union would not be exact");
+    if (8 * (size_t)P * n_cand > 200 * 1024)
+        return fail(M2C_ERR_CAPACITY, "select_global: P x n_cand candidates exceed the on-chip buffer");
+    M2C_CUDA(launch_select_global(c, reinterpret_cast<const long long *>(keys_all), n_cand, *global_plan,
+                                  tier_ids_out, counts_out, c->compute));
+    return M2C_OK;
+}
+
+m2c_status m2c_set_global_topk(m2c_ctx *c, const m2c_tier_plan *global_plan) {
+    if (!c) return fail(M2C_ERR_INVALID_ARG, "null ctx");
+    if (c->graph) {
+        cudaGraphExecDestroy(c->graph);
+        c->graph = nullptr;
+    }
+    if (!global_plan) {
+        c->global_topk = false;
+        return M2C_OK;
+    }
+    const int P = c->desc.shard_count;
+    m2c_status st = check_plan(global_plan, c->F_r * P);
+    if (st) return st;
+    const int n = global_plan->k < c->F_r ? global_plan->k : c->F_r;
+    if (8 * (size_t)P * n > 200 * 1024 || P > 32 || n > 16384)
+        return fail(M2C_ERR_CAPACITY, "global top-k: P x min(F_r, k) candidates exceed the on-chip buffer");
+    M2C_CUDA(cudaStreamSynchronize(c->compute));
+    if (c->gkeys) cudaFree(c->gkeys);
+    c->gkeys = nullptr;
+    // keys: own [n] + gathered [P][n]; then this layer's global lists [k_global]
+    const size_t kb = 8 * (size_t)(P + 1) * (n > 0 ? n : 1), lb = 4 * (size_t)(global_plan->k > 0 ? global_plan->k : 1);
+    M2C_CUDA(cudaMalloc(&c->gkeys, kb + lb));
+    c->gids = reinterpret_cast<int32_t *>(reinterpret_cast<uint8_t *>(c->gkeys) + kb);
+    c->gplan = *global_plan;
+    c->global_topk = true;
     return M2C_OK;
 }
 

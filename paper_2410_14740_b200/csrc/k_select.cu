@@ -358,11 +358,104 @@ __global__ void __launch_bounds__(1024, 1)
 size_t select_smem_bytes(int sh) { return 4 * ((size_t)kBins + 3 * ((size_t)1 << sh) + 3 * (size_t)kTieCap); }
 int select_blocks(int F_r) { return ((F_r + 31) / 32 + kChunksPerCta - 1) / kChunksPerCta; }
 
+// ---- NEXT-3: exact global top-k under d_ff sharding (P:253 global top-k semantics) --------
+// Each rank sends its local top-n candidates as 64-bit keys (score << 32 | ~global id): the
+// descending key order is (score desc, global id asc), R3.  Because a rank can contribute at
+// most k of the global top-k, n = min(F_r, k_global) candidates per rank make the union exact.
+__global__ void __launch_bounds__(256) k_cand_keys(const int32_t *__restrict__ s,
+                                                   const int32_t *__restrict__ rank_list, int n, int gbase,
+                                                   long long *__restrict__ keys) {
+    griddep_wait();
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int id = rank_list[i];
+    keys[i] = (long long)(((unsigned long long)(unsigned)s[id] << 32) | (unsigned)~(unsigned)(gbase + id));
+}
+
+// One CTA: the P gathered runs (each sorted descending) -> the three global cuts by bisection on
+// the key value (warp t, lane r binary-searches run r; counts by warp sums), then this rank's
+// run segments [K_t, K_{t-1}) -> local ids ascending per tier (rank by id inside a segment).
+__global__ void __launch_bounds__(1024) k_select_global(const long long *__restrict__ keys, int P, int n,
+                                                        int rank, int F_r, int k16, int k8, int k,
+                                                        int32_t *__restrict__ tier_ids,
+                                                        int32_t *__restrict__ counts) {
+    extern __shared__ __align__(16) long long runs[];  // [P][n]
+    __shared__ long long cut[3];
+    __shared__ int seg[4];
+    griddep_wait();
+    for (int i = threadIdx.x; i < P * n; i += blockDim.x) runs[i] = keys[i];
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    auto count_ge = [&](int r, long long X) {  // keys >= X in run r
+        int a = 0, b = n;
+        while (a < b) {
+            const int mid = (a + b) >> 1;
+            if (runs[r * n + mid] >= X) a = mid + 1;
+            else b = mid;
+        }
+        return a;
+    };
+    if (warp < 3) {
+        const int t = warp;
+        const int target = t == 0 ? k16 : (t == 1 ? k16 + k8 : k);
+        long long K = 0x7fffffffffffffffll;  // empty cut: no key reaches it
+        if (target > 0) {
+            // the target-th largest key: largest X with #(keys >= X) >= target (keys distinct)
+            long long lo = -(1ll << 60), hi = 1ll << 60;  // |key| < 2^56 (|s| < 2^24)
+            while (lo < hi) {
+                const long long mid = lo + (long long)(((unsigned long long)(hi - lo) + 1ull) >> 1);
+                int c = lane < P ? count_ge(lane, mid) : 0;
+                c = __reduce_add_sync(0xffffffffu, c);
+                if (c >= target) lo = mid;
+                else hi = mid - 1;
+            }
+            K = lo;
+        }
+        if (lane == 0) cut[t] = K;
+    }
+    __syncthreads();
+    if (threadIdx.x < 3) seg[threadIdx.x + 1] = count_ge(rank, cut[threadIdx.x]);  // nested prefixes
+    if (threadIdx.x == 0) seg[0] = 0;
+    __syncthreads();
+    const int base = rank * F_r;
+    const int off[3] = {0, k16, k16 + k8};
+    for (int t = 0; t < 3; t++) {
+        const int a = seg[t], b = seg[t + 1];
+        for (int e = a + (int)threadIdx.x; e < b; e += blockDim.x) {
+            const unsigned gid = ~(unsigned)(runs[rank * n + e] & 0xffffffffll);
+            int rk = 0;  // members with a smaller id come first
+            for (int e2 = a; e2 < b; e2++) rk += ~(unsigned)(runs[rank * n + e2] & 0xffffffffll) < gid;
+            tier_ids[off[t] + rk] = (int)gid - base;
+        }
+        if (threadIdx.x == 0) counts[t] = b - a;
+    }
+}
+
 cudaError_t init_select_attrs() {
     cudaError_t e = cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)select_smem_bytes(12));
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_rank_list, cudaFuncAttributeMaxDynamicSharedMemorySize, 8 * 16384);
+    return e;
+}
+
+cudaError_t launch_cand_keys(m2c_ctx *c, const int32_t *scores, const int32_t *rank_list, int n,
+                             long long *keys, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    cudaError_t e = launch_k(k_cand_keys, dim3((n + 255) / 256), dim3(256), 0, st, scores, rank_list, n,
+                             c->desc.shard_index * c->F_r, keys);
+    c->launch_counter++;
+    return e;
+}
+
+cudaError_t launch_select_global(m2c_ctx *c, const long long *keys, int n, const m2c_tier_plan &g,
+                                 int32_t *tier_ids, int32_t *counts, cudaStream_t st) {
+    const size_t smem = 8 * (size_t)c->desc.shard_count * n;
+    cudaError_t e = cudaFuncSetAttribute(k_select_global, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    e = launch_k(k_select_global, dim3(1), dim3(1024), smem, st, keys, c->desc.shard_count, n,
+                 c->desc.shard_index, c->F_r, g.k_fp16, g.k_int8, g.k, tier_ids, counts);
+    c->launch_counter++;
     return e;
 }
 

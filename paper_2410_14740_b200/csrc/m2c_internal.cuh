@@ -133,6 +133,11 @@ struct m2c_ctx {
     int32_t *spec_ids = nullptr;                 // [k] predicted tier lists of the next layer
     cudaStream_t stage_stream = nullptr;          // staging copies (own stream: concurrent with fills)
     cudaEvent_t ev_staged[2] = {nullptr, nullptr};  // layer parity: staging complete
+    // NEXT-3: exact global top-k in the sharded decode chain
+    bool global_topk = false;
+    m2c_tier_plan gplan{};
+    long long *gkeys = nullptr;   // [n] own candidates | [P][n] gathered
+    int32_t *gids = nullptr;      // [k_global] this rank's part of the global tier lists
     // multi-GPU
     m2c::NcclApi *nccl = nullptr;
     void *comm = nullptr;
@@ -160,6 +165,11 @@ cudaError_t launch_predict(m2c_ctx *c, const LayerState &L, const __half *x, int
 cudaError_t launch_select(m2c_ctx *c, const int32_t *scores, int *hist, const m2c_tier_plan &p,
                           int32_t *rank_list, int8_t *tier_of, int32_t *tier_ids, cudaStream_t st);
 size_t select_smem_bytes(int sh);
+// NEXT-3 (k_select.cu)
+cudaError_t launch_cand_keys(m2c_ctx *c, const int32_t *scores, const int32_t *rank_list, int n,
+                             long long *keys, cudaStream_t st);
+cudaError_t launch_select_global(m2c_ctx *c, const long long *keys, int n, const m2c_tier_plan &g,
+                                 int32_t *tier_ids, int32_t *counts, cudaStream_t st);
 int select_blocks(int F_r);
 cudaError_t launch_lru(m2c_ctx *c, LayerState &L, const int32_t *step_dev, const int32_t *tier_ids,
                        const m2c_tier_plan &p, int32_t *slots, uint32_t *hit_bits,

@@ -518,3 +518,45 @@ def test_lookahead_staging_is_transparent(m2c, mode):
     assert a.lookahead_stats() == 0
     for c in ctxs:
         c.close()
+
+
+@pytest.mark.parametrize("P,pct,a16,a8,den", [(2, 10, 25, 25, 100), (4, 10, 25, 25, 100),
+                                              (4, 30, 0, 100, 300), (8, 5, 100, 0, 100)])
+def test_global_topk_under_sharding_equals_unsharded(m2c, P, pct, a16, a8, den):
+    """NEXT-3: every rank's local top-min(F_r, k) candidates, all-gathered, give each rank
+    its part of the GLOBAL selection; the union over ranks equals the unsharded oracle's tier
+    lists bit-exactly (the shard-local default, R13, does not)."""
+    cfg = get_config("T")
+    F = cfg.d_ff
+    F_r = F // P
+    gplan = m2c.tier_plan_make(F, pct, a16, a8, den)
+    n = min(F_r, gplan.k)
+    full = layer_weights(cfg, 0, device="cuda", parts=("A", "B"))  # (the CUDA generator's draws)
+    An, Bn = full["pred_A"].cpu().numpy(), full["pred_B"].cpu().numpy()
+    ctxs = []
+    for r in range(P):
+        w = layer_weights(cfg, 0, device="cuda", shard=(r, P), parts=("A", "B"))
+        dummy = torch.zeros(F_r, cfg.d_model, dtype=torch.float16, device="cuda")
+        ctx = _ctx(m2c, cfg, m2c.tier_plan_make(F_r, pct, a16, a8, den), shard=(r, P))
+        ctx.load_layer(0, dummy, dummy, dummy, w["pred_A"], w["pred_B"])
+        ctxs.append(ctx)
+    xs = layer_input_stream(cfg, 0, 4, device="cuda")
+    gp = np.array(gplan.as_tuple(), np.int32)
+    for t in range(4):
+        x = xs[t].contiguous()
+        keys = torch.cat([c.predict_candidates(0, x, n) for c in ctxs])
+        got = [[], [], []]
+        for r, c in enumerate(ctxs):
+            ids, cnt = c.select_global(keys, n, gplan)
+            ids, cnt = ids.cpu().numpy(), cnt.cpu().numpy()
+            off = [0, gplan.k_fp16, gplan.k_fp16 + gplan.k_int8]
+            for tier in range(3):
+                seg = ids[off[tier]:off[tier] + cnt[tier]]
+                assert np.all(np.diff(seg) > 0)  # ascending local ids
+                got[tier].extend((r * F_r + seg).tolist())
+        ref = orc.select(orc.predict(xs[t].cpu().numpy(), An, Bn)["s"], gp)["tier_ids"]
+        off = [0, gplan.k_fp16, gplan.k_fp16 + gplan.k_int8, gplan.k]
+        for tier in range(3):
+            assert sorted(got[tier]) == ref[off[tier]:off[tier + 1]].tolist(), (t, tier)
+    for c in ctxs:
+        c.close()
