@@ -392,7 +392,7 @@ m2c_status m2c_create(const m2c_model_desc *desc, int32_t device, m2c_stream_t c
                  o_dprof = take(8 * (size_t)kDecodeStamps * c->G * desc->n_layers),
                  o_binsh = take(4 * (size_t)desc->n_layers), o_sabs = take(8 * (size_t)c->G),
                  o_hb = take(8 * 2 * (size_t)kHStride * r),
-                 o_runs = take(4 * (size_t)c->G * ((((F_r + c->G - 1) / c->G) + 3) & ~3)),
+                 o_runs = take(4 * (size_t)c->G * (((F_r + c->G - 1) / c->G) | 1) + 16),
                  o_dhist = take(decode_hist_bytes()),
                  o_prev = take(4 * (size_t)desc->n_layers * (plan->k > 0 ? plan->k : 1));
     // score histogram geometry: |s| <= 127^2 r, bins of 2^sh over [0, 2 smax] (4096 bins)

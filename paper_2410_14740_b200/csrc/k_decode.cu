@@ -313,7 +313,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
         // ================= P2: hq = Q(h), x -> smem, scores, histogram, sorted run ==========
         const int shl = __ldcg(p.bin_sh + l);  // this token's histogram scale for layer l
         const int rps = (F_r + G - 1) / G;      // neurons per CTA (this CTA: ids [n0, n1))
-        const int RP = (rps + 3) & ~3;          // run length in the runs array (16-B rows)
+        const int RP = rps | 1;  // run row length: odd, so same-index probes of 32 runs hit 32 banks
         {
             int8_t *hq = reinterpret_cast<int8_t *>(S.ring);
             int *keys = reinterpret_cast<int *>(S.ring + 1024);  // this CTA's run keys (<= 256)
@@ -399,7 +399,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
             // order the ring's earlier generic accesses (and the acquired global data) before
             // the async-proxy copies
             asm volatile("fence.proxy.async;" ::: "memory");
-            const uint32_t sb = (uint32_t)(4 * G * T);
+            const uint32_t sb = (uint32_t)((4 * G * T + 15) & ~15);  // (the buffer has slack)
             mbar_expect_tx(&sel_bar, (uint32_t)(4 * kBins) + sb);
             bulk_g2s_plain(hs, hist, 4 * kBins, &sel_bar);
             bulk_g2s_plain(S.ring + kSbufOff, p.runs, sb, &sel_bar);
@@ -879,7 +879,7 @@ size_t decode_hist_bytes() { return sizeof(int) * 2 * (size_t)kHistW; }
 // (the whole run: a probe past a partial prefix would stall its warp on an L2 load)
 int decode_top_len(const m2c_ctx *c) {
     const int G = c->G, rps = (c->F_r + G - 1) / G;
-    return (rps + 3) & ~3;
+    return rps | 1;
 }
 // all runs fit the ring behind the histogram scratch; run keys hold local indices < 255
 int decode_max_F() { return 254 * 148 < (kRing - kSbufOff) / 4 - 4 * 148 ? 254 * 148 : (kRing - kSbufOff) / 4 - 4 * 148; }
