@@ -287,8 +287,10 @@ class M2CContext:
     def set_graph(self, enable: bool):
         check(lib().m2c_set_graph(self._h, 1 if enable else 0))
 
-    def set_fused(self, enable: bool):
-        check(lib().m2c_set_fused(self._h, 1 if enable else 0))
+    def set_fused(self, enable):
+        """True/1: the persistent decode kernel when eligible; 2: the layer-split k_decode (one
+        launch per layer, the sharded engine) even unsharded; False/0: the per-phase chain."""
+        check(lib().m2c_set_fused(self._h, int(enable)))
 
     def profile(self, enable: bool):
         check(lib().m2c_profile(self._h, 1 if enable else 0))

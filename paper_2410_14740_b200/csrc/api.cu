@@ -261,11 +261,34 @@ static bool decode_fused(const m2c_ctx *c) {
     return true;
 }
 
+// the layer-split engine: k_decode one layer per launch, the d_ff shards' partial y summed by
+// one NCCL all-reduce between launches (the next launch adds it into x); resident stacks only
+static bool decode_split(const m2c_ctx *c) {
+    if (!c->use_fused || c->global_topk || (c->nranks < 2 && !c->force_split)) return false;
+    const int rps = (c->F_r + c->G - 1) / c->G;
+    if (c->F_r > decode_max_F() || rps > c->desc.d_model / 8 || rps > 4096) return false;
+    for (const LayerState &L : c->layers)
+        if (L.mode != 0) return false;
+    return true;
+}
+
 static cudaError_t enqueue_token(m2c_ctx *c, __half *x) {
     const m2c_tier_plan &p = c->plan;
-    c->last_token_fused = decode_fused(c);
+    c->last_token_fused = decode_fused(c) && !c->force_split;
+    c->last_token_split = !c->last_token_fused && decode_split(c);
     if (c->last_token_fused)
         return launch_decode(c, x, c->prof_ev.empty() ? nullptr : c->dec_prof, c->compute);
+    if (c->last_token_split) {
+        unsigned long long *prof = c->prof_ev.empty() ? nullptr : c->dec_prof;
+        cudaError_t e;
+        for (int l = 0; l < c->desc.n_layers; l++) {
+            if ((e = launch_decode(c, x, prof, c->compute, l, 1, l > 0 ? c->ws.y32 : nullptr, c->ws.y32))) return e;
+            if (c->nranks > 1 && c->nccl->allReduce(c->ws.y32, c->ws.y32, (size_t)c->desc.d_model, 7 /*f32*/,
+                                                    0 /*sum*/, c->comm, c->compute) != 0)
+                return cudaErrorUnknown;
+        }
+        return launch_finalize(c, c->ws.y32, x, nullptr, x, c->compute);
+    }
     cudaError_t e = launch_set_counts(c->ws.counts, p.k_fp16, p.k_int8, p.k_int4, c->compute);
     c->launch_counter++;
     if (e) return e;
@@ -733,11 +756,12 @@ m2c_status m2c_set_graph(m2c_ctx *c, int32_t enable) {
 
 m2c_status m2c_set_fused(m2c_ctx *c, int32_t enable) {
     if (!c) return fail(M2C_ERR_INVALID_ARG, "null ctx");
-    if (c->use_fused != (enable != 0) && c->graph) {
+    if (c->graph) {
         cudaGraphExecDestroy(c->graph);
         c->graph = nullptr;
     }
     c->use_fused = enable != 0;
+    c->force_split = enable == 2;
     return M2C_OK;
 }
 
@@ -831,7 +855,7 @@ m2c_status m2c_profile_read(m2c_ctx *c, float *ms, int32_t *ffn_launches) {
     if (!c || !ms) return fail(M2C_ERR_INVALID_ARG, "null argument");
     if (c->prof_ev.empty()) return fail(M2C_ERR_STATE, "profiling not enabled");
     M2C_CUDA(cudaStreamSynchronize(c->compute));
-    if (c->last_token_fused) {  // in-kernel per-CTA stamps (ns): see k_decode.cu
+    if (c->last_token_fused || c->last_token_split) {  // in-kernel per-CTA stamps (ns): see k_decode.cu
         const int L = c->desc.n_layers, G = c->G, S = kDecodeStamps;
         std::vector<unsigned long long> t((size_t)S * G * L);
         M2C_CUDA(cudaMemcpy(t.data(), c->dec_prof, 8 * t.size(), cudaMemcpyDeviceToHost));
@@ -869,7 +893,7 @@ m2c_status m2c_profile_stamps(m2c_ctx *c, uint64_t *out, int64_t cap, int64_t *n
     *n_out = n;
     if (!out) return M2C_OK;
     if (cap < n) return fail(M2C_ERR_INVALID_ARG, "profile_stamps: buffer too small");
-    if (c->prof_ev.empty() || !c->last_token_fused)
+    if (c->prof_ev.empty() || !(c->last_token_fused || c->last_token_split))
         return fail(M2C_ERR_STATE, "profile_stamps: profiling off or last token not on k_decode");
     M2C_CUDA(cudaStreamSynchronize(c->compute));
     M2C_CUDA(cudaMemcpy(out, c->dec_prof, 8 * (size_t)n, cudaMemcpyDeviceToHost));

@@ -88,6 +88,9 @@ struct DecArgs {
     int prefetch;
     int *bin_sh;                // [n_layers] histogram scale per layer (adapted token to token)
     unsigned *sabs;             // [2G] per-CTA |s| of its run's two ends (current layer)
+    // layer-split mode (d_ff-sharded decode: one launch per layer, NCCL all-reduce between):
+    const float *pre_y;         // [d] or null: the prologue first forms x = fp16(x + fp16(pre_y))
+    float *post_y;              // [d] or null: R writes the reduced partial y here instead of x
 };
 
 // histogram bin of a raw score: monotone, clamped; 2^sh-wide bins centred on 0
@@ -290,7 +293,12 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
         if (tid < 32) {
             bool bad = false;
             int m, sh;
-            fp16_fixed(__half_as_ushort(__ldcg(p.x + ch * 32 + tid)), m, sh, bad);
+            __half xv = __ldcg(p.x + ch * 32 + tid);
+            if (p.pre_y) {  // the previous layer's all-reduced y (split mode): x = fp16(x + fp16(y))
+                xv = __hadd(xv, __float2half_rn(__ldcg(p.pre_y + ch * 32 + tid)));
+                p.x[ch * 32 + tid] = xv;
+            }
+            fp16_fixed(__half_as_ushort(xv), m, sh, bad);
             if (bad) atomicOr(p.err, 1u);
             xm[tid] = m;
             xsh[tid] = sh;
@@ -844,7 +852,8 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
 #pragma unroll
                     for (int w = 0; w < 32; w++) y += rf[w][lane];
                     const __half xn = __hadd(xs_h[e], __float2half_rn(y));
-                    p.x[e] = xn;
+                    if (p.post_y) p.post_y[e] = y;  // split mode: this rank's y, to be all-reduced
+                    else p.x[e] = xn;
                     if (more) {
                         bool bad = false;
                         int m, sh;
@@ -904,11 +913,15 @@ cudaError_t decode_write_layer_table(m2c_ctx *c, void *dev_table) {
     return cudaMemcpy(dev_table, t.data(), sizeof(DecLayer) * t.size(), cudaMemcpyHostToDevice);
 }
 
-cudaError_t launch_decode(m2c_ctx *c, __half *x, unsigned long long *prof, cudaStream_t st) {
+cudaError_t launch_decode(m2c_ctx *c, __half *x, unsigned long long *prof, cudaStream_t st, int layer0,
+                          int nl, const float *pre_y, float *post_y) {
     const int d = c->desc.d_model;
+    if (nl < 0) nl = c->desc.n_layers - layer0;
     DecArgs a;
-    a.layers = reinterpret_cast<const DecLayer *>(c->dec_layers);
-    a.n_layers = c->desc.n_layers;
+    a.layers = reinterpret_cast<const DecLayer *>(c->dec_layers) + layer0;
+    a.n_layers = nl;
+    a.pre_y = pre_y;
+    a.post_y = post_y;
     a.d = d;
     a.r = c->desc.pred_rank;
     a.F_r = c->F_r;
@@ -926,13 +939,13 @@ cudaError_t launch_decode(m2c_ctx *c, __half *x, unsigned long long *prof, cudaS
     a.runs = c->dec_runs;
     a.T = decode_top_len(c);
     a.ghist = c->dec_hist;
-    a.lists = c->prev_ids;
+    a.lists = c->prev_ids + (size_t)layer0 * (c->plan.k > 0 ? c->plan.k : 1);
     a.partial = c->ws.partial;
     a.bar_flags = c->bar_flags;
     a.bar_epoch = c->bar_epoch;
     a.err = c->ws.err;
-    a.prof = prof;
-    a.bin_sh = c->dec_bin_sh;
+    a.prof = prof ? prof + (size_t)layer0 * c->G * kStamps : nullptr;
+    a.bin_sh = c->dec_bin_sh + layer0;
     a.sabs = c->dec_sabs;
     // M2C_DECODE_PREFETCH (see prefetch_layers; a tuning / measurement knob, results are identical)
     {

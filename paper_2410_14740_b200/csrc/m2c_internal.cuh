@@ -109,6 +109,8 @@ struct m2c_ctx {
     int *sel_done = nullptr;    // select completion counter
     int *sel_epoch = nullptr;   // select launch epoch
     bool use_fused = true;
+    bool force_split = false;   // layer-split k_decode even unsharded (testing; m2c_set_fused(ctx, 2))
+    bool last_token_split = false;
     // persistent decode kernel (k_decode): layer pointer table, grid-barrier flags, stamps
     void *dec_layers = nullptr;
     unsigned *bar_flags = nullptr;   // [G]
@@ -196,7 +198,8 @@ cudaError_t launch_reduce(m2c_ctx *c, int n_partials, const float *partial, cons
 cudaError_t launch_finalize(m2c_ctx *c, const float *y32, const __half *x, __half *y16,
                             __half *x_next, cudaStream_t st);
 // persistent decode kernel (k_decode.cu)
-cudaError_t launch_decode(m2c_ctx *c, __half *x, unsigned long long *prof, cudaStream_t st);
+cudaError_t launch_decode(m2c_ctx *c, __half *x, unsigned long long *prof, cudaStream_t st, int layer0 = 0,
+                          int nl = -1, const float *pre_y = nullptr, float *post_y = nullptr);
 cudaError_t init_decode_attrs();
 cudaError_t decode_write_layer_table(m2c_ctx *c, void *dev_table);
 size_t decode_layer_table_bytes(int n_layers);

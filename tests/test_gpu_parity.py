@@ -560,3 +560,35 @@ def test_global_topk_under_sharding_equals_unsharded(m2c, P, pct, a16, a8, den):
             assert sorted(got[tier]) == ref[off[tier]:off[tier + 1]].tolist(), (t, tier)
     for c in ctxs:
         c.close()
+
+
+@pytest.mark.parametrize("name,layers", [("T", 3), ("S7", 3)])
+def test_decode_layer_split_equals_fused(m2c, name, layers):
+    """The layer-split engine (k_decode one layer per launch, the partial y handed to the next
+    launch through the all-reduce buffer -- the d_ff-sharded decode) is bit-identical to the
+    whole-token k_decode and to the per-phase chain."""
+    cfg = get_config(name)
+    plan = m2c.plan_of(cfg)
+    ctxs = []
+    for mode in (1, 2, 0):
+        ctx = _ctx(m2c, cfg, plan, n_layers=layers)
+        for l in range(layers):
+            w = layer_weights(cfg, l, device="cuda")
+            ctx.load_layer(l, w["w_gate"], w["w_up"], w["w_down_t"], w["pred_A"], w["pred_B"])
+        ctx.set_fused(mode)
+        ctxs.append(ctx)
+    xs = token_stream(cfg, 5, device="cuda")
+    for t in range(5):
+        outs = []
+        for ctx in ctxs:
+            x = xs[t].contiguous().clone()
+            ctx.decode_step(x, t + 1)
+            outs.append(x)
+        torch.cuda.synchronize()
+        for l in range(layers):
+            assert torch.equal(ctxs[0].decode_lists(l), ctxs[1].decode_lists(l)), (t, l)
+        assert torch.equal(outs[0], outs[1]), t
+        assert torch.equal(outs[0], outs[2]), t
+    assert ctxs[1].stats()["kernels_per_token"] == layers + 1  # L launches + the final residual
+    for c in ctxs:
+        c.close()
