@@ -160,6 +160,12 @@ static cudaError_t enqueue_fill(m2c_ctx *c, int l, const m2c_tier_plan &p, int s
     return e;
 }
 
+// k_decode's P2/P3 (predictor + distributed exact select) fit: the same shape bounds
+static bool decode_select_ok(const m2c_ctx *c) {
+    const int rps = (c->F_r + c->G - 1) / c->G;
+    return c->F_r <= decode_max_F() && rps <= c->desc.d_model / 8 && rps <= 4096;
+}
+
 static cudaError_t enqueue_layer(m2c_ctx *c, int l, __half *x) {
     LayerState &L = c->layers[l];
     const m2c_tier_plan &p = c->plan;
@@ -209,10 +215,17 @@ static cudaError_t enqueue_layer(m2c_ctx *c, int l, __half *x) {
         if ((e = launch_finalize(c, c->ws.y32, x, nullptr, x, st))) return e;
         return mark(c, l, 4);
     }
-    if ((e = launch_predict(c, L, x, c->ws.s, c->ghist, prefetch ? lists : nullptr, st))) return e;
-    if ((e = mark(c, l, 1))) return e;
-    if ((e = launch_select(c, c->ws.s, c->ghist, p, nullptr, nullptr, ids, st))) return e;
-    if ((e = mark(c, l, 2))) return e;
+    if (L.mode != 0 && c->use_fused && decode_select_ok(c)) {
+        // the predictor + exact select of k_decode in one launch (its P2/P3 phases)
+        if ((e = launch_decode(c, x, nullptr, st, l, 1, nullptr, nullptr, ids))) return e;
+        if ((e = mark(c, l, 1))) return e;
+        if ((e = mark(c, l, 2))) return e;
+    } else {
+        if ((e = launch_predict(c, L, x, c->ws.s, c->ghist, prefetch ? lists : nullptr, st))) return e;
+        if ((e = mark(c, l, 1))) return e;
+        if ((e = launch_select(c, c->ws.s, c->ghist, p, nullptr, nullptr, ids, st))) return e;
+        if ((e = mark(c, l, 2))) return e;
+    }
     int np = c->G;
     if (L.mode == 0) {
         e = launch_ffn(c, L, x, ids, c->ws.counts, p, c->ws.partial, st);

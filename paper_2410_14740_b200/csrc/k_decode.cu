@@ -91,6 +91,7 @@ struct DecArgs {
     // layer-split mode (d_ff-sharded decode: one launch per layer, NCCL all-reduce between):
     const float *pre_y;         // [d] or null: the prologue first forms x = fp16(x + fp16(pre_y))
     float *post_y;              // [d] or null: R writes the reduced partial y here instead of x
+    int select_only;            // 1: stop after P3 (one layer; the chain's cache + FFN follow)
 };
 
 // histogram bin of a raw score: monotone, clamped; 2^sh-wide bins centred on 0
@@ -780,6 +781,13 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
             __syncthreads();
         }
         STAMP(5);
+        if (p.select_only) {  // the LRU/ATU chain: predictor + selection only; the lists are out
+            // the histogram must be clear for the next launch, once every CTA has copied it
+            grid_sync(p.bar_flags, base + ++nbar, p.err);
+            if (cta == G - 1)
+                for (int i = tid; i < kBins; i += NT) hist[i] = 0;
+            break;
+        }
 
         // ================= P4: fused dequant-GEMV FFN over this CTA's share ===============
         {
@@ -914,7 +922,7 @@ cudaError_t decode_write_layer_table(m2c_ctx *c, void *dev_table) {
 }
 
 cudaError_t launch_decode(m2c_ctx *c, __half *x, unsigned long long *prof, cudaStream_t st, int layer0,
-                          int nl, const float *pre_y, float *post_y) {
+                          int nl, const float *pre_y, float *post_y, int32_t *lists_out) {
     const int d = c->desc.d_model;
     if (nl < 0) nl = c->desc.n_layers - layer0;
     DecArgs a;
@@ -939,7 +947,8 @@ cudaError_t launch_decode(m2c_ctx *c, __half *x, unsigned long long *prof, cudaS
     a.runs = c->dec_runs;
     a.T = decode_top_len(c);
     a.ghist = c->dec_hist;
-    a.lists = c->prev_ids + (size_t)layer0 * (c->plan.k > 0 ? c->plan.k : 1);
+    a.lists = lists_out ? lists_out : c->prev_ids + (size_t)layer0 * (c->plan.k > 0 ? c->plan.k : 1);
+    a.select_only = lists_out != nullptr;
     a.partial = c->ws.partial;
     a.bar_flags = c->bar_flags;
     a.bar_epoch = c->bar_epoch;

@@ -199,7 +199,8 @@ cudaError_t launch_finalize(m2c_ctx *c, const float *y32, const __half *x, __hal
                             __half *x_next, cudaStream_t st);
 // persistent decode kernel (k_decode.cu)
 cudaError_t launch_decode(m2c_ctx *c, __half *x, unsigned long long *prof, cudaStream_t st, int layer0 = 0,
-                          int nl = -1, const float *pre_y = nullptr, float *post_y = nullptr);
+                          int nl = -1, const float *pre_y = nullptr, float *post_y = nullptr,
+                          int32_t *lists_out = nullptr);  // lists_out: select-only (one layer)
 cudaError_t init_decode_attrs();
 cudaError_t decode_write_layer_table(m2c_ctx *c, void *dev_table);
 size_t decode_layer_table_bytes(int n_layers);
