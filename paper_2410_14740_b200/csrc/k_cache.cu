@@ -9,6 +9,8 @@
 // Policy details (the paper is silent): DESIGN.md R7 -- step-granular timestamps, victims =
 // smallest (last_use, slot) with last_use < t, misses in ascending id paired with victims in
 // that order; a tier change is a miss in the new tier's pool (R9).
+#include <cstdlib>
+
 #include "m2c_internal.cuh"
 
 namespace m2c {
@@ -383,7 +385,8 @@ cudaError_t launch_fill(m2c_ctx *c, const LayerState &L, const m2c_tier_plan &p,
         a.stage[t] = stage_par >= 0 ? c->stage_buf[stage_par][t] : nullptr;
     }
     a.staged = c->ws.stats + 6;
-    cudaError_t e = launch_k(k_fill, dim3(64), dim3(256), 0, st, a, c->ws.counts, c->ws.miss_ids,
+    static const int fill_ctas = getenv("M2C_FILL_CTAS") ? atoi(getenv("M2C_FILL_CTAS")) : 64;  // tuning knob
+    cudaError_t e = launch_k(k_fill, dim3(fill_ctas), dim3(256), 0, st, a, c->ws.counts, c->ws.miss_ids,
                              c->ws.miss_items);
     c->launch_counter++;
     return e;
