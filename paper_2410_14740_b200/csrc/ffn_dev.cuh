@@ -24,6 +24,7 @@
 //    s * sum (q - z) x (R5).
 //  * The per-CTA partial y goes to a [G][d] fp32 buffer reduced in a fixed order by k_reduce.
 #pragma once
+#include <type_traits>
 #include "m2c_internal.cuh"
 
 namespace m2c {
@@ -454,7 +455,84 @@ __device__ __forceinline__ void ffn_loop(const FfnArgs &a, int d, int act, const
     __syncthreads();
     if (stamps && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(stamps[0]));
 
-    if (fast && nwarp >= 2 && (nwarp & 1) == 0 && M2C_FFN_WS) {
+    if (fast && M2C_FFN_WS == 2) {
+        // Pipelined (all records in flight): every warp first computes its gate/up units in
+        // record order as the copies land (the unit that completes record j combines its
+        // quarters in a fixed order and arrives on abar[j]), then accumulates the
+        // down-projection of its own 8 y elements per thread record by record, waiting only
+        // for each a_j -- no block-wide barrier between the two, so the down-projection of
+        // the early records overlaps the gate/up of the late ones.  Per element the
+        // operations and their order are those of the batched path (bit-identical).
+        const int P = nchunk >= 512 ? 4 : 1;
+        if (threadIdx.x < kNSlot) sm.acnt[threadIdx.x] = 0;
+        __syncthreads();
+        for (int u = warp; u < n_items * P; u += nwarp) {
+            const int j = u / P, pp = u - j * P;
+            mbar_wait(&sm.bars[(jb + j) % kNSlot], (uint32_t)(((jb + j) / kNSlot) & 1));
+            const int ds = dsc[j];
+            float pg, pu;
+            gu_any(ds >> 24, ring + (ds & 0xffffff), xs, d, sm.cb[P][pp], sm.cb[P][pp + 1], pg, pu);
+            pg = warp_sum_f(pg);
+            pu = warp_sum_f(pu);
+            if (lane == 0) {
+                if (P == 1) {
+                    sm.a_sm[j] = (act == 1) ? fmaxf(pg, 0.f) * pu : pg / (1.f + expf(-pg)) * pu;
+                    mbar_arrive(&sm.abar[(jb + j) % kNSlot]);
+                } else {
+                    sm.apart[j][pp][0] = pg;
+                    sm.apart[j][pp][1] = pu;
+                    __threadfence_block();
+                    if (atomicAdd(&sm.acnt[j], 1) == P - 1) {  // last quarter: combine, publish
+                        __threadfence_block();
+                        float g = 0.f, uu = 0.f;
+                        for (int q = 0; q < P; q++) {
+                            g += sm.apart[j][q][0];
+                            uu += sm.apart[j][q][1];
+                        }
+                        sm.a_sm[j] = (act == 1) ? fmaxf(g, 0.f) * uu : g / (1.f + expf(-g)) * uu;
+                        mbar_arrive(&sm.abar[(jb + j) % kNSlot]);
+                    }
+                }
+            }
+        }
+        if (stamps && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(stamps[1]));
+        float y[8];
+#pragma unroll
+        for (int i = 0; i < 8; i++) y[i] = 0.f;
+        // the batched path's order: tier segments, two records per step
+        auto wait_a = [&](int j) { mbar_wait(&sm.abar[(jb + j) % kNSlot], (uint32_t)(((jb + j) / kNSlot) & 1)); };
+        auto down_range = [&](auto tier_c, int ja, int jz) {
+            constexpr int TIER = decltype(tier_c)::value;
+            int j = ja;
+            for (; j + 1 < jz; j += 2) {
+                wait_a(j);
+                wait_a(j + 1);
+                const int d0 = dsc[j], d1 = dsc[j + 1];
+                const float a0 = sm.a_sm[j], a1 = sm.a_sm[j + 1];
+                down_t<TIER>(ring + (d0 & 0xffffff), d, a0, y);
+                down_t<TIER>(ring + (d1 & 0xffffff), d, a1, y);
+            }
+            if (j < jz) {
+                wait_a(j);
+                down_t<TIER>(ring + (dsc[j] & 0xffffff), d, sm.a_sm[j], y);
+            }
+        };
+        // (batches of the batched path: [bst[b], bst[b+1]); inside, tier segments)
+        const int nbt = sm.nbatch;
+        for (int bi = 0; bi < nbt; bi++) {
+            const int j0 = bst[bi], je = bst[bi + 1];
+            const int s1 = min(max(c1, j0), je), s2 = min(max(c2, j0), je);
+            down_range(std::integral_constant<int, 0>(), j0, s1);
+            down_range(std::integral_constant<int, 1>(), s1, s2);
+            down_range(std::integral_constant<int, 2>(), s2, je);
+        }
+        float *out = partial + (int64_t)blockIdx.x * d + 8 * threadIdx.x;
+        reinterpret_cast<float4 *>(out)[0] = make_float4(y[0], y[1], y[2], y[3]);
+        reinterpret_cast<float4 *>(out)[1] = make_float4(y[4], y[5], y[6], y[7]);
+        __syncthreads();  // the ring's records are consumed
+        return;
+    }
+    if (fast && nwarp >= 2 && (nwarp & 1) == 0 && M2C_FFN_WS == 1) {
         // Warp-specialised (all records in flight): warps [0, NG) compute gate/up units in
         // record order as the copies land; the unit that completes record j combines its
         // quarters in a fixed order and arrives on abar[j]; warps [NG, nwarp) own 2 x 8 y
