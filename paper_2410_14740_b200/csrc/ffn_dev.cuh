@@ -687,7 +687,10 @@ __device__ __forceinline__ SmemPtrs carve(uint8_t *smem) {
 // balancing weight of one record, in 16-B units: bytes + lambda * 3d weights.  lambda = 6 B per
 // weight fits the per-CTA FFN times measured inside k_decode (profiles/: ~0.9 us of dequant +
 // FMA per record at any precision plus ~12 ns per KB), i.e. the split is close to per-record.
-constexpr int kLambda = 6;
+#ifndef M2C_FFN_LAMBDA
+#define M2C_FFN_LAMBDA 6
+#endif
+constexpr int kLambda = M2C_FFN_LAMBDA;
 static inline int ffn_weight(int64_t nb, int d) { return (int)((nb + (int64_t)kLambda * 3 * d) / 16); }
 static inline void fill_args(m2c_ctx *c, const LayerState &L, const m2c_tier_plan &p, FfnArgs &a) {
     const int d = c->desc.d_model;
