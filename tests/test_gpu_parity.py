@@ -592,3 +592,43 @@ def test_decode_layer_split_equals_fused(m2c, name, layers):
     assert ctxs[1].stats()["kernels_per_token"] == layers + 1  # L launches + the final residual
     for c in ctxs:
         c.close()
+
+
+def test_full_s7_stack_decode_replay_against_oracle(m2c):
+    """BASELINE configs[1] at full size in the launch configuration bench.py times (32 layers,
+    k_decode, CUDA graph): the token equals the per-layer C-ABI chain's, and at sampled layers
+    the chain's recorded layer inputs replayed through the oracle (D9) give the same tier lists
+    (bit-exact) and the same y within the tolerance."""
+    cfg = get_config("S7")
+    plan = m2c.plan_of(cfg)
+    L = cfg.n_layers
+    ctx = _ctx(m2c, cfg, plan, n_layers=L)
+    sample = {0: None, 13: None, L - 1: None}
+    for l in range(L):
+        w = layer_weights(cfg, l, device="cuda")
+        ctx.load_layer(l, w["w_gate"], w["w_up"], w["w_down_t"], w["pred_A"], w["pred_B"])
+        if l in sample:
+            sample[l] = _np(w)
+        del w
+    pn = _plan_np(plan)
+    xs = token_stream(cfg, 3, device="cuda")
+    for t in range(3):
+        x0 = xs[t].contiguous()
+        x = x0.clone()
+        ctx.decode_step(x, t + 1)  # k_decode, graph (the bench path)
+        xc = x0.clone()
+        for l in range(L):
+            sel = ctx.predict_rank(l, xc, rank_list=False, tier_of=False, scores=False)
+            _, y = ctx.sparse_ffn_forward(l, xc, sel["tier_ids"], want_partial=False)
+            if t == 0 and l in sample:
+                wn, xn = sample[l], xc.cpu().numpy()
+                ref = orc.select(orc.predict(xn, wn["pred_A"], wn["pred_B"])["s"], pn)
+                assert np.array_equal(sel["tier_ids"].cpu().numpy(), ref["tier_ids"]), l
+                recs = orc.records_for(wn, ref["tier_ids"], pn)
+                yhat = orc.ffn(cfg.d_model, pn, ref["tier_ids"], recs[16], recs[8], recs[4], xn)
+                assert d10(y.cpu().numpy(), yhat) <= TOL, l
+            xc = xc + y
+        torch.cuda.synchronize()
+        assert torch.equal(x, xc), t
+        assert ctx.stats()["kernels_per_token"] == 1
+    ctx.close()
