@@ -35,6 +35,9 @@ constexpr int kNBMax = 16;   // records per batch
 #define M2C_FFN_WS 0         // warp-specialised fast path (gate/up warps | down warps): measured
                              // slower at S7 (gate/up on half the warps is the longer chain)
 #endif
+#ifndef M2C_FFN_STREAM_PREFETCH
+#define M2C_FFN_STREAM_PREFETCH 0  // streaming path: L2 prefetch of the whole share up front (measured slower at S70H)
+#endif
 #ifndef M2C_FFN_FB_MUL
 #define M2C_FFN_FB_MUL 4     // fast-path batch = M2C_FFN_FB_MUL x (warps / quarter-units per record); 1 measured slower (tools/exp_fb.sh)
 #endif
@@ -445,15 +448,30 @@ __device__ __forceinline__ void ffn_loop(const FfnArgs &a, int d, int act, const
             issued++;
         }
     };
-    if (threadIdx.x == 0 && !fast) {
-        fence_proxy_async();
-        issue_more(0);
-    }
     // x -> smem as fp16 (read by the warp-local dot products)
     if (x)
         for (int c = threadIdx.x; c < nchunk; c += blockDim.x) xs[c] = reinterpret_cast<const uint4 *>(x)[c];
     __syncthreads();
     if (stamps && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(stamps[0]));
+    // streaming path: the first copies are issued after the barrier (a bulk-copy issue can stall
+    // its thread while the TMA unit is busy; the other warps are already waiting on the records'
+    // mbarriers, and each record's offset is published by its expect_tx arrival)
+    if (threadIdx.x == 0 && !fast) {
+        fence_proxy_async();
+        issue_more(0);
+    }
+#if M2C_FFN_STREAM_PREFETCH
+    // streaming path: the ring (192 KB) bounds the bytes in flight, so the share's later
+    // records are pulled into L2 now by warp 1 (per-line prefetches, no smem), and the ring's
+    // copies then hit L2
+    if (!fast && warp == 1) {
+        for (int j = 0; j < n_items; j++) {
+            const int t = j < c1 ? 0 : (j < c2 ? 1 : 2);
+            const char *g = reinterpret_cast<const char *>(src(j));
+            for (int o = 128 * lane; o < a.nb[t]; o += 128 * 32) asm volatile("prefetch.global.L2 [%0];" ::"l"(g + o));
+        }
+    }
+#endif
 
     if (fast && M2C_FFN_WS == 2) {
         // Pipelined (all records in flight): every warp first computes its gate/up units in
