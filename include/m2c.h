@@ -206,7 +206,8 @@ m2c_status m2c_set_fused(m2c_ctx *ctx, int32_t enable);
  * of layer l (k_decode: measured on the slowest CTA, barriers included in the phase they
  * end).  ffn_launches_out = FFN kernel launches per layer (0 for k_decode).
  * m2c_profile_stamps copies k_decode's raw stamps, uint64 ns [n_layers][G][M2C_DECODE_STAMPS]
- * (0 layer start, 1 scores done, 4 after barrier Bs, 2/3/16/10 select sub-steps (runs in smem,
+ * (0 layer start, 20/21/22 P2 sub-steps (h max, hq, scores), 1 scores + sorted run done,
+ * 4 after barrier Bs, 2/3/16/10 select sub-steps (runs in smem,
  * cut bins, candidates, exact cuts), 18/19/11 list sub-steps, 5 select done, 14/15 FFN
  * sub-steps, 6 FFN done, 7 after barrier By, 8 reduction + next h done, 9 kernel end,
  * 12/13 prologue start / end (layer 0); stamps not listed are unused and hold garbage);

@@ -348,12 +348,14 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
                 mh = max(mh, (unsigned long long)(v < 0 ? -v : v));
             }
             mh = block_max_u64(mh, red_u64);
+            STAMP(20);
             for (int i = tid; i < r; i += NT) {
                 const long long hv = i == tid ? hv0 : __ldcg(hcur + (int64_t)i * kHStride);
                 const int q = quant127_u64((unsigned long long)(hv < 0 ? -hv : hv), mh);
                 hq[i] = (int8_t)(hv < 0 ? -q : q);
             }
             __syncthreads();
+            STAMP(21);
             const int4 *hq4 = reinterpret_cast<const int4 *>(hq) + part * CPL;
             while (nb0 < n1) {
                 int acc = 0;
@@ -376,6 +378,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
                 nb0 += step;
                 if (nb0 < n1) load_b();
             }
+            STAMP(22);
             __syncthreads();  // keys[] complete
             // sorted run (key descending): rank by counting, four threads per key (a quarter of
             // the comparisons each, combined by shuffles within the aligned group of four)

@@ -68,7 +68,7 @@ print("P4 per-CTA us (mid layer): min %.2f median %.2f max %.2f argmax %d" % (
 G = rows[-1].shape[1]
 p4 = np.mean([(s[:, :, 6] - s[:, :, 5]) / 1e3 for s in rows], axis=(0, 1))  # per CTA
 print("P4 mean per CTA by sixths of the grid:", " ".join(f"{p4[i * G // 6:(i + 1) * G // 6].mean():.2f}" for i in range(6)))
-sub = {"P3 load": (4, 2), "P3 cutbins": (2, 3), "P3 cand": (3, 16), "P3 rank": (16, 10), "P3 walk": (10, 18), "P3 exscan": (18, 19), "P3 write": (19, 11), "P3 tail": (11, 5), "P4 setup": (5, 14), "P4 gate/up": (14, 15), "P4 down": (15, 6)}
+sub = {"P2 h+max": (0, 20), "P2 hq": (20, 21), "P2 dots": (21, 22), "P2 sort": (22, 1), "P3 load": (4, 2), "P3 cutbins": (2, 3), "P3 cand": (3, 16), "P3 rank": (16, 10), "P3 walk": (10, 18), "P3 exscan": (18, 19), "P3 write": (19, 11), "P3 tail": (11, 5), "P4 setup": (5, 14), "P4 gate/up": (14, 15), "P4 down": (15, 6)}
 for k, (i, j) in sub.items():
     v = np.mean([((s[:, :, j] - s[:, :, i]) / 1e3).mean() for s in rows])
     print(f"{k:12s} mean-CTA {v:.2f} us")
