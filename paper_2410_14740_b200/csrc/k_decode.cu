@@ -45,7 +45,7 @@ namespace {
 #define M2C_BAR_MODE 1
 #endif
 constexpr int kBins = 4096;
-constexpr int kHistW = kBins;  // fine bins (the 64 coarse sums follow them in smem only)
+constexpr int kHistW = kBins + 64;  // fine bins, then 64 coarse bins (CTA-aggregated atomics)
 // profiling stamps per (layer, CTA): 0 layer start, 1 P2 done, 4 after Bs, 2 runs in smem,
 // 3 cut bins found, 10 cuts exact,
 // 11 lists done, 5 P3 done, 6 P4 done, 7 after By, 8 R done, 9 kernel end (last layer),
@@ -249,6 +249,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
     __shared__ int red_i[32];
     __shared__ int cut_bin[3], cut_need[3], cut_V[3], cut_I[3], ncand[3], ccnt[3];
     __shared__ int xm[32], xsh[32];
+    __shared__ int ccoarse[64];
     __shared__ __align__(8) uint64_t sel_bar, at_bar;
     const SmemPtrs S = carve(smem);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -320,6 +321,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
         STAMP(0);
 
         // ================= P2: hq = Q(h), x -> smem, scores, histogram, sorted run ==========
+        for (int i = tid; i < 64; i += NT) ccoarse[i] = 0;  // (published after the scores' barrier below)
         const int shl = __ldcg(p.bin_sh + l);  // this token's histogram scale for layer l
         const int rps = (F_r + G - 1) / G;      // neurons per CTA (this CTA: ids [n0, n1))
         const int RP = rps | 1;  // run row length: odd, so same-index probes of 32 runs hit 32 banks
@@ -373,13 +375,17 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
                 if (part == 0 && n < n1) {
                     // run key: (s, local index asc) in one int -- |s| < 2^23 (R2), local < 255
                     keys[n - n0] = (int)(((unsigned)acc << 8) | (unsigned)(255 - (n - n0)));
-                    atomicAdd(&hist[bin_of(acc, shl)], 1);
+                    const int b = bin_of(acc, shl);
+                    atomicAdd(&hist[b], 1);
+                    atomicAdd(&ccoarse[b >> 6], 1);  // smem: this CTA's coarse counts
                 }
                 nb0 += step;
                 if (nb0 < n1) load_b();
             }
             STAMP(22);
-            __syncthreads();  // keys[] complete
+            __syncthreads();  // keys[] and the coarse counts complete
+            for (int i = tid; i < 64; i += NT)
+                if (ccoarse[i]) atomicAdd(&hist[kBins + i], ccoarse[i]);
             // sorted run (key descending): rank by counting, four threads per key (a quarter of
             // the comparisons each, combined by shuffles within the aligned group of four)
             const int nown = n1 - n0;
@@ -412,8 +418,8 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
             // the async-proxy copies
             asm volatile("fence.proxy.async;" ::: "memory");
             const uint32_t sb = (uint32_t)((4 * G * T + 15) & ~15);  // (the buffer has slack)
-            mbar_expect_tx(&sel_bar, (uint32_t)(4 * kBins) + sb);
-            bulk_g2s_plain(hs, hist, 4 * kBins, &sel_bar);
+            mbar_expect_tx(&sel_bar, (uint32_t)(4 * kHistW) + sb);
+            bulk_g2s_plain(hs, hist, 4 * kHistW, &sel_bar);
             bulk_g2s_plain(S.ring + kSbufOff, p.runs, sb, &sel_bar);
         }
         if (tid < 3) {
@@ -440,23 +446,6 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
             for (int i = tid; i < kHistW; i += NT) p.ghist[((l + 1) & 1) * kHistW + i] = 0;
         mbar_wait(&sel_bar, (uint32_t)(l & 1));
         STAMP(2);
-        // coarse sums of 64 bins (all loads first: independent chains)
-        if (NW == 16) {
-            int v[4];
-#pragma unroll
-            for (int j = 0; j < 4; j++) v[j] = hs[64 * (warp + 16 * j) + lane] + hs[64 * (warp + 16 * j) + 32 + lane];
-#pragma unroll
-            for (int j = 0; j < 4; j++) v[j] = __reduce_add_sync(0xffffffffu, v[j]);
-            if (lane == 0)
-#pragma unroll
-                for (int j = 0; j < 4; j++) hs[kBins + warp + 16 * j] = v[j];
-        } else {
-            for (int cidx = warp; cidx < 64; cidx += NW) {
-                const int v = __reduce_add_sync(0xffffffffu, hs[64 * cidx + lane] + hs[64 * cidx + 32 + lane]);
-                if (lane == 0) hs[kBins + cidx] = v;
-            }
-        }
-        __syncthreads();
         // Cut t (t = 0, 1, 2: the k16-th, (k16+k8)-th and k-th score in (score desc, id asc)
         // order, R3) is found by warp t: suffix scans of the 64 coarse then 64 fine histogram
         // bins locate the bin and the rank needed inside it.
@@ -788,7 +777,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
             // the histogram must be clear for the next launch, once every CTA has copied it
             grid_sync(p.bar_flags, base + ++nbar, p.err);
             if (cta == G - 1)
-                for (int i = tid; i < kBins; i += NT) hist[i] = 0;
+                for (int i = tid; i < kHistW; i += NT) hist[i] = 0;
             break;
         }
 
