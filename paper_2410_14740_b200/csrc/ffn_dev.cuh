@@ -38,6 +38,9 @@ constexpr int kNBMax = 16;   // records per batch
 #ifndef M2C_FFN_STREAM_PREFETCH
 #define M2C_FFN_STREAM_PREFETCH 0  // streaming path: L2 prefetch of the whole share up front (measured slower at S70H)
 #endif
+#ifndef M2C_FFN_STREAM_AHEAD
+#define M2C_FFN_STREAM_AHEAD 0  // streaming path: L2 prefetch distance in records (0: off)
+#endif
 #ifndef M2C_FFN_FB_MUL
 #define M2C_FFN_FB_MUL 4     // fast-path batch = M2C_FFN_FB_MUL x (warps / quarter-units per record); 1 measured slower (tools/exp_fb.sh)
 #endif
@@ -445,6 +448,15 @@ __device__ __forceinline__ void ffn_loop(const FfnArgs &a, int d, int act, const
             uint64_t *bar = &sm.bars[(jb + j) % kNSlot];
             mbar_expect_tx(bar, (uint32_t)sz);  // release: dsc[j] is visible to its waiters
             bulk_g2s(ring + off, src(j), (uint32_t)sz, bar, pol);
+#if M2C_FFN_STREAM_AHEAD
+            // the ring bounds the bytes in flight: pull the record M2C_FFN_STREAM_AHEAD places
+            // later into L2 now (in TMA order after this copy), so its copy will hit L2
+            if (j + M2C_FFN_STREAM_AHEAD < n_items) {
+                const int j2 = j + M2C_FFN_STREAM_AHEAD;
+                const int t2 = j2 < c1 ? 0 : (j2 < c2 ? 1 : 2);
+                prefetch_l2(src(j2), (uint32_t)a.nb[t2]);
+            }
+#endif
             issued++;
         }
     };
