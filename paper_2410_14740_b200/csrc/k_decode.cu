@@ -41,6 +41,9 @@
 namespace m2c {
 namespace {
 
+#ifndef M2C_CAND_WALK
+#define M2C_CAND_WALK 1  // candidates: one binary search + a walk over the bin's members (A/B: 662 vs 676 us)
+#endif
 #ifndef M2C_BAR_MODE
 #define M2C_BAR_MODE 1
 #endif
@@ -564,8 +567,14 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
                     }
                     return a;
                 };
+#if M2C_CAND_WALK
+                const int ib = count_ge((long long)lt * 256);  // v >= lt
+                int ia = ib;                                     // v > ht: the bin's members
+                while (ia > 0 && (runkey(c, ia - 1) >> 8) <= ht) ia--;  // are few: walk up
+#else
                 const int ia = count_ge(((long long)ht + 1) * 256);  // v > ht
                 const int ib = count_ge((long long)lt * 256);        // v >= lt
+#endif
                 pcum[4 * c + t] = ia;
                 for (int e = ia; e < ib; e++) {  // the bin's members (few)
                     const int key = runkey(c, e);
