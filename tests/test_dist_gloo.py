@@ -89,3 +89,54 @@ def test_shard_range_errors():
     assert shard_range(28672, 8, 7) == (25088, 28672)
     with pytest.raises(ValueError):
         shard_range(100, 3, 0)
+
+
+def _worker_global_topk(rank, world, port, out):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+    from oracle import oracle as orc
+    from paper_2410_14740_b200 import dist as m2c_dist
+    from synth import get_config, layer_input_stream, layer_weights
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        # NEXT-3's exchange: every rank's top-min(F_r, k) candidates by (score desc, global id
+        # asc), all-gathered, contain the global top-k -- the union of the ranks' parts of the
+        # global selection equals the unsharded selection (scores from the oracle's predictor)
+        cfg = get_config("T")
+        F = cfg.d_ff
+        lo, hi = m2c_dist.shard_range(F, world, rank)
+        w = {k: v.numpy() for k, v in layer_weights(cfg, 0, shard=(rank, world), parts=("A", "B")).items()}
+        gplan = orc.tier_plan(F, 30)
+        n = min(hi - lo, int(gplan[0]))
+        x = layer_input_stream(cfg, 0, 1).numpy()[0]
+        s = orc.predict(x, w["pred_A"], w["pred_B"])["s"]
+        cand = sorted(((int(s[i]), lo + i) for i in range(hi - lo)), key=lambda c: (-c[0], c[1]))[:n]
+        allc = [None] * world
+        dist.all_gather_object(allc, cand)
+        merged = sorted((c for lst in allc for c in lst), key=lambda c: (-c[0], c[1]))
+        k, k16, k8 = int(gplan[0]), int(gplan[1]), int(gplan[2])
+        mine = [[g for (_, g) in merged[a:b] if lo <= g < hi] for a, b in ((0, k16), (k16, k16 + k8), (k16 + k8, k))]
+        parts = [None] * world
+        dist.all_gather_object(parts, mine)
+        if rank == 0:
+            full = {kk: v.numpy() for kk, v in layer_weights(cfg, 0, parts=("A", "B")).items()}
+            ref = orc.select(orc.predict(x, full["pred_A"], full["pred_B"])["s"], gplan)["tier_ids"]
+            got = []
+            for t in range(3):
+                got += sorted(g for pr in parts for g in pr[t])
+            out["equal"] = got == ref.tolist()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_global_topk_exchange_gloo(world):
+    port = _free_port()
+    with mp.Manager() as m:
+        out = m.dict()
+        mp.spawn(_worker_global_topk, args=(world, port, out), nprocs=world, join=True)
+        assert out["equal"]
