@@ -175,6 +175,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--eager", action="store_true", help="no CUDA graph")
     ap.add_argument("--unfused", action="store_true", help="per-phase kernel chain instead of k_decode")
+    ap.add_argument("--split", action="store_true",
+                    help="force the layer-split k_decode (the sharded engine) even on one GPU")
     ap.add_argument("--global-topk", action="store_true",
                     help="NEXT-3: exact global top-k across the d_ff shards (P > 1)")
     ap.add_argument("--lookahead", action="store_true",
@@ -224,6 +226,8 @@ def main():
         ctx.set_graph(False)
     if args.unfused:
         ctx.set_fused(False)
+    if args.split:
+        ctx.set_fused(2)
     if args.lookahead and cfg.cache_mode != "resident":
         ctx.set_lookahead(True)
     if args.global_topk and P > 1:
@@ -275,6 +279,7 @@ def main():
 
     # ---- phase breakdown + dominant-kernel roofline ----
     fused = kpt == 1  # the persistent decode kernel k_decode is the whole token
+    split = kpt == cfg.n_layers + 1 and cfg.cache_mode == "resident"  # layer-split k_decode (sharded)
     ctx.profile(True)
     prof = [[0.0] * 4 for _ in range(cfg.n_layers)]
     nprof = min(K, 32)
@@ -288,7 +293,7 @@ def main():
                 prof[l][i] += p[l][i] / nprof
     ctx.profile(False)
     phase_ms = [sum(prof[l][i] for l in range(cfg.n_layers)) for i in range(4)]
-    if fused:
+    if fused or split:
         # k_decode launch durations, CUDA events on its own (compute) stream, after warm-up
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                for _ in range(nprof)]
@@ -303,6 +308,10 @@ def main():
         launch_ms = sum(a.elapsed_time(b) for a, b in evs) / nprof
         bytes_launch = ab["token"]
         kname = "k_decode (persistent: predictor + select + FFN + reduce, all layers)"
+        if split:  # one launch per layer; the token time / L also holds the all-reduces (conservative)
+            launch_ms /= cfg.n_layers
+            bytes_launch = ab["layer"]
+            kname = "k_decode (layer-split: one launch per layer, all-reduce between)"
     else:
         launch_ms = phase_ms[2] / (cfg.n_layers * n_ffn)
         bytes_launch = ab["ffn_per_launch"] / n_ffn
@@ -312,7 +321,7 @@ def main():
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             tr = json.load(f).get(cfg.name)
-        if tr and tr.get("kernel") == kname.split()[0]:
+        if tr and tr.get("kernel") == kname.split()[0] and not split:  # (per whole-token launch)
             traffic = tr["bytes_per_launch"]
     except Exception:
         pass
@@ -356,7 +365,8 @@ def main():
                        "parallelism": f"dff-shard{P}" if P > 1 else "single",
                        "topk": ("global" if args.global_topk else "shard-local") if P > 1 else "global",
                        "l2": "inputs larger than L2 (%.0f MB touched per token)" % (ab["token"] / 1e6),
-                       "graph": not args.eager, "persistent_kernel": fused},
+                       "graph": not args.eager, "persistent_kernel": fused,
+                       "engine": "k_decode" if fused else ("k_decode layer-split" if split else "kernel chain")},
             "hbm_gbs": gbs, "hbm_frac": gbs / peak,
             "roofline": {"kernel": kname, "bound": "hbm",
                          "achieved": achieved, "peak": peak, "peak_src": peak_src,
