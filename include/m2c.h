@@ -169,7 +169,10 @@ m2c_status m2c_sparse_ffn_forward(m2c_ctx *ctx, int32_t layer, const void *x,
 /* ---- multi-GPU (d_ff sharding, R13) ----------------------------------------------------
  * nccl_unique_id: 128 bytes from m2c_nccl_unique_id on rank 0, broadcast by the caller (the
  * torch process group is used for bootstrap only).  nccl_lib: path of libnccl.so.2 (dlopen'd;
- * NULL = default search).  Afterwards every layer all-reduces the fp32 partial sums once. */
+ * NULL = default search).  Afterwards every layer all-reduces the fp32 partial sums once
+ * (resident stacks: the layer-split k_decode, one launch per layer; LRU/ATU: the kernel
+ * chain).  nranks == 1 creates a one-rank communicator: the same engines run with identity
+ * collectives (the single-GPU test of the NCCL wiring). */
 m2c_status m2c_nccl_unique_id(const char *nccl_lib, void *id_out_128);
 m2c_status m2c_comm_init(m2c_ctx *ctx, int32_t nranks, int32_t rank, const void *nccl_unique_id,
                          const char *nccl_lib);

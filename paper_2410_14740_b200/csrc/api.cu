@@ -192,7 +192,7 @@ static cudaError_t enqueue_layer(m2c_ctx *c, int l, __half *x) {
         if ((e = launch_stage_fill(c, Ln, (l + 1) & 1, c->stage_stream))) return e;
         if ((e = cudaEventRecord(c->ev_staged[(l + 1) & 1], c->stage_stream))) return e;
     }
-    if (L.mode == 0 && c->nranks > 1 && c->global_topk) {
+    if (L.mode == 0 && c->comm && c->global_topk) {
         // NEXT-3: exact global top-k -- local candidates (top min(F_r, k) by (score desc,
         // global id asc)), an all-gather of the keys, the global cuts, this rank's share
         const m2c_tier_plan &g = c->gplan;
@@ -250,7 +250,7 @@ static cudaError_t enqueue_layer(m2c_ctx *c, int l, __half *x) {
         np = 2 * c->G;
     }
     if ((e = mark(c, l, 3))) return e;
-    if (c->nranks > 1) {
+    if (c->comm) {  // (a communicator makes the collectives run, even for one rank)
         if ((e = launch_reduce(c, np, c->ws.partial, x, c->ws.y32, nullptr, nullptr, nullptr, st)))
             return e;
         int r = c->nccl->allReduce(c->ws.y32, c->ws.y32, (size_t)c->desc.d_model, 7 /*f32*/,
@@ -266,7 +266,7 @@ static cudaError_t enqueue_layer(m2c_ctx *c, int l, __half *x) {
 // the persistent decode kernel covers a resident, unsharded stack whose scores fit in smem
 static bool decode_fused(const m2c_ctx *c) {
     const int rps = (c->F_r + c->G - 1) / c->G;  // a CTA's own neurons: one pass of its threads
-    if (!c->use_fused || c->nranks > 1 || c->F_r > decode_max_F() || rps > c->desc.d_model / 8 ||
+    if (!c->use_fused || c->comm || c->F_r > decode_max_F() || rps > c->desc.d_model / 8 ||
         rps > 4096)
         return false;
     for (const LayerState &L : c->layers)
@@ -277,7 +277,7 @@ static bool decode_fused(const m2c_ctx *c) {
 // the layer-split engine: k_decode one layer per launch, the d_ff shards' partial y summed by
 // one NCCL all-reduce between launches (the next launch adds it into x); resident stacks only
 static bool decode_split(const m2c_ctx *c) {
-    if (!c->use_fused || c->global_topk || (c->nranks < 2 && !c->force_split)) return false;
+    if (!c->use_fused || c->global_topk || (!c->comm && !c->force_split)) return false;
     const int rps = (c->F_r + c->G - 1) / c->G;
     if (c->F_r > decode_max_F() || rps > c->desc.d_model / 8 || rps > 4096) return false;
     for (const LayerState &L : c->layers)
@@ -296,7 +296,7 @@ static cudaError_t enqueue_token(m2c_ctx *c, __half *x) {
         cudaError_t e;
         for (int l = 0; l < c->desc.n_layers; l++) {
             if ((e = launch_decode(c, x, prof, c->compute, l, 1, l > 0 ? c->ws.y32 : nullptr, c->ws.y32))) return e;
-            if (c->nranks > 1 && c->nccl->allReduce(c->ws.y32, c->ws.y32, (size_t)c->desc.d_model, 7 /*f32*/,
+            if (c->comm && c->nccl->allReduce(c->ws.y32, c->ws.y32, (size_t)c->desc.d_model, 7 /*f32*/,
                                                     0 /*sum*/, c->comm, c->compute) != 0)
                 return cudaErrorUnknown;
         }
@@ -711,7 +711,7 @@ m2c_status m2c_sparse_ffn_forward(m2c_ctx *c, int32_t layer, const void *x, cons
                             c->ws.partial + (size_t)c->G * d, cs));
         np = 2 * c->G;
     }
-    if (c->nranks > 1) {
+    if (c->comm) {
         M2C_CUDA(launch_reduce(c, np, c->ws.partial, xh, c->ws.y32, nullptr, nullptr, nullptr, cs));
         if (y_partial)
             M2C_CUDA(cudaMemcpyAsync(y_partial, c->ws.y32, 4 * (size_t)d, cudaMemcpyDeviceToDevice, cs));
@@ -741,7 +741,8 @@ m2c_status m2c_comm_init(m2c_ctx *c, int32_t nranks, int32_t rank, const void *u
     if (!c || !uid) return fail(M2C_ERR_INVALID_ARG, "comm_init: null argument");
     if (nranks != c->desc.shard_count || rank != c->desc.shard_index)
         return fail(M2C_ERR_CONFIG, "comm_init: nranks/rank must equal shard_count/shard_index");
-    if (nranks == 1) return M2C_OK;
+    // (nranks == 1 is allowed: a one-rank communicator makes the sharded engines run their
+    // collectives as identities -- the single-GPU test of the NCCL wiring)
     NcclApi *api = load_nccl(lib);
     if (!api) return fail(M2C_ERR_NCCL, "cannot dlopen libnccl.so.2");
     ncclUniqueId id;

@@ -632,3 +632,40 @@ def test_full_s7_stack_decode_replay_against_oracle(m2c):
         assert torch.equal(x, xc), t
         assert ctx.stats()["kernels_per_token"] == 1
     ctx.close()
+
+
+@pytest.mark.parametrize("engine", ["split", "chain", "global"])
+def test_nccl_wiring_single_rank(m2c, engine):
+    """The collectives of the sharded engines (ncclAllReduce between layer launches / in the
+    chain, ncclAllGather of the global-top-k keys), captured in the decode graph, run for real
+    with a one-rank communicator (identity collectives) and leave every token bit-identical
+    to the unsharded whole-token kernel -- the NCCL plumbing a multi-GPU run uses."""
+    cfg = get_config("T")
+    L = 3
+    plan = m2c.plan_of(cfg)
+    ctxs = []
+    for with_comm in (False, True):
+        ctx = _ctx(m2c, cfg, plan, n_layers=L)
+        for l in range(L):
+            w = layer_weights(cfg, l, device="cuda")
+            ctx.load_layer(l, w["w_gate"], w["w_up"], w["w_down_t"], w["pred_A"], w["pred_B"])
+        if with_comm:
+            ctx.comm_init(1, 0, m2c.nccl_unique_id())
+            if engine == "chain":
+                ctx.set_fused(False)
+            elif engine == "global":
+                ctx.set_global_topk(plan)  # one rank: the global plan is the plan
+        ctxs.append(ctx)
+    xs = token_stream(cfg, 4, device="cuda")
+    for t in range(4):
+        outs = []
+        for ctx in ctxs:
+            x = xs[t].contiguous().clone()
+            ctx.decode_step(x, t + 1)
+            outs.append(x)
+        torch.cuda.synchronize()
+        assert torch.equal(outs[0], outs[1]), t
+    kpt = ctxs[1].stats()["kernels_per_token"]
+    assert kpt == (L + 1 if engine == "split" else kpt) and kpt > 1
+    for c in ctxs:
+        c.close()
