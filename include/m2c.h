@@ -177,6 +177,30 @@ m2c_status m2c_nccl_unique_id(const char *nccl_lib, void *id_out_128);
 m2c_status m2c_comm_init(m2c_ctx *ctx, int32_t nranks, int32_t rank, const void *nccl_unique_id,
                          const char *nccl_lib);
 
+/* ---- §8(e): the all-reduce fused into the whole-token kernel over peer memory -----------
+ * For a d_ff-sharded resident stack ("fused all-reduce inside the FFN kernel via
+ * NVLink P2P stores"), k_decode can exchange each layer's reduced y chunks itself instead of
+ * the layer-split engine's NCCL all-reduce: in its reduction phase the CTA owning a 32-wide
+ * chunk of d stores the chunk into every rank's exchange buffer (peer stores over NVLink) as
+ * 8-byte (round flag << 32 | f32) words, polls until the P words of each element in its own
+ * buffer carry this round's flag, and sums them in rank order 0..P-1 (so results equal a host
+ * emulation of the rank-order sum, not necessarily NCCL's order).  No fences, no counters, no
+ * cross-GPU barrier: only the P CTAs owning the same chunk meet.
+ *   m2c_p2p_buffer: allocates this rank's exchange buffer (device, zeroed; owned by the
+ *     context): [2][P][d] u64 | u32 rounds.  dev_ptr_out: its address; ipc_handle_out (64 B,
+ *     nullable): a cudaIpcMemHandle for other processes.
+ *   m2c_p2p_connect: dev_ptrs [P] (same process: device pointers the contexts' GPUs can
+ *     access) or ipc_handles [P][64] (other processes; opened here, closed by m2c_destroy).
+ *     nranks must equal shard_count (>= 2).  All ranks must run m2c_decode_step on the same
+ *     tokens with the same grid (m2c_set_grid) and be co-resident on their GPUs; a rank that
+ *     waits > 2 s for a peer sets error bit 16 and continues (wrong result, never a hang).
+ *   m2c_set_grid: CTAs of the context's kernels, 1..SM count (default: SM count).  Two ranks
+ *     sharing one GPU (the single-GPU test of this path) use half the SMs each. */
+m2c_status m2c_p2p_buffer(m2c_ctx *ctx, uint64_t *dev_ptr_out, void *ipc_handle_out);
+m2c_status m2c_p2p_connect(m2c_ctx *ctx, int32_t nranks, const uint64_t *dev_ptrs,
+                           const void *ipc_handles);
+m2c_status m2c_set_grid(m2c_ctx *ctx, int32_t ctas);
+
 /* ---- whole token (all layers), CUDA-graph captured ------------------------------------
  * x_inout: fp16 [d] device; on return (asynchronously) holds x_L where
  * x_{l+1} = fp16(x_l + fp16(y_l)) (R14).  step: strictly increasing (LRU timestamps). */

@@ -59,6 +59,9 @@ SIGNATURES = [
      [_vp, _i32, _vp, _vp, _vp, _vp, _P(TierPlan), _vp, _vp, _vp]),
     ("m2c_nccl_unique_id", C.c_int, [C.c_char_p, _vp]),
     ("m2c_comm_init", C.c_int, [_vp, _i32, _i32, _vp, C.c_char_p]),
+    ("m2c_p2p_buffer", C.c_int, [_vp, _P(C.c_uint64), _vp]),
+    ("m2c_p2p_connect", C.c_int, [_vp, _i32, _vp, _vp]),
+    ("m2c_set_grid", C.c_int, [_vp, _i32]),
     ("m2c_decode_step", C.c_int, [_vp, _vp, _i64]),
     ("m2c_decode_lists", C.c_int, [_vp, _i32, _vp]),
     ("m2c_set_graph", C.c_int, [_vp, _i32]),

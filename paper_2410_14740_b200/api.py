@@ -329,6 +329,25 @@ class M2CContext:
         check(lib().m2c_comm_init(self._h, nranks, rank, buf,
                                   path.encode() if path else None))
 
+    def set_grid(self, ctas: int):
+        """CTAs of this context's kernels (1..SM count)."""
+        check(lib().m2c_set_grid(self._h, int(ctas)))
+
+    def p2p_buffer(self):
+        """§8(e) exchange buffer: (device address, 64-byte cudaIpcMemHandle)."""
+        ptr = C.c_uint64()
+        h = C.create_string_buffer(64)
+        check(lib().m2c_p2p_buffer(self._h, C.byref(ptr), h))
+        return ptr.value, h.raw
+
+    def p2p_connect(self, dev_ptrs=None, ipc_handles=None):
+        """Connect the in-kernel all-reduce: every rank's buffer address (same process) or
+        IPC handle (one per process, this rank's own entry is ignored)."""
+        P = self.desc.shard_count
+        ptrs = (C.c_uint64 * P)(*dev_ptrs) if dev_ptrs is not None else None
+        hs = C.create_string_buffer(b"".join(ipc_handles), 64 * P) if ipc_handles is not None else None
+        check(lib().m2c_p2p_connect(self._h, P, ptrs, hs))
+
 
 def nccl_unique_id(nccl_lib=None) -> bytes:
     buf = C.create_string_buffer(128)

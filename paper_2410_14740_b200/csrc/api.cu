@@ -163,7 +163,7 @@ static cudaError_t enqueue_fill(m2c_ctx *c, int l, const m2c_tier_plan &p, int s
 // k_decode's P2/P3 (predictor + distributed exact select) fit: the same shape bounds
 static bool decode_select_ok(const m2c_ctx *c) {
     const int rps = (c->F_r + c->G - 1) / c->G;
-    return c->F_r <= decode_max_F() && rps <= c->desc.d_model / 8 && rps <= 4096;
+    return c->F_r <= decode_max_F() && rps <= c->desc.d_model / 8 && rps <= 254;
 }
 
 static cudaError_t enqueue_layer(m2c_ctx *c, int l, __half *x) {
@@ -266,8 +266,8 @@ static cudaError_t enqueue_layer(m2c_ctx *c, int l, __half *x) {
 // the persistent decode kernel covers a resident, unsharded stack whose scores fit in smem
 static bool decode_fused(const m2c_ctx *c) {
     const int rps = (c->F_r + c->G - 1) / c->G;  // a CTA's own neurons: one pass of its threads
-    if (!c->use_fused || c->comm || c->F_r > decode_max_F() || rps > c->desc.d_model / 8 ||
-        rps > 4096)
+    if (!c->use_fused || (c->comm && !c->p2p) || c->F_r > decode_max_F() ||
+        rps > c->desc.d_model / 8 || rps > 254)
         return false;
     for (const LayerState &L : c->layers)
         if (L.mode != 0) return false;
@@ -279,7 +279,7 @@ static bool decode_fused(const m2c_ctx *c) {
 static bool decode_split(const m2c_ctx *c) {
     if (!c->use_fused || c->global_topk || (!c->comm && !c->force_split)) return false;
     const int rps = (c->F_r + c->G - 1) / c->G;
-    if (c->F_r > decode_max_F() || rps > c->desc.d_model / 8 || rps > 4096) return false;
+    if (c->F_r > decode_max_F() || rps > c->desc.d_model / 8 || rps > 254) return false;
     for (const LayerState &L : c->layers)
         if (L.mode != 0) return false;
     return true;
@@ -428,7 +428,7 @@ m2c_status m2c_create(const m2c_model_desc *desc, int32_t device, m2c_stream_t c
                  o_dprof = take(8 * (size_t)kDecodeStamps * c->G * desc->n_layers),
                  o_binsh = take(4 * (size_t)desc->n_layers), o_sabs = take(8 * (size_t)c->G),
                  o_hb = take(8 * 2 * (size_t)kHStride * r),
-                 o_runs = take(4 * (size_t)c->G * (((F_r + c->G - 1) / c->G) | 1) + 16),
+                 o_runs = take(4 * ((size_t)F_r + 2 * (size_t)c->G) + 16),  // any grid <= G
                  o_dhist = take(decode_hist_bytes()),
                  o_prev = take(4 * (size_t)desc->n_layers * (plan->k > 0 ? plan->k : 1));
     // score histogram geometry: |s| <= 127^2 r, bins of 2^sh over [0, 2 smax] (4096 bins)
@@ -521,6 +521,9 @@ m2c_status m2c_destroy(m2c_ctx *c) {
         for (int p = 0; p < 2; p++) cudaEventDestroy(c->ev_staged[p]);
         cudaFree(c->stage_mem);
     }
+    for (void *p : c->p2p_opened) cudaIpcCloseMemHandle(p);
+    if (c->p2p_tabs) cudaFree(c->p2p_tabs);
+    if (c->p2p_mem) cudaFree(c->p2p_mem);
     if (c->ws_mem) cudaFree(c->ws_mem);
     delete c;
     return M2C_OK;
@@ -755,6 +758,73 @@ m2c_status m2c_comm_init(m2c_ctx *c, int32_t nranks, int32_t rank, const void *u
     c->comm = comm;
     c->nranks = nranks;
     c->rank = rank;
+    if (c->graph) {
+        cudaGraphExecDestroy(c->graph);
+        c->graph = nullptr;
+    }
+    return M2C_OK;
+}
+
+m2c_status m2c_set_grid(m2c_ctx *c, int32_t ctas) {
+    if (!c) return fail(M2C_ERR_INVALID_ARG, "null ctx");
+    if (ctas < 1 || ctas > c->num_sms) return fail(M2C_ERR_INVALID_ARG, "set_grid: 1 <= ctas <= SM count");
+    if (c->graph) {
+        cudaGraphExecDestroy(c->graph);
+        c->graph = nullptr;
+    }
+    c->G = ctas;
+    return M2C_OK;
+}
+
+// §8(e) exchange buffer of this rank: [2 (round parity)][P][d] u64 (flag << 32 | f32) | u32 rounds
+static size_t p2p_rounds_off(const m2c_ctx *c) { return 16 * (size_t)c->desc.shard_count * c->desc.d_model; }
+
+m2c_status m2c_p2p_buffer(m2c_ctx *c, uint64_t *dev_ptr_out, void *ipc_handle_out) {
+    if (!c || !dev_ptr_out) return fail(M2C_ERR_INVALID_ARG, "p2p_buffer: null argument");
+    if (c->desc.shard_count < 2) return fail(M2C_ERR_CONFIG, "p2p_buffer: needs shard_count >= 2");
+    M2C_CUDA(cudaSetDevice(c->device));
+    if (!c->p2p_mem) {
+        c->p2p_bytes = p2p_rounds_off(c) + 256;
+        M2C_CUDA(cudaMalloc(&c->p2p_mem, c->p2p_bytes));
+        M2C_CUDA(cudaMemset(c->p2p_mem, 0, c->p2p_bytes));  // flags and rounds start at 0
+        M2C_CUDA(cudaDeviceSynchronize());
+    }
+    *dev_ptr_out = (uint64_t)(uintptr_t)c->p2p_mem;
+    if (ipc_handle_out) {
+        cudaIpcMemHandle_t h;
+        M2C_CUDA(cudaIpcGetMemHandle(&h, c->p2p_mem));
+        memcpy(ipc_handle_out, &h, sizeof(h));
+    }
+    return M2C_OK;
+}
+
+m2c_status m2c_p2p_connect(m2c_ctx *c, int32_t nranks, const uint64_t *dev_ptrs, const void *ipc_handles) {
+    if (!c || (!dev_ptrs && !ipc_handles)) return fail(M2C_ERR_INVALID_ARG, "p2p_connect: null argument");
+    if (nranks != c->desc.shard_count || nranks < 2)
+        return fail(M2C_ERR_CONFIG, "p2p_connect: nranks must equal shard_count (>= 2)");
+    if (!c->p2p_mem) return fail(M2C_ERR_STATE, "p2p_connect: call m2c_p2p_buffer first");
+    if (c->p2p) return fail(M2C_ERR_STATE, "p2p_connect: already connected");
+    M2C_CUDA(cudaSetDevice(c->device));
+    std::vector<uint8_t *> base(nranks);
+    for (int q = 0; q < nranks; q++) {
+        if (q == c->desc.shard_index) {
+            base[q] = static_cast<uint8_t *>(c->p2p_mem);
+        } else if (ipc_handles) {
+            cudaIpcMemHandle_t h;
+            memcpy(&h, static_cast<const uint8_t *>(ipc_handles) + (size_t)q * sizeof(h), sizeof(h));
+            void *ptr = nullptr;
+            M2C_CUDA(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+            c->p2p_opened.push_back(ptr);
+            base[q] = static_cast<uint8_t *>(ptr);
+        } else {
+            base[q] = reinterpret_cast<uint8_t *>((uintptr_t)dev_ptrs[q]);
+        }
+    }
+    M2C_CUDA(cudaMalloc(&c->p2p_tabs, sizeof(void *) * nranks));
+    M2C_CUDA(cudaMemcpy(c->p2p_tabs, base.data(), sizeof(void *) * nranks, cudaMemcpyHostToDevice));
+    c->p2p_xtab = static_cast<unsigned long long *const *>(c->p2p_tabs);
+    c->p2p_rounds = reinterpret_cast<unsigned *>(base[c->desc.shard_index] + p2p_rounds_off(c));
+    c->p2p = true;
     if (c->graph) {
         cudaGraphExecDestroy(c->graph);
         c->graph = nullptr;
@@ -1094,6 +1164,7 @@ m2c_status m2c_stats(m2c_ctx *c, int64_t *kpt, int64_t hits[3], int64_t misses[3
         if (err & 1) m += " non-finite input x;";
         if (err & 4) m += " decode grid-barrier timeout;";
         if (err & 8) m += " decode select count mismatch;";
+        if (err & 16) m += " p2p exchange timeout (a peer rank is not running);";
         return fail(M2C_ERR_STATE, m);
     }
     return M2C_OK;

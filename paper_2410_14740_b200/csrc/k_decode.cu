@@ -95,11 +95,23 @@ struct DecArgs {
     const float *pre_y;         // [d] or null: the prologue first forms x = fp16(x + fp16(pre_y))
     float *post_y;              // [d] or null: R writes the reduced partial y here instead of x
     int select_only;            // 1: stop after P3 (one layer; the chain's cache + FFN follow)
+    // §8(e) fused all-reduce over peer memory (d_ff-sharded whole-token decode):
+    int nrank, rank;            // nrank > 1: the R phase exchanges the reduced y chunks
+    unsigned long long *const *xpeer;  // [nrank] every rank's exchange buffer [2][nrank][d] (flag|f32)
+    unsigned *rounds;           // this rank's count of completed exchanges (all layers, all tokens)
 };
 
 // histogram bin of a raw score: monotone, clamped; 2^sh-wide bins centred on 0
 __device__ __forceinline__ int bin_of(int s, int sh) { return min(max((s >> sh) + 2048, 0), 4095); }
 
+__device__ __forceinline__ void st_relaxed_sys_u64(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_sys_u64(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -279,6 +291,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
     }
     ffn_tables(sm, d);
     const unsigned base = ld_relaxed(p.bar_epoch);  // read by every CTA before its first arrival
+    const unsigned round0 = p.nrank > 1 ? ld_relaxed(p.rounds) : 0u;
     unsigned nbar = 0;
     unsigned jb = 0;  // mbarrier uses of this CTA so far
     // per-CTA globaltimer stamps (profiling): [l][cta][kStamps], see STAMP below
@@ -860,6 +873,36 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
                     float y = 0.f;
 #pragma unroll
                     for (int w = 0; w < 32; w++) y += rf[w][lane];
+                    if (p.nrank > 1) {
+                        // the all-reduce fused into the reduction: this chunk of this rank's y
+                        // goes straight into every rank's exchange buffer as (flag | value)
+                        // 8-byte words (peer stores over NVLink; the flag is the exchange round,
+                        // so a word is complete when its flag matches -- no fences, no
+                        // counters), then every lane polls its element of the P contributions
+                        // in this rank's buffer and sums them in rank order.  Only the CTAs
+                        // owning the same chunk on the P ranks meet: no cross-GPU barrier.
+                        const int P = p.nrank;
+                        const unsigned rnd = round0 + (unsigned)l, flag = rnd + 1u;
+                        const size_t row = (size_t)(rnd & 1u) * P;
+                        const unsigned long long v = ((unsigned long long)flag << 32) | __float_as_uint(y);
+                        for (int q = 0; q < P; q++) st_relaxed_sys_u64(p.xpeer[q] + (row + p.rank) * d + e, v);
+                        const unsigned long long *mine = p.xpeer[p.rank] + row * d + e;
+                        y = 0.f;
+                        for (int q = 0; q < P; q++) {
+                            unsigned long long w = ld_relaxed_sys_u64(mine + (size_t)q * d);
+                            if ((unsigned)(w >> 32) != flag) {
+                                const unsigned long long t0 = gtimer();
+                                do {
+                                    w = ld_relaxed_sys_u64(mine + (size_t)q * d);
+                                    if (gtimer() - t0 > 2000000000ull) {
+                                        atomicOr(p.err, 16u);
+                                        break;
+                                    }
+                                } while ((unsigned)(w >> 32) != flag);
+                            }
+                            y += __uint_as_float((unsigned)w);
+                        }
+                    }
                     const __half xn = __hadd(xs_h[e], __float2half_rn(y));
                     if (p.post_y) p.post_y[e] = y;  // split mode: this rank's y, to be all-reduced
                     else p.x[e] = xn;
@@ -886,7 +929,10 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
     }
     STAMP(9);
 #undef STAMP
-    if (cta == 0 && tid == 0) *p.bar_epoch = base + nbar;  // the next launch is stream-ordered
+    if (cta == 0 && tid == 0) {
+        *p.bar_epoch = base + nbar;  // the next launch is stream-ordered
+        if (p.nrank > 1) *p.rounds = round0 + (unsigned)p.n_layers;
+    }
 }
 
 }  // namespace
@@ -950,6 +996,10 @@ cudaError_t launch_decode(m2c_ctx *c, __half *x, unsigned long long *prof, cudaS
     a.ghist = c->dec_hist;
     a.lists = lists_out ? lists_out : c->prev_ids + (size_t)layer0 * (c->plan.k > 0 ? c->plan.k : 1);
     a.select_only = lists_out != nullptr;
+    a.nrank = (c->p2p && !lists_out && !post_y) ? c->desc.shard_count : 1;
+    a.rank = c->desc.shard_index;
+    a.xpeer = c->p2p_xtab;
+    a.rounds = c->p2p_rounds;
     a.partial = c->ws.partial;
     a.bar_flags = c->bar_flags;
     a.bar_epoch = c->bar_epoch;

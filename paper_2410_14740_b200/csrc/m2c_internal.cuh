@@ -140,6 +140,14 @@ struct m2c_ctx {
     m2c_tier_plan gplan{};
     long long *gkeys = nullptr;   // [n] own candidates | [P][n] gathered
     int32_t *gids = nullptr;      // [k_global] this rank's part of the global tier lists
+    // §8(e): in-kernel all-reduce over peer memory (m2c_p2p_*)
+    bool p2p = false;
+    void *p2p_mem = nullptr;          // this rank's exchange buffer [2][P][d] (flag|f32) u64 | rounds
+    size_t p2p_bytes = 0;
+    unsigned long long *const *p2p_xtab = nullptr;  // device [P] table
+    unsigned *p2p_rounds = nullptr;
+    void *p2p_tabs = nullptr;
+    std::vector<void *> p2p_opened;   // IPC-opened peer bases (closed at destroy)
     // multi-GPU
     m2c::NcclApi *nccl = nullptr;
     void *comm = nullptr;

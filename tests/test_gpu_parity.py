@@ -669,3 +669,52 @@ def test_nccl_wiring_single_rank(m2c, engine):
     assert kpt == (L + 1 if engine == "split" else kpt) and kpt > 1
     for c in ctxs:
         c.close()
+
+
+@pytest.mark.parametrize("name,layers", [("T", 3), ("S7", 4)])
+def test_p2p_fused_allreduce_two_ranks_one_gpu(m2c, name, layers):
+    """§8(e): two d_ff shards (ranks 0/1 of P = 2) share one GPU, 74 CTAs each, and run the
+    whole-token k_decode CONCURRENTLY on their own streams with the all-reduce fused into the
+    reduction phase over the exchange buffers (peer stores + system-scope counters; on one GPU
+    the 'peer' is the same HBM, the protocol is the one NVLink peers run).  Every token must
+    equal the host-orchestrated emulation: per layer, each rank's C-ABI chain (predict_rank ->
+    sparse_ffn_forward partial y, same grid), partials summed in rank order, x += fp16(sum)."""
+    from paper_2410_14740_b200._lib import lib
+    from paper_2410_14740_b200.api import check
+    cfg = get_config(name)
+    P = 2
+    plan = m2c.plan_of(cfg, P)
+    ctxs = []
+    for r in range(P):
+        ctx = _ctx(m2c, cfg, plan, n_layers=layers, shard=(r, P))
+        for l in range(layers):
+            w = layer_weights(cfg, l, device="cuda", shard=(r, P))
+            ctx.load_layer(l, w["w_gate"], w["w_up"], w["w_down_t"], w["pred_A"], w["pred_B"])
+        ctx.set_grid(74)
+        ctxs.append(ctx)
+    ptrs = [c.p2p_buffer()[0] for c in ctxs]
+    for c in ctxs:
+        c.p2p_connect(dev_ptrs=ptrs)
+    xs = token_stream(cfg, 5, device="cuda")
+    for t in range(5):
+        xr = [xs[t].contiguous().clone() for _ in range(P)]
+        torch.cuda.synchronize()
+        for c, x in zip(ctxs, xr):  # both ranks in flight at once (no stream dependency)
+            check(lib().m2c_decode_step(c._h, x.data_ptr(), t + 1))
+        torch.cuda.synchronize()
+        for c in ctxs:
+            assert c.stats()["kernels_per_token"] == 1  # raises on a p2p / barrier timeout
+        xc = xs[t].contiguous().clone()
+        for l in range(layers):
+            parts = []
+            for c in ctxs:
+                sel = c.predict_rank(l, xc, rank_list=False, tier_of=False, scores=False)
+                yp, _ = c.sparse_ffn_forward(l, xc, sel["tier_ids"], want_partial=True)
+                parts.append(yp)
+            ysum = parts[0] + parts[1]
+            xc = xc + ysum.half()
+        torch.cuda.synchronize()
+        assert torch.equal(xr[0], xr[1]), t
+        assert torch.equal(xr[0], xc), t
+    for c in ctxs:
+        c.close()
