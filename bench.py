@@ -179,6 +179,10 @@ def main():
                     help="force the layer-split k_decode (the sharded engine) even on one GPU")
     ap.add_argument("--global-topk", action="store_true",
                     help="NEXT-3: exact global top-k across the d_ff shards (P > 1)")
+    ap.add_argument("--allreduce", default="auto", choices=["auto", "p2p", "nccl"],
+                    help="P > 1 resident: the all-reduce fused into k_decode over peer memory (p2p, "
+                         "auto) or ncclAllReduce between per-layer launches (nccl); auto falls "
+                         "back to nccl if the peer exchange cannot be set up or times out")
     ap.add_argument("--lookahead", action="store_true",
                     help="NEXT-2: stage layer l+1's predicted misses during layer l (LRU/ATU configs)")
     args = ap.parse_args()
@@ -234,6 +238,21 @@ def main():
         from paper_2410_14740_b200 import tier_plan_make
         ctx.set_global_topk(tier_plan_make(cfg.d_ff, cfg.active_pct, cfg.a16, cfg.a8, cfg.den))
 
+    allreduce = "nccl" if P > 1 else None
+    if P > 1 and cfg.cache_mode == "resident" and args.allreduce != "nccl" and not (
+            args.split or args.unfused or args.global_topk):
+        try:
+            m2c_dist.p2p_init(ctx)
+            allreduce = "p2p"
+        except Exception as e:  # (auto) keep the NCCL engine
+            if args.allreduce == "p2p":
+                raise
+            print(f"[bench] p2p exchange unavailable ({e}); using NCCL", file=sys.stderr)
+            ctx.set_fused(2)
+    if world > 1:
+        dist.barrier()  # ranks enter the coupled decode together
+        torch.cuda.synchronize()
+
     W, K = args.warmup, args.steps
     if cfg.cache_mode != "resident":
         W = max(W, cfg.warmup_tokens)  # LRU warm-up
@@ -245,7 +264,26 @@ def main():
         x.copy_(toks[t])
         ctx.decode_step(x, step)
         step += 1
-    ctx.stats(reset=True)
+    try:
+        ctx.stats(reset=True)
+        ok = 1
+    except Exception as e:
+        if allreduce != "p2p" or args.allreduce == "p2p":
+            raise
+        print(f"[bench] p2p exchange failed in warm-up ({e})", file=sys.stderr)
+        ok = 0
+    if allreduce == "p2p":  # every rank switches together
+        okt = torch.tensor([ok], dtype=torch.int32, device=dev)
+        dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+        ok = int(okt.item())
+    if not ok:
+        allreduce = "nccl"
+        ctx.set_fused(2)
+        for t in range(3):
+            x.copy_(toks[t])
+            ctx.decode_step(x, step)
+            step += 1
+        ctx.stats(reset=True)
     if args.lookahead and cfg.cache_mode != "resident":
         ctx.lookahead_stats(reset=True)
 
@@ -366,7 +404,9 @@ def main():
                        "topk": ("global" if args.global_topk else "shard-local") if P > 1 else "global",
                        "l2": "inputs larger than L2 (%.0f MB touched per token)" % (ab["token"] / 1e6),
                        "graph": not args.eager, "persistent_kernel": fused,
-                       "engine": "k_decode" if fused else ("k_decode layer-split" if split else "kernel chain")},
+                       "engine": ("k_decode" + (" + fused p2p all-reduce" if allreduce == "p2p" else ""))
+                       if fused else ("k_decode layer-split" if split else "kernel chain"),
+                       **({"allreduce": allreduce} if P > 1 else {})},
             "hbm_gbs": gbs, "hbm_frac": gbs / peak,
             "roofline": {"kernel": kname, "bound": "hbm",
                          "achieved": achieved, "peak": peak, "peak_src": peak_src,

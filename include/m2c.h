@@ -193,7 +193,7 @@ m2c_status m2c_comm_init(m2c_ctx *ctx, int32_t nranks, int32_t rank, const void 
  *     access) or ipc_handles [P][64] (other processes; opened here, closed by m2c_destroy).
  *     nranks must equal shard_count (>= 2).  All ranks must run m2c_decode_step on the same
  *     tokens with the same grid (m2c_set_grid) and be co-resident on their GPUs; a rank that
- *     waits > 2 s for a peer sets error bit 16 and continues (wrong result, never a hang).
+ *     waits > 5 s for a peer sets error bit 16 and continues (wrong result, never a hang).
  *   m2c_set_grid: CTAs of the context's kernels, 1..SM count (default: SM count).  Two ranks
  *     sharing one GPU (the single-GPU test of this path) use half the SMs each. */
 m2c_status m2c_p2p_buffer(m2c_ctx *ctx, uint64_t *dev_ptr_out, void *ipc_handle_out);

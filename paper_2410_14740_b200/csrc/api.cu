@@ -862,6 +862,10 @@ m2c_status m2c_decode_step(m2c_ctx *c, void *x_inout, int64_t step) {
                 return fail(M2C_ERR_STATE, "decode_step: step must strictly increase");
         }
     }
+    if (c->p2p && !c->comm && !(decode_fused(c) && !c->force_split))
+        return fail(M2C_ERR_CONFIG, "decode_step: the p2p exchange runs only in the whole-token "
+                                    "kernel and this stack/grid does not fit it (no communicator "
+                                    "for the other engines)");
     cudaStream_t cs = c->compute;
     if (any_lru) {
         const int32_t st32 = (int32_t)step;  // pageable source: staged before return

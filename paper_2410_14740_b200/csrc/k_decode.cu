@@ -894,7 +894,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
                                 const unsigned long long t0 = gtimer();
                                 do {
                                     w = ld_relaxed_sys_u64(mine + (size_t)q * d);
-                                    if (gtimer() - t0 > 2000000000ull) {
+                                    if (gtimer() - t0 > 5000000000ull) {
                                         atomicOr(p.err, 16u);
                                         break;
                                     }

@@ -1,5 +1,5 @@
 """World-size-2 CPU (gloo) checks of the sharded path's host logic (R13):
-NCCL-id bootstrap broadcast, shard slicing, max-over-ranks timing, and the exchange step's
+NCCL-id bootstrap broadcast, the §8(e) IPC-handle exchange, shard slicing, max-over-ranks timing, and the exchange step's
 semantics -- the all-reduced sum of the ranks' oracle partials equals the oracle run on the
 union of the shard-local selections (the FFN output is a sum over independent neurons).
 """
@@ -40,6 +40,18 @@ def _worker(rank, world, port, out):
         assert all(i == uid for i in ids)
         # timing: max over ranks
         assert m2c_dist.max_over_ranks(float(rank + 1)) == float(world)
+        # §8(e) bootstrap: every rank connects to all exchange-buffer handles in rank order
+
+        class _Ctx:
+            def p2p_buffer(self):
+                return 0, bytes([rank + 1]) * 64
+
+            def p2p_connect(self, dev_ptrs=None, ipc_handles=None):
+                self.got = ipc_handles
+
+        fc = _Ctx()
+        m2c_dist.p2p_init(fc)
+        assert fc.got == [bytes([q + 1]) * 64 for q in range(world)]
         # the sharded layer through the oracle, partial sums all-reduced over gloo
         cfg = get_config("T")
         lo, hi = m2c_dist.shard_range(cfg.d_ff, world, rank)

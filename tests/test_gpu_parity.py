@@ -718,3 +718,84 @@ def test_p2p_fused_allreduce_two_ranks_one_gpu(m2c, name, layers):
         assert torch.equal(xr[0], xc), t
     for c in ctxs:
         c.close()
+
+
+def _ipc_worker(rank, world, port, out):
+    import os
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch
+    import torch.distributed as dist
+
+    import paper_2410_14740_b200 as m2c
+    from paper_2410_14740_b200 import dist as m2c_dist
+    from synth import get_config, layer_weights, token_stream
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cfg = get_config("T")
+        L = 3
+        ctx = _ctx(m2c, cfg, m2c.plan_of(cfg, world), n_layers=L, shard=(rank, world))
+        for l in range(L):
+            w = layer_weights(cfg, l, device="cuda", shard=(rank, world))
+            ctx.load_layer(l, w["w_gate"], w["w_up"], w["w_down_t"], w["pred_A"], w["pred_B"])
+        ctx.set_grid(32)
+        m2c_dist.p2p_init(ctx)  # CUDA IPC handles over the process group
+        xs = token_stream(cfg, 2, device="cuda")
+        res = []
+        for t in range(2):
+            x = xs[t].contiguous().clone()
+            dist.barrier()
+            ctx.decode_step(x, t + 1)
+            torch.cuda.synchronize()
+            assert ctx.stats()["kernels_per_token"] == 1  # the whole-token kernel ran
+            res.append(x.cpu().numpy().tobytes())
+        out[rank] = res
+        dist.barrier()
+        ctx.close()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_p2p_ipc_two_processes(m2c):
+    """§8(e) across processes: two ranks in two processes (one GPU here; on a node, one GPU
+    each) exchange their buffers' CUDA IPC handles over the process group (dist.p2p_init) and
+    decode with the in-kernel exchange; both end with the same token, equal to the in-process
+    two-rank emulation.  (Without MPS the two processes' kernels time-slice on one GPU, so the
+    grids are small and the exchange waits span context switches.)"""
+    import socket
+
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    with mp.Manager() as mgr:
+        out = mgr.dict()
+        mp.spawn(_ipc_worker, args=(2, port, out), nprocs=2, join=True)
+        res = dict(out)
+    cfg = get_config("T")
+    L, P = 3, 2
+    plan = m2c.plan_of(cfg, P)
+    ctxs = []
+    for r in range(P):
+        ctx = _ctx(m2c, cfg, plan, n_layers=L, shard=(r, P))
+        for l in range(L):
+            w = layer_weights(cfg, l, device="cuda", shard=(r, P))
+            ctx.load_layer(l, w["w_gate"], w["w_up"], w["w_down_t"], w["pred_A"], w["pred_B"])
+        ctx.set_grid(32)
+        ctxs.append(ctx)
+    xs = token_stream(cfg, 2, device="cuda")
+    for t in range(2):
+        xc = xs[t].contiguous().clone()
+        for l in range(L):
+            parts = []
+            for c in ctxs:
+                sel = c.predict_rank(l, xc, rank_list=False, tier_of=False, scores=False)
+                parts.append(c.sparse_ffn_forward(l, xc, sel["tier_ids"], want_partial=True)[0])
+            xc = xc + (parts[0] + parts[1]).half()
+        want = xc.cpu().numpy().tobytes()
+        assert res[0][t] == res[1][t] == want, t
+    for c in ctxs:
+        c.close()
