@@ -843,9 +843,8 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
             long long *hnext = p.hb + (int64_t)((l + 1) & 1) * r * kHStride;
             float(*rf)[33] = reinterpret_cast<float(*)[33]>(S.ring);
             const __half *xs_h = reinterpret_cast<const __half *>(S.xs);
-            for (int ch = cta; ch < nchunk; ch += G) {
-                const int e = ch * 32 + lane;
-                // the k_reduce order: virtual warp w sums rows w::32; two per pass, loads in flight
+            // the k_reduce order: virtual warp w sums rows w::32; two per pass, loads in flight
+            auto reduce_chunk = [&](int e) {
                 for (int w = warp; w < 32; w += 2 * NW) {
                     const int w2 = w + NW;
                     float v[10], u[10];
@@ -868,26 +867,46 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
                         rf[w2][lane] = acc2;
                     }
                 }
-                __syncthreads();
-                if (warp == 0) {
-                    float y = 0.f;
+            };
+            const int P = p.nrank;
+            const unsigned flag = round0 + (unsigned)l + 1u;
+            const size_t row = (size_t)((flag - 1u) & 1u) * P;
+            if (P > 1) {
+                // the all-reduce fused into the reduction (§6.9): first every owned chunk of this
+                // rank's y goes straight into every rank's exchange buffer as (flag | value)
+                // 8-byte words (peer stores over NVLink; the flag is the exchange round, so a
+                // word is complete when its flag matches -- no fences, no counters); the waits
+                // follow in the loop below, so the round trips of a CTA's chunks overlap.
+                for (int ch = cta; ch < nchunk; ch += G) {
+                    const int e = ch * 32 + lane;
+                    reduce_chunk(e);
+                    __syncthreads();
+                    if (warp == 0) {
+                        float y = 0.f;
 #pragma unroll
-                    for (int w = 0; w < 32; w++) y += rf[w][lane];
-                    if (p.nrank > 1) {
-                        // the all-reduce fused into the reduction: this chunk of this rank's y
-                        // goes straight into every rank's exchange buffer as (flag | value)
-                        // 8-byte words (peer stores over NVLink; the flag is the exchange round,
-                        // so a word is complete when its flag matches -- no fences, no
-                        // counters), then every lane polls its element of the P contributions
-                        // in this rank's buffer and sums them in rank order.  Only the CTAs
-                        // owning the same chunk on the P ranks meet: no cross-GPU barrier.
-                        const int P = p.nrank;
-                        const unsigned rnd = round0 + (unsigned)l, flag = rnd + 1u;
-                        const size_t row = (size_t)(rnd & 1u) * P;
+                        for (int w = 0; w < 32; w++) y += rf[w][lane];
                         const unsigned long long v = ((unsigned long long)flag << 32) | __float_as_uint(y);
                         for (int q = 0; q < P; q++) st_relaxed_sys_u64(p.xpeer[q] + (row + p.rank) * d + e, v);
+                    }
+                    __syncthreads();
+                }
+            }
+            for (int ch = cta; ch < nchunk; ch += G) {
+                const int e = ch * 32 + lane;
+                if (P == 1) {
+                    reduce_chunk(e);
+                    __syncthreads();
+                }
+                if (warp == 0) {
+                    float y = 0.f;
+                    if (P == 1) {
+#pragma unroll
+                        for (int w = 0; w < 32; w++) y += rf[w][lane];
+                    } else {
+                        // every lane polls its element's P words in this rank's buffer and sums
+                        // them in rank order.  Only the CTAs owning the same chunk on the P
+                        // ranks meet: no cross-GPU barrier.
                         const unsigned long long *mine = p.xpeer[p.rank] + row * d + e;
-                        y = 0.f;
                         for (int q = 0; q < P; q++) {
                             unsigned long long w = ld_relaxed_sys_u64(mine + (size_t)q * d);
                             if ((unsigned)(w >> 32) != flag) {

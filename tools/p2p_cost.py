@@ -1,11 +1,11 @@
-"""§8(e) cost of the all-reduce fused into k_decode, measured on ONE GPU: P = 2 d_ff shards of
-an L-layer stack share the GPU (74 CTAs each) and decode concurrently on their own streams.
-  alone      rank 0's shard decoded by itself at 74 CTAs, no exchange (the compute floor)
-  pair-none  both shards concurrently, no exchange (two independent half-GPU kernels)
-  pair-p2p   both shards concurrently with the in-kernel exchange (peer stores, counters)
-pair-p2p - pair-none is what the exchange adds per token (on one GPU the 'peer' is the same
+"""§8(e) cost of the all-reduce fused into k_decode, measured on ONE GPU: P d_ff shards of an
+L-layer stack share the GPU (148 / P CTAs each) and decode concurrently on their own streams.
+  alone     rank 0's shard decoded by itself at 148 / P CTAs, no exchange (the compute floor)
+  all-none  all shards concurrently, no exchange (P independent kernels)
+  all-p2p   all shards concurrently with the in-kernel exchange (flagged peer stores)
+all-p2p - all-none is what the exchange adds per token (on one GPU the 'peer' is the same
 HBM; across NVLink add the link latency, ~1-2 us per layer-chunk round trip).
-usage: python tools/p2p_cost.py [CONFIG] [LAYERS] [TOKENS]   (GPU; JSON lines)"""
+usage: python tools/p2p_cost.py [CONFIG] [LAYERS] [TOKENS] [P]   (GPU; JSON lines)"""
 import json
 import os
 import sys
@@ -22,7 +22,8 @@ name = sys.argv[1] if len(sys.argv) > 1 else "S7"
 cfg = get_config(name)
 L = int(sys.argv[2]) if len(sys.argv) > 2 else cfg.n_layers
 T = int(sys.argv[3]) if len(sys.argv) > 3 else 32
-P = 2
+P = int(sys.argv[4]) if len(sys.argv) > 4 else 2
+G = 148 // P
 plan = m2c.plan_of(cfg, P)
 
 
@@ -34,7 +35,7 @@ def make(p2p):
             w = layer_weights(cfg, l, device="cuda", shard=(r, P))
             ctx.load_layer(l, w["w_gate"], w["w_up"], w["w_down_t"], w["pred_A"], w["pred_B"])
             del w
-        ctx.set_grid(74)
+        ctx.set_grid(G)
         ctxs.append(ctx)
     if p2p:
         ptrs = [c.p2p_buffer()[0] for c in ctxs]
@@ -66,10 +67,11 @@ def run(ctxs, who):
     return e0.elapsed_time(e1) / T
 
 
-for label, p2p, who in (("alone", False, [0]), ("pair-none", False, [0, 1]), ("pair-p2p", True, [0, 1])):
+for label, p2p, who in (("alone", False, [0]), ("all-none", False, list(range(P))),
+                        ("all-p2p", True, list(range(P)))):
     ctxs = make(p2p)
     ms = run(ctxs, who)
-    print(json.dumps({"config": name, "layers": L, "P": P, "mode": label, "ms_per_token": ms,
+    print(json.dumps({"config": name, "layers": L, "P": P, "ctas_per_rank": G, "mode": label, "ms_per_token": ms,
                       "us_per_layer": ms * 1e3 / L, "note": "per-token wall incl. host sync"}),
           flush=True)
     for c in ctxs:

@@ -25,7 +25,7 @@ for P in Ps:
         del w
     xs = token_stream(cfg, 40, device="cuda")
     x = torch.empty(cfg.d_model, dtype=torch.float16, device="cuda")
-    for mode, name in ((2, "layer-split k_decode"), (0, "kernel chain")):
+    for mode, name in ((1, "whole-token k_decode"), (2, "layer-split k_decode"), (0, "kernel chain")):
         ctx.set_fused(mode)
         for t in range(8):
             x.copy_(xs[t])
