@@ -38,12 +38,25 @@ constexpr int kNBMax = 16;   // records per batch
 #ifndef M2C_FFN_STREAM_PREFETCH
 #define M2C_FFN_STREAM_PREFETCH 0  // streaming path: L2 prefetch of the whole share up front (measured slower at S70H)
 #endif
+#ifndef M2C_FFN_STREAM_DIV
+#define M2C_FFN_STREAM_DIV 0  // streaming path: batches of <= kRing / DIV bytes (0: ring - largest record)
+#endif
 #ifndef M2C_FFN_STREAM_AHEAD
 #define M2C_FFN_STREAM_AHEAD 0  // streaming path: L2 prefetch distance in records (0: off)
 #endif
 #ifndef M2C_FFN_FB_MUL
 #define M2C_FFN_FB_MUL 4     // fast-path batch = M2C_FFN_FB_MUL x (warps / quarter-units per record); 1 measured slower (tools/exp_fb.sh)
 #endif
+#ifndef M2C_FFN_PBIG
+#define M2C_FFN_PBIG 4       // max gate/up parts per record (8: d = 5120 / 8192 in 128-chunk parts -- measured neutral)
+#endif
+constexpr int kPMax = M2C_FFN_PBIG > 4 ? M2C_FFN_PBIG : 4;
+// gate/up units per record: d / P elements per warp
+// (128-chunk parts when d / 1024 <= kPMax: the 4-independent-chain path of gu_chunks)
+__device__ __forceinline__ int ffn_parts(int nchunk) {
+    if (nchunk % 128 == 0 && nchunk / 128 <= M2C_FFN_PBIG && nchunk >= 512) return nchunk / 128;
+    return nchunk >= 512 ? 4 : 1;
+}
 constexpr int kNSlot = 32;   // mbarriers (>= records in flight)
 constexpr int kRing = 192 * 1024;
 constexpr int kMaxLocal = 1024;  // records one CTA may own
@@ -291,11 +304,11 @@ struct FfnShared {
     uint64_t bars[kNSlot];
     uint64_t abar[kNSlot];   // warp-specialised path: record j's activation a_j is ready
     int acnt[kNSlot];        // quarter-units of record j done
-    float apart[kNSlot][4][2];
+    float apart[kNSlot][kPMax][2];
     int span[kNSlot];
-    float part[kNBMax][4][2];
+    float part[kNBMax][kPMax][2];
     float a_sm[kNSlot];
-    int cb[5][5];        // chunk bounds: cb[P][p] = nchunk * p / P
+    int cb[kPMax + 1][kPMax + 1];  // chunk bounds: cb[P][p] = nchunk * p / P
     int rng[8];          // CTA ranges (6)
     int nbatch;
     int scan[96];
@@ -358,8 +371,8 @@ __device__ __forceinline__ void down_c(const uint8_t *rec, int d, float a, int c
 // table: chunk bounds per split into P parts (constant for a launch)
 __device__ __forceinline__ void ffn_tables(FfnShared &sm, int d) {
     const int nchunk = d / 8;
-    if (threadIdx.x < 25) {
-        const int P = threadIdx.x / 5, p = threadIdx.x % 5;
+    if (threadIdx.x < (kPMax + 1) * (kPMax + 1)) {
+        const int P = threadIdx.x / (kPMax + 1), p = threadIdx.x % (kPMax + 1);
         sm.cb[P][p] = P ? nchunk * p / P : 0;
     }
 }
@@ -405,7 +418,7 @@ __device__ __forceinline__ void ffn_loop(const FfnArgs &a, int d, int act, const
             }
             // batches of one record per warp (P quarter-units each): the down-projection of a
             // batch overlaps the arrival of the next batch's records
-            const int FB = max(1, min(kNBMax, (nwarp / (nchunk >= 512 ? 4 : 1)) * M2C_FFN_FB_MUL));
+            const int FB = max(1, min(kNBMax, (nwarp / ffn_parts(nchunk)) * M2C_FFN_FB_MUL));
             const int nbt = (n_items + FB - 1) / FB;
             if (j == 0) sm.nbatch = nbt;
             if (j <= nbt) bst[j] = min(j * FB, n_items);
@@ -420,7 +433,12 @@ __device__ __forceinline__ void ffn_loop(const FfnArgs &a, int d, int act, const
             while (nb < kNBMax && j0 + nb < n_items) {
                 const int j = j0 + nb;
                 const int sz = j < c1 ? nbA : (j < c2 ? nbB : nbC);
+#if M2C_FFN_STREAM_DIV
+                // smaller batches: the next batch's copies land while this one computes
+                if (nb > 0 && bytes + sz > kRing / M2C_FFN_STREAM_DIV) break;
+#else
                 if (nb > 0 && bytes + sz + mx > kRing) break;
+#endif
                 bytes += sz;
                 nb++;
             }
@@ -493,7 +511,7 @@ __device__ __forceinline__ void ffn_loop(const FfnArgs &a, int d, int act, const
         // for each a_j -- no block-wide barrier between the two, so the down-projection of
         // the early records overlaps the gate/up of the late ones.  Per element the
         // operations and their order are those of the batched path (bit-identical).
-        const int P = nchunk >= 512 ? 4 : 1;
+        const int P = ffn_parts(nchunk);
         if (threadIdx.x < kNSlot) sm.acnt[threadIdx.x] = 0;
         __syncthreads();
         for (int u = warp; u < n_items * P; u += nwarp) {
@@ -569,7 +587,7 @@ __device__ __forceinline__ void ffn_loop(const FfnArgs &a, int d, int act, const
         // elements per thread and accumulate the down-projection record by record as each
         // a_j becomes ready -- the down-projection overlaps the arrival of later records.
         // Per element the operations and their order are those of the batched path.
-        const int P = nchunk >= 512 ? 4 : 1;
+        const int P = ffn_parts(nchunk);
         const int NG = nwarp / 2;
         if (threadIdx.x < kNSlot) sm.acnt[threadIdx.x] = 0;
         __syncthreads();
@@ -635,13 +653,13 @@ __device__ __forceinline__ void ffn_loop(const FfnArgs &a, int d, int act, const
 #pragma unroll
     for (int i = 0; i < 8; i++) y[i] = 0.f;
     const int nbt = sm.nbatch;
-    const int P = nchunk >= 512 ? 4 : 1;
+    const int P = ffn_parts(nchunk);
     for (int bi = 0; bi < nbt; bi++) {
         const int j0 = bst[bi], nb = bst[bi + 1] - j0;
         // gate/up: units (record b, quarter p) dealt round-robin to the warps (a warp may take
         // several); each unit ends in a warp-shuffle reduction, quarters combine in order
         for (int u = warp; u < nb * P; u += nwarp) {
-            const int b = P == 4 ? (u >> 2) : u, pp = P == 4 ? (u & 3) : 0;
+            const int b = u / P, pp = u - b * P;
             const int j = j0 + b;
             mbar_wait(&sm.bars[(jb + j) % kNSlot], (uint32_t)(((jb + j) / kNSlot) & 1));
             const int ds = dsc[j];
