@@ -41,6 +41,9 @@ constexpr int kNBMax = 16;   // records per batch
 #ifndef M2C_FFN_STREAM_DIV
 #define M2C_FFN_STREAM_DIV 0  // streaming path: batches of <= kRing / DIV bytes (0: ring - largest record)
 #endif
+#ifndef M2C_FFN_STREAM_PIPE
+#define M2C_FFN_STREAM_PIPE 0  // streaming path: 1 = records released one by one as consumed (bit-identical, measured slower)
+#endif
 #ifndef M2C_FFN_STREAM_AHEAD
 #define M2C_FFN_STREAM_AHEAD 0  // streaming path: L2 prefetch distance in records (0: off)
 #endif
@@ -304,6 +307,9 @@ struct FfnShared {
     uint64_t bars[kNSlot];
     uint64_t abar[kNSlot];   // warp-specialised path: record j's activation a_j is ready
     int acnt[kNSlot];        // quarter-units of record j done
+    int cons[kNSlot];        // streaming pipeline: warps done with record j's down-projection
+    unsigned aflag[kNSlot];  // streaming pipeline: tag (jb + j + 1) once a_sm[slot] holds a_j
+    int issued;              // streaming pipeline: records issued so far (thread 0 publishes)
     float apart[kNSlot][kPMax][2];
     int span[kNSlot];
     float part[kNBMax][kPMax][2];
@@ -317,6 +323,7 @@ struct FfnShared {
 
 __device__ __forceinline__ void ffn_init_bars(FfnShared &sm) {  // thread 0, before any use
     for (int i = 0; i < kNSlot; i++) {
+        sm.aflag[i] = 0xffffffffu;
         mbar_init(&sm.bars[i], 1);
         mbar_init(&sm.abar[i], 1);
     }
@@ -477,7 +484,17 @@ __device__ __forceinline__ void ffn_loop(const FfnArgs &a, int d, int act, const
 #endif
             issued++;
         }
+#if M2C_FFN_STREAM_PIPE
+        *reinterpret_cast<volatile int *>(&sm.issued) = issued;
+#endif
     };
+#if M2C_FFN_STREAM_PIPE
+    if (!fast && threadIdx.x < kNSlot) {
+        sm.cons[threadIdx.x] = 0;
+        sm.acnt[threadIdx.x] = 0;
+        if (threadIdx.x == 0) sm.issued = 0;
+    }
+#endif
     // x -> smem as fp16 (read by the warp-local dot products)
     if (x)
         for (int c = threadIdx.x; c < nchunk; c += blockDim.x) xs[c] = reinterpret_cast<const uint4 *>(x)[c];
@@ -503,6 +520,111 @@ __device__ __forceinline__ void ffn_loop(const FfnArgs &a, int d, int act, const
     }
 #endif
 
+#if M2C_FFN_STREAM_PIPE
+    if (!fast) {
+        // Streaming pipeline (the share exceeds the ring): ring space is released record by
+        // record, in order, as soon as every warp has done its down-projection of it, so the
+        // copies of later records stream in continuously instead of batch by batch.  Each warp
+        // computes its gate/up units (record j, part pp dealt round-robin) of every ISSUED
+        // record as the copies land; the last part of a record combines the parts in a fixed
+        // order and publishes a_j (tag aflag); every warp then accumulates the down-projection
+        // of its 8 y elements per thread record by record in ascending j.  Per element the
+        // operations and their order are the batched path's (bit-identical).  Thread 0 is also
+        // the producer: whenever it would wait it frees consumed records and issues more, so no
+        // wait can block the copies it depends on.
+        const int P = ffn_parts(nchunk);
+        int freed = 0;
+        auto produce = [&]() {  // thread 0 only
+            bool any = false;
+            while (freed < issued &&
+                   *reinterpret_cast<volatile int *>(&sm.cons[(jb + freed) % kNSlot]) == nwarp) {
+                sm.cons[(jb + freed) % kNSlot] = 0;
+                used -= sm.span[(jb + freed) % kNSlot];
+                freed++;
+                any = true;
+            }
+            if (any) {
+                fence_proxy_async();  // the consumers' generic ring reads precede the new copies
+                issue_more(freed);
+            }
+        };
+        const bool prod = threadIdx.x == 0;
+        auto wait_bar = [&](uint64_t *bar, uint32_t par) {
+            if (prod) {
+                while (!mbar_test(bar, par)) produce();
+            } else {
+                mbar_wait(bar, par);
+            }
+        };
+        float y[8];
+#pragma unroll
+        for (int i = 0; i < 8; i++) y[i] = 0.f;
+        int u = warp;  // this warp's next gate/up unit: record u / P, part u % P
+        for (int j = 0; j < n_items; j++) {
+            // gate/up units of every issued record (and at least of record j)
+            for (;;) {
+                if (u >= n_items * P) break;
+                const int jj = u / P, pp = u - jj * P;
+                if (jj > j) {  // (one read for the whole warp: the decision must be uniform)
+                    const int is = __shfl_sync(0xffffffffu, *reinterpret_cast<volatile int *>(&sm.issued), 0);
+                    if (jj >= is) break;
+                } else {
+                    while (jj >= *reinterpret_cast<volatile int *>(&sm.issued))
+                        if (prod) produce();
+                }
+                const unsigned sl = (jb + jj) % kNSlot;
+                wait_bar(&sm.bars[sl], ((jb + jj) / kNSlot) & 1);
+                const int ds = dsc[jj];
+                float pg, pu;
+                gu_any(ds >> 24, ring + (ds & 0xffffff), xs, d, sm.cb[P][pp], sm.cb[P][pp + 1], pg, pu);
+                pg = warp_sum_f(pg);
+                pu = warp_sum_f(pu);
+                if (lane == 0) {
+                    sm.apart[sl][pp][0] = pg;
+                    sm.apart[sl][pp][1] = pu;
+                    __threadfence_block();
+                    if (atomicAdd(&sm.acnt[sl], 1) == P - 1) {  // last part: combine, publish
+                        __threadfence_block();
+                        float g = 0.f, uu = 0.f;
+                        for (int q = 0; q < P; q++) {
+                            g += sm.apart[sl][q][0];
+                            uu += sm.apart[sl][q][1];
+                        }
+                        sm.acnt[sl] = 0;
+                        sm.a_sm[sl] = (act == 1) ? fmaxf(g, 0.f) * uu : g / (1.f + expf(-g)) * uu;
+                        __threadfence_block();
+                        *reinterpret_cast<volatile unsigned *>(&sm.aflag[sl]) = jb + (unsigned)jj + 1u;
+                    }
+                }
+                __syncwarp();
+                u += nwarp;
+            }
+            // down-projection of record j (ascending j: the batched path's order)
+            const unsigned sl = (jb + j) % kNSlot, tag = jb + (unsigned)j + 1u;
+            while (*reinterpret_cast<volatile unsigned *>(&sm.aflag[sl]) != tag)
+                if (prod) produce();
+            __threadfence_block();
+            const int ds = dsc[j];
+            const float aj = *reinterpret_cast<volatile float *>(&sm.a_sm[sl]);
+            const int tier = ds >> 24;
+            if (tier == 0) down_t<0>(ring + (ds & 0xffffff), d, aj, y);
+            else if (tier == 1) down_t<1>(ring + (ds & 0xffffff), d, aj, y);
+            else down_t<2>(ring + (ds & 0xffffff), d, aj, y);
+            __syncwarp();
+            if (lane == 0) {
+                __threadfence_block();
+                atomicAdd(&sm.cons[sl], 1);
+            }
+            if (prod) produce();
+        }
+        if (stamps && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(stamps[1]));
+        float *out = partial + (int64_t)blockIdx.x * d + 8 * threadIdx.x;
+        reinterpret_cast<float4 *>(out)[0] = make_float4(y[0], y[1], y[2], y[3]);
+        reinterpret_cast<float4 *>(out)[1] = make_float4(y[4], y[5], y[6], y[7]);
+        __syncthreads();  // the ring's records are consumed
+        return;
+    }
+#endif
     if (fast && M2C_FFN_WS == 2) {
         // Pipelined (all records in flight): every warp first computes its gate/up units in
         // record order as the copies land (the unit that completes record j combines its
