@@ -110,9 +110,10 @@ def algorithmic_bytes(cfg, plan, P):
             "token": cfg.n_layers * (rec + r * d + F_r * r + 2 * d)}
 
 
-def oracle_sample(cfg, P, layers, tokens, device_weights=None):
-    """Time the CPU oracle (as it stands, 1 thread) on a bounded sample: `tokens` tokens through
-    `layers` layers of the workload; returns seconds per (token, layer) and the sample string."""
+def oracle_sample(cfg, P, layers, tokens, device_weights=None, threads=1):
+    """Time the CPU oracle (as it stands, 1 thread; threads > 1: its bit-identical OpenMP variant,
+    SURVEY 8(d)) on a bounded sample: `tokens` tokens through `layers` layers of the workload;
+    returns seconds per (token, layer) and the sample string."""
     import numpy as np
     from oracle import oracle as orc
     from synth import layer_weights, token_stream
@@ -134,11 +135,15 @@ def oracle_sample(cfg, P, layers, tokens, device_weights=None):
                 recs[b][i] = orc.pack(b, w["w_gate"], w["w_up"], w["w_down_t"], int(i), int(i) + 1)[0]
         for x in xs:
             t0 = time.perf_counter()
-            orc.layer_forward(w, recs, x, plan, act=0 if cfg.act == "silu" else 1)
+            if threads > 1:
+                orc.layer_forward_mt(w, recs, x, plan, threads, act=0 if cfg.act == "silu" else 1)
+            else:
+                orc.layer_forward(w, recs, x, plan, act=0 if cfg.act == "silu" else 1)
             total += time.perf_counter() - t0
             n += 1
     return total / n, f"{tokens} tokens x {layers} layers of the {cfg.name} workload (shard 0/{P}), " \
-                      f"1 thread, oracle pack untimed; scaled x{cfg.n_layers} layers per token"
+                      f"{threads} thread{'s' if threads > 1 else ''}, oracle pack untimed; " \
+                      f"scaled x{cfg.n_layers} layers per token"
 
 
 def run_reference(args, world, rank):
@@ -383,11 +388,42 @@ def main():
         e2e = {"value": K / el, "unit": "tokens/s", "h2d_bytes_per_step": 2 * cfg.d_model,
                "d2h_bytes_per_step": 2 * cfg.d_model}
 
+    h2d_peak = None
+    if cfg.cache_mode != "resident":
+        hb = torch.empty(256 << 20, dtype=torch.uint8).pin_memory()
+        db = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+        db.copy_(hb, non_blocking=True)
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c0.record()
+        for _ in range(4):
+            db.copy_(hb, non_blocking=True)
+        c1.record()
+        torch.cuda.synchronize()
+        h2d_peak = 4 * (256 << 20) / (c0.elapsed_time(c1) * 1e-3) / 1e9
+        del hb, db
+    ar_us = None
+    if world > 1:
+        yb = torch.zeros(cfg.d_model, dtype=torch.float32, device=dev)
+        for _ in range(10):
+            dist.all_reduce(yb)
+        torch.cuda.synchronize()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record()
+        for _ in range(100):
+            dist.all_reduce(yb)
+        a1.record()
+        torch.cuda.synchronize()
+        ar_us = m2c_dist.max_over_ranks(a0.elapsed_time(a1) * 10.0, dev)  # ms/100 -> us
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         per, sample = oracle_sample(cfg, P, 1, 12)
         cpu = {"value": 1.0 / (per * cfg.n_layers), "unit": "tokens/s", "cores": 1,
                "kind": "oracle", "sample": sample}
+        nthr = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+        if nthr and nthr > 1:  # also the oracle's OpenMP variant on all host cores
+            per_mt, sample_mt = oracle_sample(cfg, P, 1, 12, threads=nthr)
+            cpu["all_cores"] = {"value": 1.0 / (per_mt * cfg.n_layers), "cores": nthr,
+                                "sample": sample_mt}
 
     if rank == 0:
         hits, miss = st["hits"], st["misses"]
@@ -424,6 +460,17 @@ def main():
             line["cache"] = {"hits": hits, "misses": miss, "lookahead": bool(args.lookahead),
                              "staged_fills": staged,
                              "hit_ratio": [h / max(1, h + m) for h, m in zip(hits, miss)]}
+            # the H2D link bounds this config -- miss-fill bytes against the
+            # box's pinned H2D peak, measured in the same run
+            from paper_2410_14740_b200 import record_bytes
+            fill_b = sum(m * record_bytes(b, cfg.d_model) for m, b in zip(miss, (16, 8, 4))) / K
+            line["pcie"] = {"h2d_peak_gbs": h2d_peak, "fill_bytes_per_token": fill_b,
+                            "fill_gbs_whole_token": fill_b * tok_s / 1e9,
+                            "frac_of_h2d_peak": fill_b * tok_s / 1e9 / h2d_peak,
+                            "note": "fill GB/s averaged over the whole token time (fills also "
+                                    "overlap the hit FFN); peak = 256 MiB pinned cudaMemcpyAsync"}
+        if world > 1:
+            line["allreduce_32k_us"] = ar_us  # ncclAllReduce of fp32[d] alone
         print(json.dumps(line), flush=True)
     ctx.close()
     if world > 1:

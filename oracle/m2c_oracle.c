@@ -363,6 +363,85 @@ int orc_ffn(int d, const int32_t plan[4], const int32_t *tier_ids, const uint8_t
     return ORC_OK;
 }
 
+/* ------------------------------------------------------------------------- */
+/* SURVEY 8(d) "oracle timing: an OpenMP variant over neurons on all host      */
+/* cores".  The same O2/O4 and O6 arithmetic in the same order per output:    */
+/* integer dot products split over rows; a_n split over neurons; yhat_j split */
+/* over j with the neuron sum in the serial order -- bit-identical to          */
+/* orc_predict / orc_ffn (pinned by tests/test_oracle_ffn.py).  Timing only.   */
+/* ------------------------------------------------------------------------- */
+int orc_predict_mt(int d, int r, int F_r, const uint16_t *x, const int8_t *A, const int8_t *B,
+                   int64_t *h, int8_t *hq, int32_t *s, int nthreads)
+{
+    if (d <= 0 || r <= 0 || F_r < 0 || d > 8192 || nthreads < 1) return ORC_EINVAL;
+    int64_t *X = (int64_t *)malloc(sizeof(int64_t) * (size_t)d);
+    for (int j = 0; j < d; j++) {
+        double v = orc_half_to_double(x[j]);
+        if (!isfinite(v)) { free(X); return ORC_EINVAL; }
+        X[j] = (int64_t)ldexp(v, 24);
+    }
+#pragma omp parallel for num_threads(nthreads) schedule(static)
+    for (int i = 0; i < r; i++) {
+        int64_t acc = 0;
+        for (int j = 0; j < d; j++) acc += (int64_t)A[(size_t)i * d + j] * X[j];
+        h[i] = acc;
+    }
+    free(X);
+    int64_t Mh = 0;
+    for (int i = 0; i < r; i++) {
+        int64_t a = h[i] < 0 ? -h[i] : h[i];
+        if (a > Mh) Mh = a;
+    }
+    for (int i = 0; i < r; i++) hq[i] = quant_sym_127(h[i], Mh);
+#pragma omp parallel for num_threads(nthreads) schedule(static)
+    for (int n = 0; n < F_r; n++) {
+        int64_t acc = 0;
+        for (int i = 0; i < r; i++) acc += (int64_t)B[(size_t)n * r + i] * hq[i];
+        s[n] = (int32_t)acc;
+    }
+    return ORC_OK;
+}
+
+int orc_ffn_mt(int d, const int32_t plan[4], const int32_t *tier_ids, const uint8_t *rec16,
+               const uint8_t *rec8, const uint8_t *rec4, const uint16_t *x, int act, double *yhat,
+               int nthreads)
+{
+    if (nthreads < 1) return ORC_EINVAL;
+    const uint8_t *recs[3] = {rec16, rec8, rec4};
+    const int bits[3] = {16, 8, 4};
+    const int k = plan[1] + plan[2] + plan[3];
+    double *xd = (double *)malloc(sizeof(double) * (size_t)d);
+    double *a = (double *)malloc(sizeof(double) * (size_t)(k > 0 ? k : 1));
+    double *wdall = (double *)malloc(sizeof(double) * (size_t)(k > 0 ? k : 1) * d);
+    for (int j = 0; j < d; j++) xd[j] = orc_half_to_double(x[j]);
+#pragma omp parallel num_threads(nthreads)
+    {
+        double *wg = (double *)malloc(sizeof(double) * 2 * (size_t)d);
+        double *wu = wg + d;
+#pragma omp for schedule(dynamic, 4)
+        for (int idx = 0; idx < k; idx++) {
+            const int t = idx < plan[1] ? 0 : (idx < plan[1] + plan[2] ? 1 : 2);
+            const int64_t nb = orc_record_bytes(bits[t], d);
+            orc_dequant_record(bits[t], d, recs[t] + (size_t)tier_ids[idx] * nb, wg, wu,
+                               wdall + (size_t)idx * d);
+            double g = 0.0, u = 0.0;
+            for (int j = 0; j < d; j++) { g += wg[j] * xd[j]; u += wu[j] * xd[j]; }
+            a[idx] = (act == 1) ? (g > 0.0 ? g : 0.0) * u : g / (1.0 + exp(-g)) * u;
+        }
+        free(wg);
+#pragma omp for schedule(static)
+        for (int j = 0; j < d; j++) {
+            double y = 0.0;
+            for (int idx = 0; idx < k; idx++) y += a[idx] * wdall[(size_t)idx * d + j];
+            yhat[j] = y;
+        }
+    }
+    free(wdall);
+    free(a);
+    free(xd);
+    return ORC_OK;
+}
+
 /* O8 stack harness: x_next = fp16_rne(x + fp16_rne(yhat)) (exact sum in double). */
 void orc_residual(int d, const uint16_t *x, const double *yhat, uint16_t *y16, uint16_t *x_next)
 {

@@ -16,7 +16,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "m2c_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
-CFLAGS = ["-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared"]
+CFLAGS = ["-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared", "-fopenmp"]
 
 
 def build(force: bool = False) -> str:
@@ -58,6 +58,8 @@ def _setup(L):
     L.orc_predict.argtypes = [C.c_int] * 3 + [vp] * 6
     L.orc_select.argtypes = [C.c_int, vp, vp, vp, vp, vp]
     L.orc_ffn.argtypes = [C.c_int, vp, vp, vp, vp, vp, vp, C.c_int, vp, vp]
+    L.orc_predict_mt.argtypes = [C.c_int] * 3 + [vp] * 6 + [C.c_int]
+    L.orc_ffn_mt.argtypes = [C.c_int, vp, vp, vp, vp, vp, vp, C.c_int, vp, C.c_int]
     L.orc_residual.argtypes = [C.c_int, vp, vp, vp, vp]
     L.orc_residual.restype = None
     L.orc_lru_step.argtypes = [C.c_int, C.c_int, vp, vp, vp, i32, vp, C.c_int] + [vp] * 8
@@ -157,6 +159,45 @@ def ffn(d, plan, tier_ids, rec16, rec8, rec4, x, act=0, return_a=False):
                   _p(np.ascontiguousarray(rec8)), _p(np.ascontiguousarray(rec4)), _p(x), act,
                   _p(y), _p(a))
     return (y, a[: int(plan[0])]) if return_a else y
+
+
+def predict_mt(x, A, B, threads):
+    """predict() with the integer dot products split over `threads` OpenMP threads
+    (bit-identical; SURVEY 8(d) multi-core oracle timing)."""
+    x = _u16(x)
+    A = np.ascontiguousarray(A, np.int8)
+    B = np.ascontiguousarray(B, np.int8)
+    r, d = A.shape
+    F_r = B.shape[0]
+    h = np.zeros(r, np.int64)
+    hq = np.zeros(r, np.int8)
+    s = np.zeros(F_r, np.int32)
+    if lib().orc_predict_mt(d, r, F_r, _p(x), _p(A), _p(B), _p(h), _p(hq), _p(s), int(threads)):
+        raise ValueError("predict_mt: non-finite x or bad shape")
+    return dict(h=h, hq=hq, s=s)
+
+
+def ffn_mt(d, plan, tier_ids, rec16, rec8, rec4, x, threads, act=0):
+    """ffn() over `threads` OpenMP threads: a_n split over neurons, yhat_j split over j with
+    the neuron sum in the serial order (bit-identical; SURVEY 8(d) multi-core oracle timing)."""
+    plan = np.ascontiguousarray(plan, np.int32)
+    ids = np.ascontiguousarray(tier_ids, np.int32)
+    x = _u16(x)
+    y = np.zeros(d)
+    if lib().orc_ffn_mt(d, _p(plan), _p(ids), _p(np.ascontiguousarray(rec16)),
+                        _p(np.ascontiguousarray(rec8)), _p(np.ascontiguousarray(rec4)), _p(x), act,
+                        _p(y), int(threads)):
+        raise ValueError("ffn_mt: bad threads")
+    return y
+
+
+def layer_forward_mt(w, recs, x, plan, threads, act=0):
+    """layer_forward() on `threads` cores (timing of the oracle on all host cores)."""
+    pr = predict_mt(x, w["pred_A"], w["pred_B"], threads)
+    sel = select(pr["s"], plan)
+    d = np.asarray(x).size
+    yhat = ffn_mt(d, plan, sel["tier_ids"], recs[16], recs[8], recs[4], x, threads, act)
+    return dict(pr, **sel, yhat=yhat)
 
 
 def residual(x, yhat):

@@ -67,6 +67,26 @@ def test_mixed_tiers_equal_gather_matmul():
     assert np.max(np.abs(y - y16)) < 0.2 * np.max(np.abs(y16))
 
 
+@pytest.mark.parametrize("threads", [1, 3, 8])
+def test_multicore_oracle_is_bit_identical(threads):
+    """SURVEY 8(d)'s multi-core oracle timing variant computes exactly what the serial oracle
+    does (same per-output operation order); its timing is therefore of the same program."""
+    F, d, r = 400, 384, 32
+    g, u, dn, x = _layer(F, d, 7)
+    recs = {b: orc.pack(b, g, u, dn) for b in (16, 8, 4)}
+    rng = np.random.default_rng(1)
+    A = rng.integers(-127, 128, (r, d)).astype(np.int8)
+    B = rng.integers(-127, 128, (F, r)).astype(np.int8)
+    w = {"pred_A": A, "pred_B": B}
+    plan = orc.tier_plan(F, 20)
+    for act in (0, 1):
+        ref = orc.layer_forward(w, recs, x, plan, act)
+        got = orc.layer_forward_mt(w, recs, x, plan, threads, act)
+        for key in ("h", "hq", "s", "tier_ids"):
+            assert np.array_equal(ref[key], got[key]), key
+        assert np.array_equal(ref["yhat"], got["yhat"])
+
+
 def test_residual_rounding():
     rng = np.random.default_rng(2)
     x = rng.standard_normal(4096).astype(np.float16)
