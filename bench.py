@@ -447,6 +447,7 @@ def main():
             "roofline": {"kernel": kname, "bound": "hbm",
                          "achieved": achieved, "peak": peak, "peak_src": peak_src,
                          "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                         "frac_of_nominal_8000": achieved / 8000.0,
                          "bytes_per_launch": bytes_launch, "ms_per_launch": launch_ms},
             "phase_ms_per_token": dict(zip(["predict", "select", "cache+ffn", "reduce"], phase_ms)),
             "gpu_launches": kpt * K,
