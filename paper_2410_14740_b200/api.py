@@ -28,6 +28,20 @@ def _require_cuda(*ts):
             raise ValueError("libm2c compute calls take CUDA tensors (no CPU fallback)")
 
 
+def _event_handle(ev, stream):
+    """cudaEvent_t of a torch.cuda.Event.  torch creates the CUDA event lazily at its first
+    record(): an event never recorded has handle 0, which the C ABI would read as 'no event'
+    (no wait -- the miss FFN would race the fills).  Force its creation on `stream` first."""
+    if ev is None:
+        return None
+    if not ev.cuda_event:
+        ev.record(stream)
+    h = ev.cuda_event
+    if not h:
+        raise M2CError(1, "fill_done: could not create the CUDA event")
+    return h
+
+
 def record_bytes(tier_bits: int, d_model: int) -> int:
     return int(lib().m2c_record_bytes(tier_bits, d_model))
 
@@ -252,7 +266,7 @@ class M2CContext:
             out["miss_log"] = torch.full((max(k, 1), 2), -1, dtype=torch.int32, device=dev)
             out["evict_log"] = torch.full((max(k, 1), 2), -1, dtype=torch.int32, device=dev)
             out["counts"] = torch.zeros(6, dtype=torch.int32, device=dev)
-        ev = fill_done.cuda_event if fill_done is not None else None
+        ev = _event_handle(fill_done, self.copy)
         self._call(lib().m2c_cache_lookup_fill, self._h, layer, step, _ptr(tier_ids), C.byref(plan),
                                           _ptr(out["slots"]), _ptr(out["hit_bitmap"]),
                                           _ptr(out.get("miss_log")), _ptr(out.get("evict_log")),
@@ -268,7 +282,7 @@ class M2CContext:
         d = self.desc.d_model
         yp = torch.empty(d, dtype=torch.float32, device=self.device) if want_partial else None
         y = torch.empty(d, dtype=torch.float16, device=self.device) if want_y else None
-        ev = fill_done.cuda_event if fill_done is not None else None
+        ev = _event_handle(fill_done, self.copy)
         self._call(lib().m2c_sparse_ffn_forward, self._h, layer, _ptr(x), _ptr(tier_ids), _ptr(slots),
                                            _ptr(hit_bitmap), C.byref(plan),
                                            C.c_void_p(ev) if ev else None, _ptr(yp), _ptr(y))

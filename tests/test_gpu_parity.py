@@ -799,3 +799,101 @@ def test_p2p_ipc_two_processes(m2c):
         assert res[0][t] == res[1][t] == want, t
     for c in ctxs:
         c.close()
+
+
+def test_lru_full_s13_layer_against_oracle(m2c):
+    """BASELINE configs[2] at full size (one 5120 x 13824 layer, pools capped at 25% of the
+    layer's FP16 bytes, C = (1696, 1696, 3402)): 32 tokens of predict -> LRU lookup + fill ->
+    FFN through the C ABI; every token's slots, hit bits, miss and eviction logs equal oracle
+    O7 per tier pool bit-exactly (through the cold start into the eviction regime), and at
+    sampled tokens y equals O6 within the tolerance."""
+    cfg = get_config("S13")
+    plan = m2c.plan_of(cfg)
+    w = layer_weights(cfg, 0, device="cuda")
+    wn = _np(w)
+    ctx = _ctx(m2c, cfg, plan)
+    cc = m2c.cache_cfg_capped(ctx.desc, plan, 1, 4, "lru")
+    # R8: M = 0.25 * 6dF / sum_t k_t nb_t with 16-B padded records = 4.9166 -> (1696, 1696, 3402)
+    # (SURVEY's 3403 rounds M to 4.918 first)
+    assert [int(cc.cap_slots[t]) for t in range(3)] == [1696, 1696, 3402]
+    ctx.reserve_host_tier(ctx.layer_footprint(cc)[1])
+    ctx.load_layer(0, w["w_gate"], w["w_up"], w["w_down_t"], w["pred_A"], w["pred_B"], cc)
+    pools = [orc.LRUPool(int(cc.cap_slots[t]), cfg.d_ff) for t in range(3)]
+    seg = [0, plan.k_fp16, plan.k_fp16 + plan.k_int8, plan.k]
+    xs = layer_input_stream(cfg, 0, 32, device="cuda")
+    ev = torch.cuda.Event()
+    recs = None
+    n_evict = 0
+    for t in range(32):
+        x = xs[t].contiguous()
+        sel = ctx.predict_rank(0, x, rank_list=False, tier_of=False, scores=False)
+        ids = sel["tier_ids"]
+        lk = ctx.cache_lookup_fill(0, 10 + t, ids, fill_done=ev)
+        _, y = ctx.sparse_ffn_forward(0, x, ids, lk["slots"], lk["hit_bitmap"], fill_done=ev,
+                                      want_partial=False)
+        idn = ids.cpu().numpy()
+        slots = lk["slots"].cpu().numpy()
+        bits = _bits(lk["hit_bitmap"], plan.k)
+        ml, el = lk["miss_log"].cpu().numpy(), lk["evict_log"].cpu().numpy()
+        cnt = lk["counts"].cpu().numpy()
+        for tau in range(3):
+            ref = pools[tau].step(10 + t, idn[seg[tau]:seg[tau + 1]])
+            assert np.array_equal(slots[seg[tau]:seg[tau + 1]], ref["slots"]), (t, tau)
+            rb = np.array([(ref["hit_bits"][i // 32] >> (i % 32)) & 1
+                           for i in range(seg[tau + 1] - seg[tau])], np.uint32)
+            assert np.array_equal(bits[seg[tau]:seg[tau + 1]], rb), (t, tau)
+            nm, ne = len(ref["miss"]), len(ref["evict"])
+            assert cnt[tau] == nm and cnt[3 + tau] == ne, (t, tau)
+            assert np.array_equal(ml[seg[tau]:seg[tau] + nm], ref["miss"])
+            assert np.array_equal(el[seg[tau]:seg[tau] + ne], ref["evict"])
+            n_evict += ne
+        if t in (0, 17, 31):
+            if recs is None:
+                recs = orc.layer_records(wn)
+            ref = orc.select(orc.predict(x.cpu().numpy(), wn["pred_A"], wn["pred_B"])["s"],
+                             _plan_np(plan))
+            assert np.array_equal(idn, ref["tier_ids"]), t
+            yhat = orc.ffn(cfg.d_model, _plan_np(plan), idn, recs[16], recs[8], recs[4],
+                           x.cpu().numpy())
+            assert d10(y.cpu().numpy(), yhat) <= TOL, t
+    assert n_evict > 0  # the pools filled up and evicted
+    ctx.close()
+
+
+def test_decode_step_lru_s13_shape_matches_api_chain(m2c):
+    """The LRU decode engine bench.py times at configs[2] (graph-captured select-only k_decode
+    at d = 5120 -> k_lru -> copy-stream k_fill || hit FFN -> miss FFN -> reduce) equals the
+    per-call C-ABI chain bit-exactly over 10 tokens of a 3-layer full-width S13 stack."""
+    cfg = get_config("S13")
+    L = 3
+    plan = m2c.plan_of(cfg)
+    ctxs = []
+    for _ in range(2):
+        ctx = _ctx(m2c, cfg, plan, n_layers=L)
+        cc = m2c.cache_cfg_capped(ctx.desc, plan, 1, 4, "lru")
+        ctx.reserve_host_tier(L * ctx.layer_footprint(cc)[1])
+        for l in range(L):
+            w = layer_weights(cfg, l, device="cuda")
+            ctx.load_layer(l, w["w_gate"], w["w_up"], w["w_down_t"], w["pred_A"], w["pred_B"], cc)
+            del w
+        ctxs.append(ctx)
+    a, b = ctxs
+    xs = token_stream(cfg, 10, device="cuda")
+    ev = torch.cuda.Event()
+    for t in range(10):
+        x = xs[t].contiguous().clone()
+        a.decode_step(x, t + 1)
+        xc = xs[t].contiguous().clone()
+        for l in range(L):
+            sel = b.predict_rank(l, xc, rank_list=False, tier_of=False, scores=False)
+            lk = b.cache_lookup_fill(l, t + 1, sel["tier_ids"], logs=False, fill_done=ev)
+            _, y = b.sparse_ffn_forward(l, xc, sel["tier_ids"], lk["slots"], lk["hit_bitmap"],
+                                        fill_done=ev, want_partial=False)
+            xc = xc + y
+        torch.cuda.synchronize()
+        assert torch.equal(x, xc), t
+    sa, sb = a.stats(), b.stats()
+    assert sa["hits"] == sb["hits"] and sa["misses"] == sb["misses"]
+    assert sa["kernels_per_token"] > 1
+    for c in ctxs:
+        c.close()
