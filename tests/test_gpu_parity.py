@@ -200,7 +200,8 @@ def test_ffn_relu_flag(m2c):
 
 
 @pytest.mark.parametrize("name,shard,layer", [("S7", (0, 1), 5), ("S13", (0, 1), 7),
-                                              ("S70", (5, 8), 11)])
+                                              ("S70", (5, 8), 11), ("S70", (1, 2), 3),
+                                              ("S70H", (0, 1), 20)])
 def test_ffn_full_shapes(m2c, name, shard, layer):
     e16, e32 = _ffn_case(m2c, get_config(name), layer, 2, shard)
     assert e16 <= TOL and e32 <= 1e-4, (e16, e32)
@@ -562,7 +563,7 @@ def test_global_topk_under_sharding_equals_unsharded(m2c, P, pct, a16, a8, den):
         c.close()
 
 
-@pytest.mark.parametrize("name,layers", [("T", 3), ("S7", 3)])
+@pytest.mark.parametrize("name,layers", [("T", 3), ("S7", 3), ("S70H", 2)])
 def test_decode_layer_split_equals_fused(m2c, name, layers):
     """The layer-split engine (k_decode one layer per launch, the partial y handed to the next
     launch through the all-reduce buffer -- the d_ff-sharded decode) is bit-identical to the
