@@ -248,11 +248,17 @@ def main():
             args.split or args.unfused or args.global_topk):
         try:
             m2c_dist.p2p_init(ctx)
-            allreduce = "p2p"
+            ok = 1
         except Exception as e:  # (auto) keep the NCCL engine
             if args.allreduce == "p2p":
                 raise
             print(f"[bench] p2p exchange unavailable ({e}); using NCCL", file=sys.stderr)
+            ok = 0
+        okt = torch.tensor([ok], dtype=torch.int32, device=dev)  # every rank decides together
+        dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+        if int(okt.item()):
+            allreduce = "p2p"
+        else:
             ctx.set_fused(2)
     if world > 1:
         dist.barrier()  # ranks enter the coupled decode together

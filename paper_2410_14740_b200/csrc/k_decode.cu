@@ -909,7 +909,10 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
                         const unsigned long long *mine = p.xpeer[p.rank] + row * d + e;
                         for (int q = 0; q < P; q++) {
                             unsigned long long w = ld_relaxed_sys_u64(mine + (size_t)q * d);
-                            if ((unsigned)(w >> 32) != flag) {
+                            if ((unsigned)(w >> 32) != flag &&
+                                !(*reinterpret_cast<volatile unsigned *>(p.err) & 16u)) {
+                                // (after one timeout no CTA waits again: a dead peer costs
+                                // 5 s per token, not per chunk)
                                 const unsigned long long t0 = gtimer();
                                 do {
                                     w = ld_relaxed_sys_u64(mine + (size_t)q * d);
