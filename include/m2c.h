@@ -243,6 +243,10 @@ m2c_status m2c_set_fused(m2c_ctx *ctx, int32_t enable);
 #define M2C_DECODE_STAMPS 24
 m2c_status m2c_profile(m2c_ctx *ctx, int32_t enable);
 m2c_status m2c_profile_read(m2c_ctx *ctx, float *ms, int32_t *ffn_launches_out);
+/* Miss-fill duration of each LRU/ATU layer in the last profiled m2c_decode_step (ms, copy
+ * stream, CUDA events around the fill kernels; 0 for resident layers).  M2C_ERR_STATE if
+ * profiling is off or the last step ran k_decode alone (no fills). */
+m2c_status m2c_profile_fill(m2c_ctx *ctx, float *ms_per_layer);
 m2c_status m2c_profile_stamps(m2c_ctx *ctx, uint64_t *out, int64_t cap, int64_t *n_out);
 
 /* Kernels launched by the last m2c_decode_step (per token), and cumulative cache counters

@@ -69,6 +69,7 @@ SIGNATURES = [
     ("m2c_stats", C.c_int, [_vp, _P(_i64), _P(_i64), _P(_i64), _i32]),
     ("m2c_profile", C.c_int, [_vp, _i32]),
     ("m2c_profile_read", C.c_int, [_vp, _P(C.c_float), _P(_i32)]),
+    ("m2c_profile_fill", C.c_int, [_vp, _P(C.c_float)]),
     ("m2c_profile_stamps", C.c_int, [_vp, _P(C.c_uint64), _i64, _P(_i64)]),
     ("m2c_predict_candidates", C.c_int, [_vp, _i32, _vp, _i32, _vp]),
     ("m2c_select_global", C.c_int, [_vp, _vp, _i32, _P(TierPlan), _vp, _vp]),

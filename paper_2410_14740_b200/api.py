@@ -318,6 +318,12 @@ class M2CContext:
         check(lib().m2c_profile_read(self._h, ms, C.byref(n)))
         return [list(ms[4 * l:4 * l + 4]) for l in range(L)], n.value
 
+    def profile_fill(self):
+        """Miss-fill duration (ms) per layer of the last profiled decode step (0: resident)."""
+        ms = (C.c_float * self.desc.n_layers)()
+        check(lib().m2c_profile_fill(self._h, ms))
+        return list(ms)
+
     def profile_stamps(self):
         """Raw k_decode stamps of the last decode step (profiling on): numpy uint64
         [n_layers, G, DECODE_STAMPS] in ns (include/m2c.h documents the stamp points)."""

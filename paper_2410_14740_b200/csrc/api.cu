@@ -141,9 +141,16 @@ static bool al16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) =
 static int32_t *step_ptr(m2c_ctx *c) { return c->ws.counts + 15; }
 
 // ---- the token: all layers on the compute stream (+ copy stream for LRU fills) ----
+// profiling events per layer: 5 compute-stream marks (phase boundaries) + 2 around the miss
+// fill on the copy stream
+constexpr int kProfEv = 7;
+static cudaError_t mark_copy(m2c_ctx *c, int l, int i) {
+    if (c->prof_ev.empty()) return cudaSuccess;
+    return cudaEventRecordWithFlags(c->prof_ev[kProfEv * l + 5 + i], c->copy, cudaEventRecordExternal);
+}
 static cudaError_t mark(m2c_ctx *c, int l, int i) {
     if (c->prof_ev.empty()) return cudaSuccess;
-    return cudaEventRecordWithFlags(c->prof_ev[5 * l + i], c->compute, cudaEventRecordExternal);
+    return cudaEventRecordWithFlags(c->prof_ev[kProfEv * l + i], c->compute, cudaEventRecordExternal);
 }
 
 // the miss fill of layer l: from the in-memory host tier, or (NEXT-1) from the layer's DRAM
@@ -238,7 +245,9 @@ static cudaError_t enqueue_layer(m2c_ctx *c, int l, __half *x) {
         // NEXT-2: layer l's records staged during layer l-1 (parity l & 1) fill device-side
         const bool la = c->lookahead && !c->store;
         if (la && l > 0 && (e = cudaStreamWaitEvent(c->copy, c->ev_staged[l & 1], 0))) return e;
+        if ((e = mark_copy(c, l, 0))) return e;
         if ((e = enqueue_fill(c, l, p, la && l > 0 ? (l & 1) : -1))) return e;
+        if ((e = mark_copy(c, l, 1))) return e;
         if (la && l > 0 && (e = launch_stage_clear(c, L, l & 1, c->copy))) return e;
         if ((e = cudaEventRecord(c->ev_fill, c->copy))) return e;
         e = launch_ffn(c, L, x, c->ws.hit_items, c->ws.counts + 4, p, c->ws.partial, st);
@@ -929,7 +938,7 @@ m2c_status m2c_profile(m2c_ctx *c, int32_t enable) {
     for (cudaEvent_t e : c->prof_ev) cudaEventDestroy(e);
     c->prof_ev.clear();
     if (enable) {
-        c->prof_ev.resize(5 * (size_t)c->desc.n_layers);
+        c->prof_ev.resize(kProfEv * (size_t)c->desc.n_layers);
         for (auto &e : c->prof_ev) M2C_CUDA(cudaEventCreate(&e));
     }
     if (c->graph) {
@@ -970,8 +979,23 @@ m2c_status m2c_profile_read(m2c_ctx *c, float *ms, int32_t *ffn_launches) {
     }
     for (int l = 0; l < c->desc.n_layers; l++)
         for (int i = 0; i < 4; i++)
-            M2C_CUDA(cudaEventElapsedTime(&ms[4 * l + i], c->prof_ev[5 * l + i], c->prof_ev[5 * l + i + 1]));
+            M2C_CUDA(cudaEventElapsedTime(&ms[4 * l + i], c->prof_ev[kProfEv * l + i],
+                                          c->prof_ev[kProfEv * l + i + 1]));
     if (ffn_launches) *ffn_launches = c->layers[0].mode == 0 ? 1 : 2;
+    return M2C_OK;
+}
+
+m2c_status m2c_profile_fill(m2c_ctx *c, float *ms) {
+    if (!c || !ms) return fail(M2C_ERR_INVALID_ARG, "null argument");
+    if (c->prof_ev.empty()) return fail(M2C_ERR_STATE, "profiling not enabled");
+    if (c->last_token_fused || c->last_token_split) return fail(M2C_ERR_STATE, "no fills in the last step");
+    M2C_CUDA(cudaStreamSynchronize(c->copy));
+    M2C_CUDA(cudaStreamSynchronize(c->compute));
+    for (int l = 0; l < c->desc.n_layers; l++) {
+        ms[l] = 0.f;
+        if (c->layers[l].mode == 0) continue;
+        M2C_CUDA(cudaEventElapsedTime(&ms[l], c->prof_ev[kProfEv * l + 5], c->prof_ev[kProfEv * l + 6]));
+    }
     return M2C_OK;
 }
 
