@@ -898,3 +898,31 @@ def test_decode_step_lru_s13_shape_matches_api_chain(m2c):
     assert sa["kernels_per_token"] > 1
     for c in ctxs:
         c.close()
+
+
+def test_profile_fill_reports_lru_fills(m2c):
+    """m2c_profile_fill (the S13 roofline's denominator): positive fill durations for LRU
+    layers of a profiled decode step; a resident whole-token step has none (M2C_ERR_STATE)."""
+    cfg = get_config("T")
+    L = 2
+    plan = m2c.plan_of(cfg)
+    ctx = _ctx(m2c, cfg, plan, n_layers=L)
+    cc = m2c.cache_cfg_capped(ctx.desc, plan, 1, 4, "lru")
+    ctx.reserve_host_tier(L * ctx.layer_footprint(cc)[1])
+    for l in range(L):
+        w = layer_weights(cfg, l, device="cuda")
+        ctx.load_layer(l, w["w_gate"], w["w_up"], w["w_down_t"], w["pred_A"], w["pred_B"], cc)
+    ctx.profile(True)
+    x = token_stream(cfg, 1, device="cuda")[0].contiguous()
+    ctx.decode_step(x, 1)  # cold pools: every selected record is a miss
+    ms = ctx.profile_fill()
+    assert len(ms) == L and all(v > 0 for v in ms)
+    ctx.close()
+    res = _ctx(m2c, cfg, plan, n_layers=1)
+    w = layer_weights(cfg, 0, device="cuda")
+    res.load_layer(0, w["w_gate"], w["w_up"], w["w_down_t"], w["pred_A"], w["pred_B"])
+    res.profile(True)
+    res.decode_step(x.clone(), 1)
+    with pytest.raises(m2c.M2CError):
+        res.profile_fill()
+    res.close()
