@@ -224,7 +224,9 @@ static cudaError_t enqueue_layer(m2c_ctx *c, int l, __half *x) {
     }
     if (L.mode != 0 && c->use_fused && decode_select_ok(c)) {
         // the predictor + exact select of k_decode in one launch (its P2/P3 phases)
-        if ((e = launch_decode(c, x, nullptr, st, l, 1, nullptr, nullptr, ids))) return e;
+        if ((e = launch_decode(c, x, c->prof_ev.empty() ? nullptr : c->dec_prof, st, l, 1, nullptr,
+                               nullptr, ids)))
+            return e;
         if ((e = mark(c, l, 1))) return e;
         if ((e = mark(c, l, 2))) return e;
     } else {
@@ -1005,7 +1007,7 @@ m2c_status m2c_profile_stamps(m2c_ctx *c, uint64_t *out, int64_t cap, int64_t *n
     *n_out = n;
     if (!out) return M2C_OK;
     if (cap < n) return fail(M2C_ERR_INVALID_ARG, "profile_stamps: buffer too small");
-    if (c->prof_ev.empty() || !(c->last_token_fused || c->last_token_split))
+    if (c->prof_ev.empty() || !(c->last_token_fused || c->last_token_split || decode_select_ok(c)))
         return fail(M2C_ERR_STATE, "profile_stamps: profiling off or last token not on k_decode");
     M2C_CUDA(cudaStreamSynchronize(c->compute));
     M2C_CUDA(cudaMemcpy(out, c->dec_prof, 8 * (size_t)n, cudaMemcpyDeviceToHost));

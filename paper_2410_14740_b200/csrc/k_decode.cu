@@ -325,6 +325,10 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
         h_chunk(p.layers[0].At + (int64_t)ch * 32 * r, r, xm, xsh, p.hb);
         __syncthreads();
     }
+    // select-only launches leave their histogram dirty (no barrier after P3): every launch
+    // clears layer 0's here, ordered before every CTA's P2 atomics by the barrier below
+    if (cta == G - 1)
+        for (int i = tid; i < kHistW; i += NT) p.ghist[i] = 0;
     grid_sync(p.bar_flags, base + ++nbar, p.err);
     STAMP(13);
 
@@ -795,13 +799,8 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
             __syncthreads();
         }
         STAMP(5);
-        if (p.select_only) {  // the LRU/ATU chain: predictor + selection only; the lists are out
-            // the histogram must be clear for the next launch, once every CTA has copied it
-            grid_sync(p.bar_flags, base + ++nbar, p.err);
-            if (cta == G - 1)
-                for (int i = tid; i < kHistW; i += NT) hist[i] = 0;
-            break;
-        }
+        if (p.select_only) break;  // the LRU/ATU chain: predictor + selection only; the lists
+                                    // are out (the histogram is cleared by the next launch's prologue)
 
         // ================= P4: fused dequant-GEMV FFN over this CTA's share ===============
         {
