@@ -290,6 +290,9 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
         for (int i = 0; i < 6; i++) sm.rng[i] = rg[i];
     }
     ffn_tables(sm, d);
+    // (launched with programmatic stream serialization -- select-only launches of the LRU chain:
+    // the set-up above overlapped the previous kernel; nothing it wrote is read before here)
+    griddep_wait();
     const unsigned base = ld_relaxed(p.bar_epoch);  // read by every CTA before its first arrival
     const unsigned round0 = p.nrank > 1 ? ld_relaxed(p.rounds) : 0u;
     unsigned nbar = 0;
@@ -1038,11 +1041,20 @@ cudaError_t launch_decode(m2c_ctx *c, __half *x, unsigned long long *prof, cudaS
     cfg.blockDim = dim3(d / 8);
     cfg.dynamicSmemBytes = kSmemBytes;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident (grid barriers)
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    static const int pdl = [] {  // M2C_DECODE_PDL=0 disables (A/B knob; results identical)
+        const char *ev = getenv("M2C_DECODE_PDL");
+        return ev ? atoi(ev) : 1;
+    }();
+    if (lists_out && pdl) {  // select-only (LRU chain): overlap the launch with the previous kernel
+        attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[1].val.programmaticStreamSerializationAllowed = 1;
+        cfg.numAttrs = 2;
+    }
     // <= 512 threads (d <= 4096): 128 registers per thread; else 64
     cudaError_t e = d / 8 <= 512 ? cudaLaunchKernelEx(&cfg, k_decode<512>, a)
                                  : cudaLaunchKernelEx(&cfg, k_decode<1024>, a);
