@@ -351,6 +351,12 @@ def main():
     phase_ms = [sum(prof[l][i] for l in range(cfg.n_layers)) for i in range(4)]
     if fused or split:
         # k_decode launch durations, CUDA events on its own (compute) stream, after warm-up
+        # (one untimed step first: profile(False) dropped the graph, and its re-capture would
+        # leave the GPU idle between the first pair of events)
+        x.copy_(toks[W])
+        ctx.decode_step(x, step)
+        step += 1
+        torch.cuda.synchronize()
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                for _ in range(nprof)]
         with torch.cuda.stream(ctx.compute):
