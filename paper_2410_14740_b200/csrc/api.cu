@@ -173,6 +173,38 @@ static bool decode_select_ok(const m2c_ctx *c) {
     return c->F_r <= decode_max_F() && rps <= c->desc.d_model / 8 && rps <= 254;
 }
 
+// the early-fill LRU engine: not with the NEXT-2 lookahead or a NEXT-1 store (their fills
+// have their own sources); M2C_EARLY_FILL=0 disables it (A/B knob, results identical)
+static bool early_fill_on(const m2c_ctx *c) {
+    static const bool env_on = !(getenv("M2C_EARLY_FILL") && atoi(getenv("M2C_EARLY_FILL")) == 0);
+    return env_on && c->early_fill && c->early_mem && !c->lookahead && !c->store;
+}
+
+static cudaError_t early_fill_alloc(m2c_ctx *c) {
+    if (c->early_mem) return cudaSuccess;
+    const m2c_tier_plan &p = c->plan;
+    const int k = p.k > 0 ? p.k : 1;
+    const int kt[3] = {p.k_fp16, p.k_int8, p.k_int4};
+    size_t off = a256(4 * (16 + (size_t)k)) + a256(4 * (size_t)k), st_off[3];
+    for (int t = 0; t < 3; t++) {
+        st_off[t] = off;
+        off += a256((size_t)(kt[t] > 0 ? kt[t] : 1) * c->nb[t]);
+    }
+    cudaError_t e = cudaMalloc(&c->early_mem, off);
+    if (e) return e;
+    uint8_t *b = static_cast<uint8_t *>(c->early_mem);
+    c->mq = reinterpret_cast<int32_t *>(b);
+    c->ident = reinterpret_cast<int32_t *>(b + a256(4 * (16 + (size_t)k)));
+    for (int t = 0; t < 3; t++) c->mstage[t] = b + st_off[t];
+    std::vector<int32_t> id(k, 0);
+    for (int t = 0, seg = 0; t < 3; seg += kt[t], t++)
+        for (int m = 0; m < kt[t]; m++) id[seg + m] = m;
+    if ((e = cudaMemset(c->mq, 0, 4 * (16 + (size_t)k)))) return e;
+    if ((e = cudaMemcpy(c->ident, id.data(), 4 * (size_t)k, cudaMemcpyHostToDevice))) return e;
+    if ((e = cudaEventCreateWithFlags(&c->ev_q, cudaEventDisableTiming))) return e;
+    return cudaEventCreateWithFlags(&c->ev_scat, cudaEventDisableTiming);
+}
+
 static cudaError_t enqueue_layer(m2c_ctx *c, int l, __half *x) {
     LayerState &L = c->layers[l];
     const m2c_tier_plan &p = c->plan;
@@ -239,6 +271,35 @@ static cudaError_t enqueue_layer(m2c_ctx *c, int l, __half *x) {
     if (L.mode == 0) {
         e = launch_ffn(c, L, x, ids, c->ws.counts, p, c->ws.partial, st);
         if (e) return e;
+    } else if (early_fill_on(c)) {
+        // early fill: the misses (ids without a slot) are queued first and their host-tier
+        // copies start into the staging area while k_lru chooses the victims; the miss FFN
+        // reads the staging area; the copy stream then scatters the records into their slots
+        if ((e = launch_missq(c, L, c->ws.tier_ids, p, st))) return e;
+        if ((e = cudaEventRecord(c->ev_q, st))) return e;
+        if ((e = cudaStreamWaitEvent(c->copy, c->ev_q, 0))) return e;
+        if ((e = mark_copy(c, l, 0))) return e;
+        const uint8_t *hsrc[3] = {L.host_rec[0], L.host_rec[1], L.host_rec[2]};
+        if ((e = launch_copy_recs(c, hsrc, c->mstage, p, c->mq, c->mq + 16, c->ident, c->copy))) return e;
+        if ((e = mark_copy(c, l, 1))) return e;
+        if ((e = cudaEventRecord(c->ev_fill, c->copy))) return e;
+        e = launch_lru(c, L, step_ptr(c), c->ws.tier_ids, p, c->ws.slots, c->ws.hit_bits, nullptr, nullptr, st);
+        if (e) return e;
+        if ((e = cudaEventRecord(c->ev_lookup, st))) return e;
+        if ((e = cudaStreamWaitEvent(c->copy, c->ev_lookup, 0))) return e;
+        const uint8_t *ssrc[3] = {c->mstage[0], c->mstage[1], c->mstage[2]};
+        uint8_t *pdst[3] = {L.pool[0], L.pool[1], L.pool[2]};
+        if ((e = launch_copy_recs(c, ssrc, pdst, p, c->ws.counts, c->ident, c->ws.miss_items, c->copy)))
+            return e;
+        if ((e = cudaEventRecord(c->ev_scat, c->copy))) return e;
+        e = launch_ffn(c, L, x, c->ws.hit_items, c->ws.counts + 4, p, c->ws.partial, st);
+        if (e) return e;
+        if ((e = cudaStreamWaitEvent(st, c->ev_fill, 0))) return e;
+        LayerState Ls = L;
+        for (int t = 0; t < 3; t++) Ls.pool[t] = c->mstage[t];
+        e = launch_ffn(c, Ls, x, c->ident, c->mq + 8, p, c->ws.partial + (size_t)c->G * c->desc.d_model, st);
+        if (e) return e;
+        np = 2 * c->G;
     } else {
         e = launch_lru(c, L, step_ptr(c), c->ws.tier_ids, p, c->ws.slots, c->ws.hit_bits, nullptr, nullptr, st);
         if (e) return e;
@@ -316,8 +377,12 @@ static cudaError_t enqueue_token(m2c_ctx *c, __half *x) {
     cudaError_t e = launch_set_counts(c->ws.counts, p.k_fp16, p.k_int8, p.k_int4, c->compute);
     c->launch_counter++;
     if (e) return e;
-    for (int l = 0; l < c->desc.n_layers; l++)
+    bool early = false;
+    for (int l = 0; l < c->desc.n_layers; l++) {
         if ((e = enqueue_layer(c, l, x))) return e;
+        early |= c->layers[l].mode != 0 && early_fill_on(c);
+    }
+    if (early) return cudaStreamWaitEvent(c->compute, c->ev_scat, 0);  // join the last scatter
     return cudaSuccess;
 }
 
@@ -532,6 +597,12 @@ m2c_status m2c_destroy(m2c_ctx *c) {
         for (int p = 0; p < 2; p++) cudaEventDestroy(c->ev_staged[p]);
         cudaFree(c->stage_mem);
     }
+    if (c->early_mem) {
+        cudaStreamSynchronize(c->copy);
+        cudaFree(c->early_mem);
+    }
+    if (c->ev_q) cudaEventDestroy(c->ev_q);
+    if (c->ev_scat) cudaEventDestroy(c->ev_scat);
     for (void *p : c->p2p_opened) cudaIpcCloseMemHandle(p);
     if (c->p2p_tabs) cudaFree(c->p2p_tabs);
     if (c->p2p_mem) cudaFree(c->p2p_mem);
@@ -878,6 +949,7 @@ m2c_status m2c_decode_step(m2c_ctx *c, void *x_inout, int64_t step) {
                                     "kernel and this stack/grid does not fit it (no communicator "
                                     "for the other engines)");
     cudaStream_t cs = c->compute;
+    if (any_lru && !c->early_mem) M2C_CUDA(early_fill_alloc(c));
     if (any_lru) {
         const int32_t st32 = (int32_t)step;  // pageable source: staged before return
         M2C_CUDA(cudaMemcpyAsync(step_ptr(c), &st32, 4, cudaMemcpyHostToDevice, cs));

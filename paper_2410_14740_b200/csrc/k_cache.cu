@@ -180,6 +180,31 @@ __global__ void __launch_bounds__(NT, 1)
     }
 }
 
+// Early fill (decode engine, LRU/ATU): the misses of a step are the list entries whose id has
+// no slot yet -- known before the victims are chosen.  k_missq compacts them per tier in
+// ascending list order (the order k_lru pairs them with victims), so the host-tier copies can
+// start into a staging area while k_lru runs; the miss FFN reads the staging area and the
+// records are scattered into their victim slots afterwards (copy stream).
+__global__ void __launch_bounds__(NT, 1)
+    k_missq(LruArgs a, const int32_t *__restrict__ tier_ids, int32_t *__restrict__ q) {
+    // q: [16] header (q[8 + t] = misses of tier t) | ids [k] (segments as tier_ids)
+    __shared__ int scan_sm[NW];
+    griddep_wait();
+    const int tau = blockIdx.x;
+    const int n = a.cnt[tau], seg = a.seg[tau];
+    const int32_t *slot_of = a.slot_of[tau];
+    const int32_t *R = tier_ids + seg;
+    const int CH = (n + NT - 1) / NT;
+    const int i0 = min(n, (int)threadIdx.x * CH), i1 = min(n, i0 + CH);
+    int nm = 0;
+    for (int i = i0; i < i1; i++) nm += slot_of[R[i]] < 0;
+    int tot;
+    int pos = block_scan1(nm, &tot, scan_sm);
+    for (int i = i0; i < i1; i++)
+        if (slot_of[R[i]] < 0) q[16 + seg + pos++] = R[i];
+    if (threadIdx.x == 0) q[8 + tau] = tot;
+}
+
 struct StageArgs {
     const uint8_t *host[3];   // layer l+1's host tier
     const int32_t *slot_of[3];  // layer l+1's pools (read before layer l+1's lookup)
@@ -368,6 +393,43 @@ cudaError_t launch_stage_clear(m2c_ctx *c, const LayerState &Ln, int par, cudaSt
     const int k = c->plan.k;
     if (k <= 0) return cudaSuccess;
     cudaError_t e = launch_k(k_stage_clear, dim3((k + 255) / 256), dim3(256), 0, st, stage_args(c, Ln, par));
+    c->launch_counter++;
+    return e;
+}
+
+cudaError_t launch_missq(m2c_ctx *c, const LayerState &L, const int32_t *tier_ids,
+                         const m2c_tier_plan &p, cudaStream_t st) {
+    LruArgs a;
+    const int cnt[3] = {p.k_fp16, p.k_int8, p.k_int4};
+    const int seg[3] = {0, p.k_fp16, p.k_fp16 + p.k_int8};
+    for (int t = 0; t < 3; t++) {
+        a.slot_of[t] = L.slot_of[t];
+        a.seg[t] = seg[t];
+        a.cnt[t] = cnt[t];
+    }
+    cudaError_t e = launch_k(k_missq, dim3(3), dim3(NT), 0, st, a, tier_ids, c->mq);
+    c->launch_counter++;
+    return e;
+}
+
+// generic record copy: dst[t] + dsti[seg + m] * nb  <-  src[t] + srci[seg + m] * nb for the
+// counts[8 + t] entries of each tier (k_fill without the lookahead)
+cudaError_t launch_copy_recs(m2c_ctx *c, const uint8_t *const src[3], uint8_t *const dst[3],
+                             const m2c_tier_plan &p, const int32_t *counts, const int32_t *srci,
+                             const int32_t *dsti, cudaStream_t st) {
+    FillArgs a;
+    const int seg[3] = {0, p.k_fp16, p.k_fp16 + p.k_int8};
+    for (int t = 0; t < 3; t++) {
+        a.host[t] = src[t];
+        a.pool[t] = dst[t];
+        a.nb[t] = c->nb[t];
+        a.seg[t] = seg[t];
+        a.stage_of[t] = nullptr;
+        a.stage[t] = nullptr;
+    }
+    a.staged = c->ws.stats + 6;
+    static const int fill_ctas = getenv("M2C_FILL_CTAS") ? atoi(getenv("M2C_FILL_CTAS")) : 64;
+    cudaError_t e = launch_k(k_fill, dim3(fill_ctas), dim3(256), 0, st, a, counts, srci, dsti);
     c->launch_counter++;
     return e;
 }

@@ -140,6 +140,13 @@ struct m2c_ctx {
     m2c_tier_plan gplan{};
     long long *gkeys = nullptr;   // [n] own candidates | [P][n] gathered
     int32_t *gids = nullptr;      // [k_global] this rank's part of the global tier lists
+    // early fill (decode engine, LRU/ATU layers): miss queue, identity list, staging area
+    int32_t *mq = nullptr;        // [16 + k]: q[8 + t] = misses of tier t; ids from q + 16
+    int32_t *ident = nullptr;     // [k]: ident[seg_t + m] = m
+    uint8_t *mstage[3] = {nullptr, nullptr, nullptr};  // [k_t][nb_t]
+    void *early_mem = nullptr;
+    bool early_fill = true;
+    cudaEvent_t ev_q = nullptr, ev_scat = nullptr;
     // §8(e): in-kernel all-reduce over peer memory (m2c_p2p_*)
     bool p2p = false;
     void *p2p_mem = nullptr;          // this rank's exchange buffer [2][P][d] (flag|f32) u64 | rounds
@@ -181,6 +188,11 @@ cudaError_t launch_cand_keys(m2c_ctx *c, const int32_t *scores, const int32_t *r
 cudaError_t launch_select_global(m2c_ctx *c, const long long *keys, int n, const m2c_tier_plan &g,
                                  int32_t *tier_ids, int32_t *counts, cudaStream_t st);
 int select_blocks(int F_r);
+cudaError_t launch_missq(m2c_ctx *c, const LayerState &L, const int32_t *tier_ids,
+                         const m2c_tier_plan &p, cudaStream_t st);
+cudaError_t launch_copy_recs(m2c_ctx *c, const uint8_t *const src[3], uint8_t *const dst[3],
+                             const m2c_tier_plan &p, const int32_t *counts, const int32_t *srci,
+                             const int32_t *dsti, cudaStream_t st);
 cudaError_t launch_lru(m2c_ctx *c, LayerState &L, const int32_t *step_dev, const int32_t *tier_ids,
                        const m2c_tier_plan &p, int32_t *slots, uint32_t *hit_bits,
                        int32_t *miss_log, int32_t *evict_log, cudaStream_t st);
