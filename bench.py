@@ -388,6 +388,20 @@ def main():
     except Exception:
         pass
 
+    # ---- measured adjacent-token top-k overlap at layer 0 (target ~0.80) ----
+    overlap = None
+    if cfg.cache_mode == "resident" and (fused or split):
+        prev, ov = None, []
+        for t in range(9):
+            x.copy_(toks[W + t % K])
+            ctx.decode_step(x, step)
+            step += 1
+            cur = set(ctx.decode_lists(0).cpu().tolist())
+            if prev is not None and cur:
+                ov.append(len(cur & prev) / len(cur))
+            prev = cur
+        overlap = sum(ov) / len(ov) if ov else None
+
     # ---- end to end through the public API: pinned host in, host out, every step ----
     e2e = None
     if not args.no_e2e:
@@ -471,6 +485,7 @@ def main():
             "phase_ms_per_token": dict(zip(["predict", "select", "cache+ffn", "reduce"], phase_ms)),
             "gpu_launches": kpt * K,
             "kernels_per_token": kpt,
+            "topk_overlap_layer0": overlap,
             "clocks": clk.summary(),
             "e2e": e2e,
             "cpu_baseline": cpu,
