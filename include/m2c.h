@@ -97,7 +97,12 @@ m2c_status m2c_layer_footprint(const m2c_model_desc *desc, const m2c_cache_cfg *
                                size_t *hbm_bytes, size_t *host_pinned_bytes);
 
 /* ---- context --------------------------------------------------------------------------- */
-/* Creates a context on `device` with borrowed streams `compute` and `copy` (copy carries the
+/* Device-side invariant violations (non-finite x, a grid-barrier or peer-exchange timeout, an
+ * inconsistent selection count) are flagged by the kernels into a pinned host word; the next
+ * call on the context that takes it returns M2C_ERR_STATE (without synchronising) and
+ * m2c_last_error() names the violation.
+ *
+ * Creates a context on `device` with borrowed streams `compute` and `copy` (copy carries the
  * miss fills, "dedicated CUDA streams").  `decode_plan` is the plan m2c_decode_step
  * uses.  The context allocates a small device workspace (O(F_r + k + 148 d) bytes). */
 m2c_status m2c_create(const m2c_model_desc *desc, int32_t device, m2c_stream_t compute,
@@ -160,7 +165,10 @@ m2c_status m2c_cache_lookup_fill(m2c_ctx *ctx, int32_t layer, int64_t step,
  * = everything resident; else hits are computed first, then the compute stream waits on
  * fill_done (if non-NULL) and the misses are computed (R11).  Outputs (device, either may be
  * NULL): y_partial fp32 [d] = this rank's sum before any all-reduce; y fp16 [d] = the
- * all-reduced (if the context has a communicator with >1 rank) sum rounded to fp16. */
+ * all-reduced (if the context has a communicator with >1 rank) sum rounded to fp16.
+ * LRU/ATU layers: the hit and miss work lists are the ones the context's most recent
+ * m2c_cache_lookup_fill built, so that call must be for THIS layer (no other lookup and no
+ * m2c_decode_step in between), else M2C_ERR_STATE. */
 m2c_status m2c_sparse_ffn_forward(m2c_ctx *ctx, int32_t layer, const void *x,
                                   const int32_t *tier_ids, const int32_t *slots,
                                   const uint32_t *hit_bitmap, const m2c_tier_plan *plan,
@@ -195,7 +203,8 @@ m2c_status m2c_comm_init(m2c_ctx *ctx, int32_t nranks, int32_t rank, const void 
  *     tokens with the same grid (m2c_set_grid) and be co-resident on their GPUs; a rank that
  *     waits > 5 s for a peer sets error bit 16 and continues (wrong result, never a hang).
  *   m2c_set_grid: CTAs of the context's kernels, 1..SM count (default: SM count).  Two ranks
- *     sharing one GPU (the single-GPU test of this path) use half the SMs each. */
+ *     sharing one GPU (the single-GPU test of this path) use half the SMs each.  Synchronises
+ *     the compute stream and resets the decode kernel's grid-barrier counter. */
 m2c_status m2c_p2p_buffer(m2c_ctx *ctx, uint64_t *dev_ptr_out, void *ipc_handle_out);
 m2c_status m2c_p2p_connect(m2c_ctx *ctx, int32_t nranks, const uint64_t *dev_ptrs,
                            const void *ipc_handles);

@@ -138,6 +138,30 @@ static m2c_status check_plan(const m2c_tier_plan *p, int F_r) {
 
 static bool al16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
+// a device-side invariant violation of an earlier call (flag_error) makes the
+// next host call return M2C_ERR_STATE.  Reads the pinned mirror only (no synchronisation);
+// reporting clears it (the device word keeps the bits for m2c_stats).
+static std::string err_bits_text(uint32_t err) {
+    std::string m;
+    if (err & 1) m += " non-finite input x;";
+    if (err & 4) m += " decode grid-barrier timeout;";
+    if (err & 8) m += " decode select count mismatch;";
+    if (err & 16) m += " p2p exchange timeout (a peer rank is not running);";
+    return m;
+}
+static m2c_status check_device_flag(m2c_ctx *c) {
+    const uint32_t v = c && c->err_host ? *reinterpret_cast<volatile uint32_t *>(c->err_host) : 0u;
+    if (!v) return M2C_OK;
+    *reinterpret_cast<volatile uint32_t *>(c->err_host) = 0;
+    return fail(M2C_ERR_STATE, "device flagged an invariant violation in an earlier call:" +
+                                   err_bits_text(v & 0x7fffffffu));
+}
+#define M2C_CHECK_DEVICE_FLAG(c)                               \
+    do {                                                       \
+        m2c_status _s = check_device_flag(c);                  \
+        if (_s != M2C_OK) return _s;                           \
+    } while (0)
+
 static int32_t *step_ptr(m2c_ctx *c) { return c->ws.counts + 15; }
 
 // ---- the token: all layers on the compute stream (+ copy stream for LRU fills) ----
@@ -283,6 +307,10 @@ static cudaError_t enqueue_layer(m2c_ctx *c, int l, __half *x) {
         if ((e = launch_copy_recs(c, hsrc, c->mstage, p, c->mq, c->mq + 16, c->ident, c->copy))) return e;
         if ((e = mark_copy(c, l, 1))) return e;
         if ((e = cudaEventRecord(c->ev_fill, c->copy))) return e;
+        // the previous layer's scatter (copy stream) reads ws.counts[8..10] and ws.miss_items,
+        // which this k_lru rewrites: join it first (it overlapped that layer's miss FFN, reduce
+        // and this layer's select, so the wait is normally already satisfied)
+        if (c->scat_pending && (e = cudaStreamWaitEvent(st, c->ev_scat, 0))) return e;
         e = launch_lru(c, L, step_ptr(c), c->ws.tier_ids, p, c->ws.slots, c->ws.hit_bits, nullptr, nullptr, st);
         if (e) return e;
         if ((e = cudaEventRecord(c->ev_lookup, st))) return e;
@@ -292,6 +320,7 @@ static cudaError_t enqueue_layer(m2c_ctx *c, int l, __half *x) {
         if ((e = launch_copy_recs(c, ssrc, pdst, p, c->ws.counts, c->ident, c->ws.miss_items, c->copy)))
             return e;
         if ((e = cudaEventRecord(c->ev_scat, c->copy))) return e;
+        c->scat_pending = true;
         e = launch_ffn(c, L, x, c->ws.hit_items, c->ws.counts + 4, p, c->ws.partial, st);
         if (e) return e;
         if ((e = cudaStreamWaitEvent(st, c->ev_fill, 0))) return e;
@@ -382,7 +411,10 @@ static cudaError_t enqueue_token(m2c_ctx *c, __half *x) {
         if ((e = enqueue_layer(c, l, x))) return e;
         early |= c->layers[l].mode != 0 && early_fill_on(c);
     }
-    if (early) return cudaStreamWaitEvent(c->compute, c->ev_scat, 0);  // join the last scatter
+    if (early) {
+        c->scat_pending = false;
+        return cudaStreamWaitEvent(c->compute, c->ev_scat, 0);  // join the last scatter
+    }
     return cudaSuccess;
 }
 
@@ -497,7 +529,7 @@ m2c_status m2c_create(const m2c_model_desc *desc, int32_t device, m2c_stream_t c
                  o_hit = take(4 * (size_t)F_r), o_miss = take(4 * (size_t)F_r),
                  o_mid = take(4 * (size_t)F_r), o_cnt = take(4 * 16),
                  o_part = take(4 * (size_t)2 * c->G * d), o_y = take(4 * (size_t)d),
-                 o_x = take(2 * (size_t)d), o_stats = take(8 * 8), o_err = take(4),
+                 o_x = take(2 * (size_t)d), o_stats = take(8 * 8), o_err = take(16),
                  o_hist = take(4 * 2 * 4096), o_sst = take(8 * (size_t)select_blocks(F_r)),
                  o_sdone = take(4), o_sepoch = take(4), o_bflags = take(4 * (size_t)c->G),
                  o_bepoch = take(4), o_dlay = take(decode_layer_table_bytes(desc->n_layers)),
@@ -559,14 +591,24 @@ m2c_status m2c_create(const m2c_model_desc *desc, int32_t device, m2c_stream_t c
     }
     if (e == cudaSuccess)  // no previous selection yet: -1 disables the prefetch hint
         e = cudaMemset(c->prev_ids, 0xff, 4 * (size_t)desc->n_layers * (plan->k > 0 ? plan->k : 1));
-    static bool attrs_done = false;
-    if (e == cudaSuccess && !attrs_done) {
+    // kernel attributes (max dynamic smem) are per device: set once per device
+    static uint64_t attrs_done = 0;  // bit = device index (< 64)
+    if (e == cudaSuccess && !(device < 64 && ((attrs_done >> device) & 1))) {
         e = init_select_attrs();
         if (e == cudaSuccess) e = init_cache_attrs();
         if (e == cudaSuccess) e = init_ffn_attrs();
         if (e == cudaSuccess) e = init_decode_attrs();
-        attrs_done = e == cudaSuccess;
+        if (e == cudaSuccess && device < 64) attrs_done |= 1ull << device;
     }
+    // the device error word's pinned host mirror (flag_error): the next host call sees it
+    if (e == cudaSuccess) e = cudaHostAlloc(reinterpret_cast<void **>(&c->err_host), 4, cudaHostAllocMapped);
+    if (e == cudaSuccess) {
+        *c->err_host = 0;
+        void *dptr = nullptr;
+        e = cudaHostGetDevicePointer(&dptr, c->err_host, 0);
+        if (e == cudaSuccess) e = cudaMemcpy(c->ws.err + 2, &dptr, sizeof(dptr), cudaMemcpyHostToDevice);
+    }
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_fill_api, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_lookup, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_fill, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_stage, cudaEventDisableTiming);
@@ -607,6 +649,8 @@ m2c_status m2c_destroy(m2c_ctx *c) {
     if (c->p2p_tabs) cudaFree(c->p2p_tabs);
     if (c->p2p_mem) cudaFree(c->p2p_mem);
     if (c->ws_mem) cudaFree(c->ws_mem);
+    if (c->err_host) cudaFreeHost(c->err_host);
+    if (c->ev_fill_api) cudaEventDestroy(c->ev_fill_api);
     delete c;
     return M2C_OK;
 }
@@ -627,6 +671,7 @@ m2c_status m2c_quant_pack(int32_t d, int32_t bits, const void *g, const void *u,
 m2c_status m2c_load_layer(m2c_ctx *c, int32_t layer, const void *g, const void *u, const void *dn,
                           const int8_t *A, const int8_t *B, const m2c_cache_cfg *cfg,
                           void *hbm_region, void *host_region) {
+    M2C_CHECK_DEVICE_FLAG(c);
     if (!c || !cfg || !g || !u || !dn || !A || !B || !hbm_region)
         return fail(M2C_ERR_INVALID_ARG, "load_layer: null argument");
     if (layer < 0 || layer >= c->desc.n_layers) return fail(M2C_ERR_INVALID_ARG, "bad layer");
@@ -702,6 +747,7 @@ m2c_status m2c_load_layer(m2c_ctx *c, int32_t layer, const void *g, const void *
 m2c_status m2c_predict_rank(m2c_ctx *c, int32_t layer, const void *x, const m2c_tier_plan *plan,
                             int32_t *rank_list, int8_t *tier_of, int32_t *tier_ids,
                             int32_t *scores) {
+    M2C_CHECK_DEVICE_FLAG(c);
     if (!c || !x || !plan || (!tier_ids && plan->k > 0))
         return fail(M2C_ERR_INVALID_ARG, "predict_rank: null argument");
     if (layer < 0 || layer >= c->desc.n_layers || !c->layers[layer].loaded)
@@ -722,6 +768,7 @@ m2c_status m2c_cache_lookup_fill(m2c_ctx *c, int32_t layer, int64_t step, const 
                                  const m2c_tier_plan *plan, int32_t *slots, uint32_t *hit_bitmap,
                                  int32_t *miss_log, int32_t *evict_log, int32_t *counts,
                                  m2c_event_t fill_done) {
+    M2C_CHECK_DEVICE_FLAG(c);
     if (!c || !plan || !hit_bitmap || ((!tier_ids || !slots) && plan->k > 0))
         return fail(M2C_ERR_INVALID_ARG, "cache_lookup_fill: null argument");
     if (layer < 0 || layer >= c->desc.n_layers || !c->layers[layer].loaded)
@@ -732,10 +779,10 @@ m2c_status m2c_cache_lookup_fill(m2c_ctx *c, int32_t layer, int64_t step, const 
     if (step <= L.last_step || step > INT32_MAX - 2 || step < 0)
         return fail(M2C_ERR_STATE, "cache_lookup_fill: step must strictly increase (0..2^31-3)");
     cudaStream_t cs = c->compute;
-    const size_t nbits = sizeof(uint32_t) * ((plan->k + 31) / 32 + 1);
+    const size_t nbits = sizeof(uint32_t) * ((plan->k + 31) / 32);  // the documented size exactly
     if (L.mode == 0) {  // resident: identity, all hits
         M2C_CUDA(cudaMemcpyAsync(slots, tier_ids, 4 * (size_t)plan->k, cudaMemcpyDeviceToDevice, cs));
-        M2C_CUDA(cudaMemsetAsync(hit_bitmap, 0, nbits, cs));
+        if (nbits) M2C_CUDA(cudaMemsetAsync(hit_bitmap, 0, nbits, cs));
         if (plan->k) M2C_CUDA(cudaMemsetAsync(hit_bitmap, 0xff, 4 * (size_t)(plan->k / 32), cs));
         if (plan->k % 32) {
             const uint32_t tail = (1u << (plan->k % 32)) - 1;
@@ -753,6 +800,9 @@ m2c_status m2c_cache_lookup_fill(m2c_ctx *c, int32_t layer, int64_t step, const 
         }
         const int32_t st32 = (int32_t)step;
         M2C_CUDA(cudaMemcpyAsync(step_ptr(c), &st32, 4, cudaMemcpyHostToDevice, cs));
+        // an earlier lookup's fill (copy stream) may still read the workspace miss lists that
+        // this k_lru rewrites
+        if (c->fill_pending) M2C_CUDA(cudaStreamWaitEvent(cs, c->ev_fill_api, 0));
         M2C_CUDA(launch_lru(c, L, step_ptr(c), tier_ids, *plan, slots, hit_bitmap, miss_log, evict_log, cs));
         if (counts) {
             M2C_CUDA(cudaMemcpyAsync(counts, c->ws.counts + 8, 12, cudaMemcpyDeviceToDevice, cs));
@@ -761,8 +811,11 @@ m2c_status m2c_cache_lookup_fill(m2c_ctx *c, int32_t layer, int64_t step, const 
         M2C_CUDA(cudaEventRecord(c->ev_lookup, cs));
         M2C_CUDA(cudaStreamWaitEvent(c->copy, c->ev_lookup, 0));
         M2C_CUDA(enqueue_fill(c, layer, *plan));
+        M2C_CUDA(cudaEventRecord(c->ev_fill_api, c->copy));
+        c->fill_pending = true;
         if (fill_done) M2C_CUDA(cudaEventRecord(reinterpret_cast<cudaEvent_t>(fill_done), c->copy));
     }
+    c->ws_lists_layer = layer;  // the hit / miss lists m2c_sparse_ffn_forward will read
     L.last_step = step;
     return M2C_OK;
 }
@@ -771,6 +824,7 @@ m2c_status m2c_sparse_ffn_forward(m2c_ctx *c, int32_t layer, const void *x, cons
                                   const int32_t *slots, const uint32_t *hit_bitmap,
                                   const m2c_tier_plan *plan, m2c_event_t fill_done,
                                   float *y_partial, void *y) {
+    M2C_CHECK_DEVICE_FLAG(c);
     if (!c || !x || !plan || (!tier_ids && plan->k > 0))
         return fail(M2C_ERR_INVALID_ARG, "sparse_ffn_forward: null argument");
     if (layer < 0 || layer >= c->desc.n_layers || !c->layers[layer].loaded)
@@ -781,6 +835,10 @@ m2c_status m2c_sparse_ffn_forward(m2c_ctx *c, int32_t layer, const void *x, cons
     LayerState &L = c->layers[layer];
     if (L.mode != 0 && !hit_bitmap)
         return fail(M2C_ERR_STATE, "LRU/ATU layer: pass the lookup's slots and hit_bitmap");
+    if (hit_bitmap && c->ws_lists_layer != layer)
+        return fail(M2C_ERR_STATE, "sparse_ffn_forward: the context's hit / miss lists belong to "
+                                   "another layer -- call m2c_cache_lookup_fill for this layer "
+                                   "right before its FFN (m2c.h)");
     cudaStream_t cs = c->compute;
     const __half *xh = (const __half *)x;
     const int d = c->desc.d_model;
@@ -854,6 +912,11 @@ m2c_status m2c_set_grid(m2c_ctx *c, int32_t ctas) {
         cudaGraphExecDestroy(c->graph);
         c->graph = nullptr;
     }
+    // k_decode's grid barrier waits for (epoch + n) * G arrivals on one counter: a new G needs
+    // a fresh counter (after every launch of the old grid has drained)
+    M2C_CUDA(cudaStreamSynchronize(c->compute));
+    M2C_CUDA(cudaMemset(c->bar_flags, 0, 4 * (size_t)c->num_sms));
+    M2C_CUDA(cudaMemset(c->bar_epoch, 0, 4));
     c->G = ctas;
     return M2C_OK;
 }
@@ -932,6 +995,7 @@ m2c_status m2c_set_fused(m2c_ctx *c, int32_t enable) {
 }
 
 m2c_status m2c_decode_step(m2c_ctx *c, void *x_inout, int64_t step) {
+    M2C_CHECK_DEVICE_FLAG(c);
     if (!c || !x_inout) return fail(M2C_ERR_INVALID_ARG, "decode_step: null argument");
     if (!al16(x_inout)) return fail(M2C_ERR_INVALID_ARG, "x must be 16-B aligned");
     bool any_lru = false;
@@ -955,6 +1019,10 @@ m2c_status m2c_decode_step(m2c_ctx *c, void *x_inout, int64_t step) {
         M2C_CUDA(cudaMemcpyAsync(step_ptr(c), &st32, 4, cudaMemcpyHostToDevice, cs));
     }
     __half *x = static_cast<__half *>(x_inout);
+    if (c->fill_pending) {  // a per-call lookup's fill may still read the workspace miss lists
+        M2C_CUDA(cudaStreamWaitEvent(cs, c->ev_fill_api, 0));
+        c->fill_pending = false;
+    }
     if (c->dec_table_dirty) {  // pool / predictor pointers of every layer for k_decode
         M2C_CUDA(cudaStreamSynchronize(cs));
         M2C_CUDA(decode_write_layer_table(c, c->dec_layers));
@@ -991,10 +1059,12 @@ m2c_status m2c_decode_step(m2c_ctx *c, void *x_inout, int64_t step) {
     for (int l = 0; l < c->desc.n_layers; l++)
         if (c->layers[l].mode != 0) c->layers[l].last_step = step;
     c->decoded = true;
+    c->ws_lists_layer = -1;  // the engine reused the workspace lists
     return M2C_OK;
 }
 
 m2c_status m2c_decode_lists(m2c_ctx *c, int32_t layer, int32_t *tier_ids_out) {
+    M2C_CHECK_DEVICE_FLAG(c);
     if (!c || !tier_ids_out) return fail(M2C_ERR_INVALID_ARG, "decode_lists: null argument");
     if (layer < 0 || layer >= c->desc.n_layers) return fail(M2C_ERR_INVALID_ARG, "bad layer");
     if (c->layers[layer].mode != 0 || !c->decoded)
@@ -1023,6 +1093,7 @@ m2c_status m2c_profile(m2c_ctx *c, int32_t enable) {
 }
 
 m2c_status m2c_profile_read(m2c_ctx *c, float *ms, int32_t *ffn_launches) {
+    M2C_CHECK_DEVICE_FLAG(c);
     if (!c || !ms) return fail(M2C_ERR_INVALID_ARG, "null argument");
     if (c->prof_ev.empty()) return fail(M2C_ERR_STATE, "profiling not enabled");
     M2C_CUDA(cudaStreamSynchronize(c->compute));
@@ -1088,6 +1159,7 @@ m2c_status m2c_profile_stamps(m2c_ctx *c, uint64_t *out, int64_t cap, int64_t *n
 
 m2c_status m2c_predict_candidates(m2c_ctx *c, int32_t layer, const void *x, int32_t n_cand,
                                   int64_t *keys_out) {
+    M2C_CHECK_DEVICE_FLAG(c);
     if (!c || !x || !keys_out) return fail(M2C_ERR_INVALID_ARG, "predict_candidates: null argument");
     if (layer < 0 || layer >= c->desc.n_layers || !c->layers[layer].loaded)
         return fail(M2C_ERR_STATE, "predict_candidates: layer not loaded");
@@ -1104,6 +1176,7 @@ m2c_status m2c_predict_candidates(m2c_ctx *c, int32_t layer, const void *x, int3
 
 m2c_status m2c_select_global(m2c_ctx *c, const int64_t *keys_all, int32_t n_cand,
                              const m2c_tier_plan *global_plan, int32_t *tier_ids_out, int32_t *counts_out) {
+    M2C_CHECK_DEVICE_FLAG(c);
     if (!c || !keys_all || !global_plan || !tier_ids_out || !counts_out)
         return fail(M2C_ERR_INVALID_ARG, "select_global: null argument");
     const int P = c->desc.shard_count;
@@ -1260,14 +1333,10 @@ m2c_status m2c_stats(m2c_ctx *c, int64_t *kpt, int64_t hits[3], int64_t misses[3
         if (misses) misses[t] = (int64_t)h[3 + t];
     }
     if (reset) M2C_CUDA(cudaMemset(c->ws.stats, 0, sizeof(h)));
+    if (c->err_host) *reinterpret_cast<volatile uint32_t *>(c->err_host) = 0;
     if (err) {
         cudaMemset(c->ws.err, 0, 4);
-        std::string m = "device flagged:";
-        if (err & 1) m += " non-finite input x;";
-        if (err & 4) m += " decode grid-barrier timeout;";
-        if (err & 8) m += " decode select count mismatch;";
-        if (err & 16) m += " p2p exchange timeout (a peer rank is not running);";
-        return fail(M2C_ERR_STATE, m);
+        return fail(M2C_ERR_STATE, "device flagged:" + err_bits_text(err));
     }
     return M2C_OK;
 }

@@ -349,7 +349,8 @@ cudaError_t launch_lru(m2c_ctx *c, LayerState &L, const int32_t *step_dev, const
         while (P2 < L.cap[t] || P2 < cnt[t]) P2 <<= 1;
         maxcnt = cnt[t] > maxcnt ? cnt[t] : maxcnt;
     }
-    cudaError_t e = cudaMemsetAsync(hit_bits, 0, sizeof(uint32_t) * ((p.k + 31) / 32 + 1), st);
+    // exactly ceil(k/32) words: hit_bits may be the caller's buffer (m2c.h documents that size)
+    cudaError_t e = p.k > 0 ? cudaMemsetAsync(hit_bits, 0, sizeof(uint32_t) * ((p.k + 31) / 32), st) : cudaSuccess;
     if (e != cudaSuccess) return e;
     const size_t smem = lru_smem_bytes(P2, maxcnt);
     e = launch_k(k_lru, dim3(3), dim3(NT), smem, st, a, step_dev, tier_ids, slots, hit_bits,

@@ -146,7 +146,7 @@ __device__ __forceinline__ void grid_sync(unsigned *counter, unsigned target, ui
         while ((int)(ld_acquire(counter) - want) < 0) {
 #endif
             if (gtimer() - t0 > 2000000000ull) {
-                atomicOr(err, 4u);
+                flag_error(err, 4u);
                 break;
             }
         }
@@ -320,7 +320,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
                 p.x[ch * 32 + tid] = xv;
             }
             fp16_fixed(__half_as_ushort(xv), m, sh, bad);
-            if (bad) atomicOr(p.err, 1u);
+            if (bad) flag_error(p.err, 1u);
             xm[tid] = m;
             xsh[tid] = sh;
         }
@@ -492,7 +492,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
             }
             const unsigned who = __ballot_sync(0xffffffffu, cbin >= 0);
             if (!who) {  // histogram total < target: cannot happen with a consistent plan
-                if (lane == 0) atomicOr(p.err, 8u);
+                if (lane == 0) flag_error(p.err, 8u);
                 continue;
             }
             const int src = __ffs(who) - 1;
@@ -607,7 +607,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
             for (int t = warp; t < 3; t += NW) {
                 const int m = ncand[t];
                 if (tg(t) <= 0 || m > kCand) continue;
-                if (ccnt[t] != m && lane == 0) atomicOr(p.err, 8u);
+                if (ccnt[t] != m && lane == 0) flag_error(p.err, 8u);
                 const int2 c0 = lane < m ? cand[t * kCand + lane] : make_int2(0, 0);
                 const int2 c1 = lane + 32 < m ? cand[t * kCand + lane + 32] : make_int2(0, 0);
                 int r0 = 0, r1 = 0;
@@ -753,7 +753,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
                     e1 += qv[u].y - qv[u].x;
                     e2 += qv[u].z - qv[u].y;
                 }
-                if (lane == 31 && (i0 != p.k16 || i1 != p.k8 || i2 != p.k4)) atomicOr(p.err, 8u);
+                if (lane == 31 && (i0 != p.k16 || i1 != p.k8 || i2 != p.k4)) flag_error(p.err, 8u);
             }
             __syncthreads();
             STAMP(19);
@@ -919,7 +919,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
                                 do {
                                     w = ld_relaxed_sys_u64(mine + (size_t)q * d);
                                     if (gtimer() - t0 > 5000000000ull) {
-                                        atomicOr(p.err, 16u);
+                                        flag_error(p.err, 16u);
                                         break;
                                     }
                                 } while ((unsigned)(w >> 32) != flag);
@@ -934,7 +934,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
                         bool bad = false;
                         int m, sh;
                         fp16_fixed(__half_as_ushort(xn), m, sh, bad);
-                        if (bad) atomicOr(p.err, 1u);
+                        if (bad) flag_error(p.err, 1u);
                         xm[lane] = m;
                         xsh[lane] = sh;
                     }

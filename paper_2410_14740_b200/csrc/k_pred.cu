@@ -50,7 +50,7 @@ __global__ void __launch_bounds__(kHThreads) k_pred_h(int d, int r, const __half
         bool bad = false;
         int m, sh;
         fp16_fixed(b, m, sh, bad);
-        if (bad) atomicOr(err, 1u);  // Inf / NaN input: flagged, contributes 0
+        if (bad) flag_error(err, 1u);  // Inf / NaN input: flagged, contributes 0
         xm[threadIdx.x] = m;
         xsh[threadIdx.x] = sh;
     }

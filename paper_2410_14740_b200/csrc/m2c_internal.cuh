@@ -73,7 +73,8 @@ struct Workspace {
     float *y32 = nullptr;          // [d]
     __half *xbuf = nullptr;        // [d]
     unsigned long long *stats = nullptr;  // [8] hits[3], misses[3], staged fills, - (cumulative)
-    uint32_t *err = nullptr;       // device error flag
+    uint32_t *err = nullptr;       // device error flag word; err + 2 holds the host mirror's
+                                   // device address (flag_error)
 };
 
 }  // namespace m2c
@@ -155,6 +156,14 @@ struct m2c_ctx {
     unsigned *p2p_rounds = nullptr;
     void *p2p_tabs = nullptr;
     std::vector<void *> p2p_opened;   // IPC-opened peer bases (closed at destroy)
+    // device error flag mirrored into pinned host memory (checked by every host call)
+    uint32_t *err_host = nullptr;
+    // early-fill engine: the last layer's scatter (copy stream) still reads the miss lists
+    bool scat_pending = false;
+    // per-call API: layer whose hit / miss lists the last m2c_cache_lookup_fill left in ws
+    int ws_lists_layer = -1;
+    bool fill_pending = false;        // per-call API: a miss fill still reads the ws miss lists
+    cudaEvent_t ev_fill_api = nullptr;
     // multi-GPU
     m2c::NcclApi *nccl = nullptr;
     void *comm = nullptr;
@@ -375,6 +384,16 @@ __device__ __forceinline__ void fp16_fixed(unsigned b, int &m, int &sh, bool &ba
         sh = e - 1;
     }
     if (b & 0x8000) m = -m;
+}
+// Device-side invariant violation: set `bit` in the context's device error word and mirror
+// it into the pinned host word whose address the context stores right after it (ws.err + 2),
+// so the NEXT host call on the context returns M2C_ERR_STATE without synchronising
+// (SURVEY §8(b)).  err bits: 1 non-finite x, 4 grid-barrier timeout, 8 select count
+// mismatch, 16 p2p exchange timeout.
+__device__ __forceinline__ void flag_error(uint32_t *err, unsigned bit) {
+    atomicOr(err, bit);
+    uint32_t *mirror = *reinterpret_cast<uint32_t *const *>(err + 2);
+    if (mirror) *reinterpret_cast<volatile uint32_t *>(mirror) = 0x80000000u | bit;
 }
 __device__ __forceinline__ void red_add_u64(long long *p, long long v) {
     asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
