@@ -7,11 +7,14 @@ mixed-precision FFN decode step (M2Cache, arXiv 2410.14740) on B200.
 
 A step = one decode token through the whole synthetic FFN stack (all L layers: predictor,
 top-k + tier split, cache lookup/fill, fused dequant-GEMV FFN, reduce/all-reduce, residual).
-N = 1 default workload: configs[1], the LLaMA-2-7B-shaped stack (32 x 4096 x 11008), whole
-model resident.  N > 1 (torchrun): configs[3], the 70B-shaped stack with d_ff sharded over
-the N ranks (one NCCL all-reduce per layer), total work fixed ("strong").
-Prints ONE JSON line (rank 0).  --impl reference times the CPU oracle instead (the tier's
-reference arm).
+Default workload at EVERY N (BASELINE metric "... 1/2/4/8 B200" = configs[3]): the
+LLaMA-2-70B-shaped FFN stack (8192 x 28672, 10% active, FP16/INT8/INT4 1:1:2) at the depth
+that fits one B200 (40 layers; all 80 layers x 3 tiers = 200 GB do not), d_ff sharded over
+the N ranks (one exchange of the down-projection partials per layer), total work fixed
+("strong").  S7 / S13 / S70 / T are --config lines (profiles/).
+`--gpus N` without a torchrun environment re-launches itself under torch.distributed.run
+(one process per GPU, 127.0.0.1 rendezvous).  Prints ONE JSON line (rank 0).
+--impl reference times the CPU oracle instead (the tier's reference arm).
 """
 from __future__ import annotations
 
@@ -36,8 +39,9 @@ WORKLOAD = {
            "HBM neuron cache capped at 25% of FFN FP16 bytes, LRU misses filled from pinned host",
     "S70": "configs[3]: LLaMA-2-70B-shaped FFN stack 80 x (8192 x 28672), 10% active 1:1:2, "
            "d_ff sharded over the ranks, NCCL all-reduce of down-projection partials",
-    "S70H": "configs[3] at 1 GPU: 40-layer half-depth 70B-shaped stack (all 80 layers x 3 tiers "
-            "= 199.9 GB exceed one B200)",
+    "S70H": "configs[3] shape: LLaMA-2-70B-shaped FFN stack (8192 x 28672), 40 layers (the depth "
+            "one B200 holds: 80 layers x 3 tiers = 199.9 GB), 10% active 1:1:2, resident, d_ff "
+            "sharded over the N GPUs (one all-reduce of the down-projection partials per layer)",
 }
 
 
@@ -146,27 +150,60 @@ def oracle_sample(cfg, P, layers, tokens, device_weights=None, threads=1):
                       f"scaled x{cfg.n_layers} layers per token"
 
 
-def run_reference(args, world, rank):
-    """--impl reference: the tier's reference arm is the CPU oracle (it runs on host cores)."""
+def workload(args, world):
+    """(config, shard count) of the run: S70H sharded over the N ranks unless --config says
+    otherwise; the sharded configs are S70H and S70 (80 layers, N >= 2)."""
     from synth import get_config
+    cfg = get_config(args.config or "S70H")
+    if cfg.name == "S70" and world == 1:
+        cfg = get_config("S70H")
+    P = world if cfg.name in ("S70", "S70H") else 1
+    if world > 1 and P == 1:
+        raise SystemExit(f"--config {cfg.name} is a single-GPU workload; use S70H / S70 at N > 1")
+    return cfg, P
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the tier's reference arm is the CPU oracle (it runs on host cores;
+    under torchrun only rank 0 works)."""
     if rank != 0:
         return
-    cfg = get_config(args.config or ("S7" if world == 1 else "S70"))
-    P = world if cfg.name == "S70" else 1
-    steps = max(1, min(args.steps, 64))
+    cfg, P = workload(args, world)
+    steps = max(1, min(args.steps, 16 if cfg.d_model >= 8192 else 64))
     per, sample = oracle_sample(cfg, P, 1, max(1, min(args.warmup, 2)) + steps)
+    # whole job: the P shards' (token, layer) work, one after another on the host, x L layers
+    per *= P
     value = 1.0 / (per * cfg.n_layers)
+    if P > 1:
+        sample += f"; x{P} shards (shard 0 timed)"
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s",
             "n_gpus": world, "steps": steps, "warmup": args.warmup,
             "ms_per_step": per * 1e3, "higher_is_better": True,
             "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded; SURVEY §8(d) recipe)",
-            "config": {"workload": WORKLOAD[cfg.name], "model": cfg.name},
+            "config": {"workload": WORKLOAD[cfg.name], "model": cfg.name, "layers": cfg.n_layers,
+                       "d_model": cfg.d_model, "d_ff": cfg.d_ff, "active_pct": cfg.active_pct,
+                       "parallelism": f"dff-shard{P}" if P > 1 else "single"},
             "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": 1, "kind": "oracle",
                              "sample": sample + "; each step = one (token, layer)"},
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def relaunch(args):
+    """`python bench.py --gpus N` outside torchrun: one process per GPU under
+    torch.distributed.run on 127.0.0.1 (rank 0 prints the line)."""
+    import socket
+    import subprocess
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    sys.exit(subprocess.call(cmd))
 
 
 def main():
@@ -191,6 +228,8 @@ def main():
     ap.add_argument("--lookahead", action="store_true",
                     help="NEXT-2: stage layer l+1's predicted misses during layer l (LRU/ATU configs)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(args)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -210,10 +249,7 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    cfg = get_config(args.config or ("S7" if world == 1 else "S70"))
-    P = world if world > 1 else 1
-    if cfg.name == "S70" and P == 1:
-        cfg = get_config("S70H")
+    cfg, P = workload(args, world)
     plan = plan_of(cfg, P)
     ctx = M2CContext(cfg.d_model, cfg.d_ff, cfg.n_layers, cfg.pred_rank, plan, shard=(rank, P),
                      act=0 if cfg.act == "silu" else 1, device=local)
@@ -324,7 +360,7 @@ def main():
     tok_s = K / (ms / 1e3)
     ab = algorithmic_bytes(cfg, plan, P)
     peak, peak_src = _peaks()
-    gbs = ab["token"] * K / (ms / 1e3) / 1e9 * P / P  # per-GPU bytes x tokens / time
+    gbs = ab["token"] * K / (ms / 1e3) / 1e9  # one rank's algorithmic bytes per token x tokens / time
 
     # ---- phase breakdown + dominant-kernel roofline ----
     fused = kpt == 1  # the persistent decode kernel k_decode is the whole token
@@ -448,15 +484,22 @@ def main():
         torch.cuda.synchronize()
         ar_us = m2c_dist.max_over_ranks(a0.elapsed_time(a1) * 10.0, dev)  # ms/100 -> us
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        per, sample = oracle_sample(cfg, P, 1, 12)
-        cpu = {"value": 1.0 / (per * cfg.n_layers), "unit": "tokens/s", "cores": 1,
-               "kind": "oracle", "sample": sample}
+    if rank == 0 and not args.no_cpu_baseline:
+        # the oracle as it stands on this box's host cores, bounded sample; at N > 1 in shard
+        # mode (rank 0's slice: SURVEY 8(d) "1 token in shard mode"), tokens/s of the whole
+        # job = 1 / (P x per-(token, layer, shard) time x L) -- the shards would run one after
+        # another on the same host
+        ntok = 12 if world == 1 else 3
+        per, sample = oracle_sample(cfg, P, 1, ntok)
+        cpu = {"value": 1.0 / (per * cfg.n_layers * P), "unit": "tokens/s", "cores": 1,
+               "kind": "oracle", "sample": sample + (f"; x{P} shards" if P > 1 else "")}
         nthr = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
-        if nthr and nthr > 1:  # also the oracle's OpenMP variant on all host cores
-            per_mt, sample_mt = oracle_sample(cfg, P, 1, 12, threads=nthr)
+        if nthr and nthr > 1 and world == 1:  # also its OpenMP variant, all cores
+            per_mt, sample_mt = oracle_sample(cfg, P, 1, ntok, threads=nthr)
             cpu["all_cores"] = {"value": 1.0 / (per_mt * cfg.n_layers), "cores": nthr,
                                 "sample": sample_mt}
+    if world > 1:
+        dist.barrier()  # the other ranks wait for rank 0's oracle sample
 
     if rank == 0:
         hits, miss = st["hits"], st["misses"]
@@ -471,7 +514,10 @@ def main():
                        "cache": cfg.cache_mode, "global_batch": 1, "seq_len": 1,
                        "parallelism": f"dff-shard{P}" if P > 1 else "single",
                        "topk": ("global" if args.global_topk else "shard-local") if P > 1 else "global",
-                       "l2": "inputs larger than L2 (%.0f MB touched per token)" % (ab["token"] / 1e6),
+                       "l2": ("inputs larger than L2 (%.0f MB touched per token per GPU > 126 MB L2; "
+                              "no flush needed)" if ab["token"] > 126e6 else
+                              "working set (%.0f MB per token) fits the 126 MB L2 and is NOT flushed: "
+                              "information only, not a bench line") % (ab["token"] / 1e6),
                        "graph": not args.eager, "persistent_kernel": fused,
                        "engine": ("k_decode" + (" + fused p2p all-reduce" if allreduce == "p2p" else ""))
                        if fused else ("k_decode layer-split" if split else "kernel chain"),
