@@ -215,11 +215,25 @@ m2c_status m2c_set_grid(m2c_ctx *ctx, int32_t ctas);
  * x_{l+1} = fp16(x_l + fp16(y_l)) (R14).  step: strictly increasing (LRU timestamps). */
 m2c_status m2c_decode_step(m2c_ctx *ctx, void *x_inout, int64_t step);
 
-/* The tier lists the last m2c_decode_step selected for resident layer `layer`: int32 [k],
- * three ascending segments k16 | k8 | k4 (the layout of m2c_predict_rank's tier_ids), copied
- * to the device buffer tier_ids_out on the compute stream.  M2C_ERR_STATE for an LRU/ATU layer
- * (its lists are not kept per layer) or before the first decode step. */
+/* The tier lists the last m2c_decode_step selected for layer `layer` (any cache mode): int32
+ * [k], three ascending segments k16 | k8 | k4 (the layout of m2c_predict_rank's tier_ids),
+ * written to the device buffer tier_ids_out on the compute stream.  M2C_ERR_STATE before the
+ * first decode step; M2C_ERR_CAPACITY if a tier has more than 32768 entries. */
 m2c_status m2c_decode_lists(m2c_ctx *ctx, int32_t layer, int32_t *tier_ids_out);
+
+/* Parity trace (the replay harness): with device buffers x_trace fp16
+ * [n_layers + 1][d] and y_trace fp32 [n_layers][d] set (caller-owned; NULL, NULL disables),
+ * every later m2c_decode_step also writes each layer's input x_l, the final x_L, and each
+ * layer's output y_l (after the all-reduce when sharded) before its fp16 rounding.  Every
+ * engine writes the same quantities; the decode graph is re-captured. */
+m2c_status m2c_set_trace(m2c_ctx *ctx, void *x_trace, float *y_trace);
+
+/* LRU/ATU pool state of (layer, tier) (R7, oracle O7): occupant_out int32 [cap] (-1 = empty)
+ * and last_out int32 [cap] (step of the last use, -1 = never), device buffers (either may be
+ * NULL), copied asynchronously on the compute stream; *cap_out = the pool's slot count.
+ * M2C_ERR_STATE for a resident layer. */
+m2c_status m2c_cache_state(m2c_ctx *ctx, int32_t layer, int32_t tier, int32_t *occupant_out,
+                           int32_t *last_out, int32_t *cap_out);
 
 /* Disables (0) or enables (1, default) CUDA-graph capture of m2c_decode_step. */
 m2c_status m2c_set_graph(m2c_ctx *ctx, int32_t enable);

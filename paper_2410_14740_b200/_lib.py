@@ -65,6 +65,8 @@ SIGNATURES = [
     ("m2c_decode_step", C.c_int, [_vp, _vp, _i64]),
     ("m2c_decode_lists", C.c_int, [_vp, _i32, _vp]),
     ("m2c_set_graph", C.c_int, [_vp, _i32]),
+    ("m2c_set_trace", C.c_int, [_vp, _vp, _vp]),
+    ("m2c_cache_state", C.c_int, [_vp, _i32, _i32, _vp, _vp, _P(_i32)]),
     ("m2c_set_fused", C.c_int, [_vp, _i32]),
     ("m2c_stats", C.c_int, [_vp, _P(_i64), _P(_i64), _P(_i64), _i32]),
     ("m2c_profile", C.c_int, [_vp, _i32]),

@@ -298,6 +298,27 @@ class M2CContext:
         self._call(lib().m2c_decode_lists, self._h, layer, _ptr(out))
         return out[:self.plan.k]
 
+    def set_trace(self, enable: bool = True):
+        """Parity trace (D9): afterwards every decode_step records x_l [L+1, d] fp16 and y_l
+        [L, d] f32 into ``self.trace_x`` / ``self.trace_y`` (device tensors owned here)."""
+        L, d = self.desc.n_layers, self.desc.d_model
+        if enable:
+            self.trace_x = torch.zeros(L + 1, d, dtype=torch.float16, device=self.device)
+            self.trace_y = torch.zeros(L, d, dtype=torch.float32, device=self.device)
+            check(lib().m2c_set_trace(self._h, _ptr(self.trace_x), _ptr(self.trace_y)))
+        else:
+            check(lib().m2c_set_trace(self._h, None, None))
+            self.trace_x = self.trace_y = None
+
+    def cache_state(self, layer, tier):
+        """LRU/ATU pool state of (layer, tier): (occupant int32 [cap], last_use int32 [cap])."""
+        cap = C.c_int32()
+        check(lib().m2c_cache_state(self._h, layer, tier, None, None, C.byref(cap)))
+        occ = torch.empty(max(cap.value, 1), dtype=torch.int32, device=self.device)
+        last = torch.empty(max(cap.value, 1), dtype=torch.int32, device=self.device)
+        check(lib().m2c_cache_state(self._h, layer, tier, _ptr(occ), _ptr(last), C.byref(cap)))
+        return occ[:cap.value], last[:cap.value]
+
     def set_graph(self, enable: bool):
         check(lib().m2c_set_graph(self._h, 1 if enable else 0))
 

@@ -191,11 +191,8 @@ static cudaError_t enqueue_fill(m2c_ctx *c, int l, const m2c_tier_plan &p, int s
     return e;
 }
 
-// k_decode's P2/P3 (predictor + distributed exact select) fit: the same shape bounds
-static bool decode_select_ok(const m2c_ctx *c) {
-    const int rps = (c->F_r + c->G - 1) / c->G;
-    return c->F_r <= decode_max_F() && rps <= c->desc.d_model / 8 && rps <= 254;
-}
+// k_decode's P2/P3 (predictor + distributed exact select) and FFN share fit the kernel
+static bool decode_select_ok(const m2c_ctx *c) { return decode_shape_ok(c); }
 
 // the early-fill LRU engine: not with the NEXT-2 lookahead or a NEXT-1 store (their fills
 // have their own sources); M2C_EARLY_FILL=0 disables it (A/B knob, results identical)
@@ -239,8 +236,11 @@ static cudaError_t enqueue_layer(m2c_ctx *c, int l, __half *x) {
     // The lists of layer l persist to the next token as its prefetch hint.
     int32_t *lists = c->prev_ids + (size_t)l * (p.k > 0 ? p.k : 1);
     const bool prefetch = L.mode == 0 && c->use_fused;
-    int32_t *ids = L.mode == 0 ? lists : c->ws.tier_ids;
+    int32_t *ids = lists;  // this layer's tier lists (kept per layer: m2c_decode_lists)
     if ((e = mark(c, l, 0))) return e;
+    if (c->trace_x && (e = cudaMemcpyAsync(c->trace_x + (size_t)l * c->desc.d_model, x, 2 * (size_t)c->desc.d_model,
+                                           cudaMemcpyDeviceToDevice, st)))
+        return e;
     if (L.mode != 0 && c->lookahead && !c->store && l + 1 < c->desc.n_layers) {
         // NEXT-2: predict layer l+1's selection from x_l first, and stage its would-be
         // misses on the staging stream (its own PCIe transfer, concurrent with this layer's)
@@ -276,6 +276,9 @@ static cudaError_t enqueue_layer(m2c_ctx *c, int l, __half *x) {
         if (c->nccl->allReduce(c->ws.y32, c->ws.y32, (size_t)c->desc.d_model, 7 /*f32*/, 0 /*sum*/, c->comm, st) != 0)
             return cudaErrorUnknown;
         if ((e = launch_finalize(c, c->ws.y32, x, nullptr, x, st))) return e;
+        if (c->trace_y && (e = cudaMemcpyAsync(c->trace_y + (size_t)l * c->desc.d_model, c->ws.y32,
+                                               4 * (size_t)c->desc.d_model, cudaMemcpyDeviceToDevice, st)))
+            return e;
         return mark(c, l, 4);
     }
     if (L.mode != 0 && c->use_fused && decode_select_ok(c)) {
@@ -283,6 +286,8 @@ static cudaError_t enqueue_layer(m2c_ctx *c, int l, __half *x) {
         if ((e = launch_decode(c, x, c->prof_ev.empty() ? nullptr : c->dec_prof, st, l, 1, nullptr,
                                nullptr, ids)))
             return e;
+        // (rank order -> ascending ids per tier: the order the LRU update pairs misses in, R7)
+        if ((e = launch_sort_tiers(c, ids, p, st))) return e;
         if ((e = mark(c, l, 1))) return e;
         if ((e = mark(c, l, 2))) return e;
     } else {
@@ -299,7 +304,7 @@ static cudaError_t enqueue_layer(m2c_ctx *c, int l, __half *x) {
         // early fill: the misses (ids without a slot) are queued first and their host-tier
         // copies start into the staging area while k_lru chooses the victims; the miss FFN
         // reads the staging area; the copy stream then scatters the records into their slots
-        if ((e = launch_missq(c, L, c->ws.tier_ids, p, st))) return e;
+        if ((e = launch_missq(c, L, ids, p, st))) return e;
         if ((e = cudaEventRecord(c->ev_q, st))) return e;
         if ((e = cudaStreamWaitEvent(c->copy, c->ev_q, 0))) return e;
         if ((e = mark_copy(c, l, 0))) return e;
@@ -311,7 +316,7 @@ static cudaError_t enqueue_layer(m2c_ctx *c, int l, __half *x) {
         // which this k_lru rewrites: join it first (it overlapped that layer's miss FFN, reduce
         // and this layer's select, so the wait is normally already satisfied)
         if (c->scat_pending && (e = cudaStreamWaitEvent(st, c->ev_scat, 0))) return e;
-        e = launch_lru(c, L, step_ptr(c), c->ws.tier_ids, p, c->ws.slots, c->ws.hit_bits, nullptr, nullptr, st);
+        e = launch_lru(c, L, step_ptr(c), ids, p, c->ws.slots, c->ws.hit_bits, nullptr, nullptr, st);
         if (e) return e;
         if ((e = cudaEventRecord(c->ev_lookup, st))) return e;
         if ((e = cudaStreamWaitEvent(c->copy, c->ev_lookup, 0))) return e;
@@ -330,7 +335,7 @@ static cudaError_t enqueue_layer(m2c_ctx *c, int l, __half *x) {
         if (e) return e;
         np = 2 * c->G;
     } else {
-        e = launch_lru(c, L, step_ptr(c), c->ws.tier_ids, p, c->ws.slots, c->ws.hit_bits, nullptr, nullptr, st);
+        e = launch_lru(c, L, step_ptr(c), ids, p, c->ws.slots, c->ws.hit_bits, nullptr, nullptr, st);
         if (e) return e;
         if ((e = cudaEventRecord(c->ev_lookup, st))) return e;
         if ((e = cudaStreamWaitEvent(c->copy, c->ev_lookup, 0))) return e;
@@ -358,8 +363,12 @@ static cudaError_t enqueue_layer(m2c_ctx *c, int l, __half *x) {
                                    0 /*sum*/, c->comm, st);
         if (r != 0) return cudaErrorUnknown;
         if ((e = launch_finalize(c, c->ws.y32, x, nullptr, x, st))) return e;
+        if (c->trace_y && (e = cudaMemcpyAsync(c->trace_y + (size_t)l * c->desc.d_model, c->ws.y32,
+                                               4 * (size_t)c->desc.d_model, cudaMemcpyDeviceToDevice, st)))
+            return e;
     } else {
-        if ((e = launch_reduce(c, np, c->ws.partial, x, nullptr, nullptr, x, nullptr, st))) return e;
+        float *ytr = c->trace_y ? c->trace_y + (size_t)l * c->desc.d_model : nullptr;
+        if ((e = launch_reduce(c, np, c->ws.partial, x, ytr, nullptr, x, nullptr, st))) return e;
     }
     return mark(c, l, 4);
 }
@@ -367,9 +376,8 @@ static cudaError_t enqueue_layer(m2c_ctx *c, int l, __half *x) {
 // the persistent decode kernel covers a resident, unsharded stack whose scores fit in smem
 static bool decode_fused(const m2c_ctx *c) {
     const int rps = (c->F_r + c->G - 1) / c->G;  // a CTA's own neurons: one pass of its threads
-    if (!c->use_fused || (c->comm && !c->p2p) || c->F_r > decode_max_F() ||
-        rps > c->desc.d_model / 8 || rps > 254)
-        return false;
+    (void)rps;
+    if (!c->use_fused || (c->comm && !c->p2p) || !decode_shape_ok(c)) return false;
     for (const LayerState &L : c->layers)
         if (L.mode != 0) return false;
     return true;
@@ -380,7 +388,8 @@ static bool decode_fused(const m2c_ctx *c) {
 static bool decode_split(const m2c_ctx *c) {
     if (!c->use_fused || c->global_topk || (!c->comm && !c->force_split)) return false;
     const int rps = (c->F_r + c->G - 1) / c->G;
-    if (c->F_r > decode_max_F() || rps > c->desc.d_model / 8 || rps > 254) return false;
+    (void)rps;
+    if (!decode_shape_ok(c)) return false;
     for (const LayerState &L : c->layers)
         if (L.mode != 0) return false;
     return true;
@@ -395,13 +404,20 @@ static cudaError_t enqueue_token(m2c_ctx *c, __half *x) {
     if (c->last_token_split) {
         unsigned long long *prof = c->prof_ev.empty() ? nullptr : c->dec_prof;
         cudaError_t e;
+        const size_t d = c->desc.d_model;
         for (int l = 0; l < c->desc.n_layers; l++) {
             if ((e = launch_decode(c, x, prof, c->compute, l, 1, l > 0 ? c->ws.y32 : nullptr, c->ws.y32))) return e;
-            if (c->comm && c->nccl->allReduce(c->ws.y32, c->ws.y32, (size_t)c->desc.d_model, 7 /*f32*/,
+            if (c->comm && c->nccl->allReduce(c->ws.y32, c->ws.y32, d, 7 /*f32*/,
                                                     0 /*sum*/, c->comm, c->compute) != 0)
                 return cudaErrorUnknown;
+            if (c->trace_y && (e = cudaMemcpyAsync(c->trace_y + l * d, c->ws.y32, 4 * d,
+                                                   cudaMemcpyDeviceToDevice, c->compute)))
+                return e;
         }
-        return launch_finalize(c, c->ws.y32, x, nullptr, x, c->compute);
+        if ((e = launch_finalize(c, c->ws.y32, x, nullptr, x, c->compute))) return e;
+        if (c->trace_x)
+            return cudaMemcpyAsync(c->trace_x + c->desc.n_layers * d, x, 2 * d, cudaMemcpyDeviceToDevice, c->compute);
+        return cudaSuccess;
     }
     cudaError_t e = launch_set_counts(c->ws.counts, p.k_fp16, p.k_int8, p.k_int4, c->compute);
     c->launch_counter++;
@@ -411,6 +427,10 @@ static cudaError_t enqueue_token(m2c_ctx *c, __half *x) {
         if ((e = enqueue_layer(c, l, x))) return e;
         early |= c->layers[l].mode != 0 && early_fill_on(c);
     }
+    if (c->trace_x &&
+        (e = cudaMemcpyAsync(c->trace_x + (size_t)c->desc.n_layers * c->desc.d_model, x,
+                             2 * (size_t)c->desc.d_model, cudaMemcpyDeviceToDevice, c->compute)))
+        return e;
     if (early) {
         c->scat_pending = false;
         return cudaStreamWaitEvent(c->compute, c->ev_scat, 0);  // join the last scatter
@@ -536,7 +556,7 @@ m2c_status m2c_create(const m2c_model_desc *desc, int32_t device, m2c_stream_t c
                  o_dprof = take(8 * (size_t)kDecodeStamps * c->G * desc->n_layers),
                  o_binsh = take(4 * (size_t)desc->n_layers), o_sabs = take(8 * (size_t)c->G),
                  o_hb = take(8 * 2 * (size_t)kHStride * r),
-                 o_runs = take(4 * ((size_t)F_r + 2 * (size_t)c->G) + 16),  // any grid <= G
+                 o_bucket = take(decode_bucket_bytes()), o_sdump = take(4 * (size_t)F_r),
                  o_dhist = take(decode_hist_bytes()),
                  o_prev = take(4 * (size_t)desc->n_layers * (plan->k > 0 ? plan->k : 1));
     // score histogram geometry: |s| <= 127^2 r, bins of 2^sh over [0, 2 smax] (4096 bins)
@@ -580,7 +600,8 @@ m2c_status m2c_create(const m2c_model_desc *desc, int32_t device, m2c_stream_t c
     c->dec_bin_sh = (int *)(b + o_binsh);
     c->dec_sabs = (unsigned *)(b + o_sabs);
     c->dec_hb = (long long *)(b + o_hb);
-    c->dec_runs = (int *)(b + o_runs);
+    c->dec_bucket = (unsigned long long *)(b + o_bucket);
+    c->dec_sdump = (int *)(b + o_sdump);
     c->dec_hist = (int *)(b + o_dhist);
     e = cudaMemset(c->ws_mem, 0, off);
     if (e == cudaSuccess) {  // k_decode's first token: a histogram scale that covers |s| <= smax
@@ -1067,12 +1088,46 @@ m2c_status m2c_decode_lists(m2c_ctx *c, int32_t layer, int32_t *tier_ids_out) {
     M2C_CHECK_DEVICE_FLAG(c);
     if (!c || !tier_ids_out) return fail(M2C_ERR_INVALID_ARG, "decode_lists: null argument");
     if (layer < 0 || layer >= c->desc.n_layers) return fail(M2C_ERR_INVALID_ARG, "bad layer");
-    if (c->layers[layer].mode != 0 || !c->decoded)
-        return fail(M2C_ERR_STATE, "decode_lists: no decode step yet, or an LRU/ATU layer");
-    const int k = c->plan.k;
-    if (k > 0)
+    if (!c->decoded) return fail(M2C_ERR_STATE, "decode_lists: no decode step yet");
+    const m2c_tier_plan &p = c->plan;
+    if (p.k_fp16 > sort_tiers_max() || p.k_int8 > sort_tiers_max() || p.k_int4 > sort_tiers_max())
+        return fail(M2C_ERR_CAPACITY, "decode_lists: a tier has more than 32768 entries");
+    const int k = p.k;
+    if (k > 0) {
+        // the engines keep each layer's selection in rank order (k_decode) or ascending per
+        // tier (chain); the API returns three ascending segments
         M2C_CUDA(cudaMemcpyAsync(tier_ids_out, c->prev_ids + (size_t)layer * k, 4 * (size_t)k,
                                  cudaMemcpyDeviceToDevice, c->compute));
+        M2C_CUDA(launch_sort_tiers(c, tier_ids_out, p, c->compute));
+    }
+    return M2C_OK;
+}
+
+m2c_status m2c_set_trace(m2c_ctx *c, void *x_trace, float *y_trace) {
+    if (!c) return fail(M2C_ERR_INVALID_ARG, "null ctx");
+    M2C_CUDA(cudaStreamSynchronize(c->compute));
+    c->trace_x = static_cast<__half *>(x_trace);
+    c->trace_y = y_trace;
+    if (c->graph) {
+        cudaGraphExecDestroy(c->graph);
+        c->graph = nullptr;
+    }
+    return M2C_OK;
+}
+
+m2c_status m2c_cache_state(m2c_ctx *c, int32_t layer, int32_t tier, int32_t *occupant_out,
+                           int32_t *last_out, int32_t *cap_out) {
+    M2C_CHECK_DEVICE_FLAG(c);
+    if (!c || !cap_out) return fail(M2C_ERR_INVALID_ARG, "cache_state: null argument");
+    if (layer < 0 || layer >= c->desc.n_layers || tier < 0 || tier > 2)
+        return fail(M2C_ERR_INVALID_ARG, "cache_state: bad layer / tier");
+    const LayerState &L = c->layers[layer];
+    if (!L.loaded || L.mode == 0) return fail(M2C_ERR_STATE, "cache_state: not an LRU/ATU layer");
+    *cap_out = L.cap[tier];
+    const size_t b = 4 * (size_t)L.cap[tier];
+    if (occupant_out)
+        M2C_CUDA(cudaMemcpyAsync(occupant_out, L.occupant[tier], b, cudaMemcpyDeviceToDevice, c->compute));
+    if (last_out) M2C_CUDA(cudaMemcpyAsync(last_out, L.last[tier], b, cudaMemcpyDeviceToDevice, c->compute));
     return M2C_OK;
 }
 

@@ -13,9 +13,10 @@ __global__ void __launch_bounds__(1024, 1)
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ FfnShared sm;
     const SmemPtrs S = carve(smem);
-    if (threadIdx.x == 0) ffn_init_bars(sm);
+    if (threadIdx.x == 0) ffn_init(sm, d);
     griddep_launch();
     griddep_wait();
+    for (int c = threadIdx.x; c < d / 8; c += blockDim.x) S.xs[c] = reinterpret_cast<const uint4 *>(x)[c];
     if (threadIdx.x == 0) {
         int r[6];
         cta_ranges(a, counts[0], counts[1], counts[2], blockIdx.x, gridDim.x, r);
@@ -29,7 +30,8 @@ __global__ void __launch_bounds__(1024, 1)
         if (j < c2) return a.pool[1] + (int64_t)items[a.seg[1] + a1 + (j - c1)] * a.nb[1];
         return a.pool[2] + (int64_t)items[a.seg[2] + a2 + (j - c2)] * a.nb[2];
     };
-    ffn_loop(a, d, act, x, n_items, c1, c2, src, S.ring, S.xs, S.dsc, S.bst, sm, partial);
+    FfnPipe pipe;
+    ffn_run(a, d, act, n_items, c1, c2, src, S.ring, S.xs, S.a, sm, pipe, partial);
 }
 
 }  // namespace

@@ -119,8 +119,9 @@ struct m2c_ctx {
     unsigned long long *dec_prof = nullptr;  // [n_layers][G][kDecodeStamps]
     int *dec_bin_sh = nullptr;       // [n_layers] k_decode histogram scale per layer
     long long *dec_hb = nullptr;     // [2][r][kHStride] k_decode h accumulators (layer parity)
-    int *dec_runs = nullptr;         // [G][RP] k_decode per-CTA sorted score keys
-    int *dec_hist = nullptr;         // [2][4096 + 64] k_decode score histograms
+    unsigned long long *dec_bucket = nullptr;  // [2][4096][128] k_decode rank keys per score bin
+    int *dec_sdump = nullptr;        // [F_r] k_decode scores of the current layer
+    int *dec_hist = nullptr;         // [2][4096] k_decode score histograms
     unsigned *dec_sabs = nullptr;    // [G] per-CTA max |s| scratch
     bool dec_table_dirty = true;
     bool last_token_fused = false;
@@ -156,6 +157,9 @@ struct m2c_ctx {
     unsigned *p2p_rounds = nullptr;
     void *p2p_tabs = nullptr;
     std::vector<void *> p2p_opened;   // IPC-opened peer bases (closed at destroy)
+    // parity trace (m2c_set_trace): x_l [L+1][d] fp16, y_l [L][d] f32, caller-owned
+    __half *trace_x = nullptr;
+    float *trace_y = nullptr;
     // device error flag mirrored into pinned host memory (checked by every host call)
     uint32_t *err_host = nullptr;
     // early-fill engine: the last layer's scatter (copy stream) still reads the miss lists
@@ -233,9 +237,12 @@ cudaError_t launch_decode(m2c_ctx *c, __half *x, unsigned long long *prof, cudaS
 cudaError_t init_decode_attrs();
 cudaError_t decode_write_layer_table(m2c_ctx *c, void *dev_table);
 size_t decode_layer_table_bytes(int n_layers);
-int decode_max_F();
 size_t decode_hist_bytes();
-int decode_top_len(const m2c_ctx *c);
+size_t decode_bucket_bytes();
+bool decode_shape_ok(const m2c_ctx *c);
+int sort_tiers_max();
+// rank-order tier lists -> ascending ids per tier segment, in place (k_decode.cu)
+cudaError_t launch_sort_tiers(m2c_ctx *c, int32_t *ids, const m2c_tier_plan &p, cudaStream_t st);
 cudaError_t init_select_attrs();
 cudaError_t init_cache_attrs();
 cudaError_t init_ffn_attrs();

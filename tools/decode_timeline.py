@@ -9,7 +9,7 @@ from synth import get_config, layer_weights, token_stream
 
 name = sys.argv[1] if len(sys.argv) > 1 else "S7"
 cfg = get_config(name)
-L = int(sys.argv[2]) if len(sys.argv) > 2 else cfg.n_layers
+L = int(sys.argv[2]) if len(sys.argv) > 2 and sys.argv[2] else cfg.n_layers
 T = int(sys.argv[3]) if len(sys.argv) > 3 else 8
 plan = m2c.plan_of(cfg, 1)
 ctx = m2c.M2CContext(cfg.d_model, cfg.d_ff, L, cfg.pred_rank, plan, act=0 if cfg.act == "silu" else 1)
@@ -28,7 +28,7 @@ for t in range(T):
     s = ctx.profile_stamps().astype(np.int64)  # [L, G, 10]
     rows.append(s)
 ctx.profile(False)
-names = ["P2 hq+s+hist", "Bs", "P3 cuts", "P3 lists", "P4 ffn", "By", "R red+h", "Bx"]
+names = ["P2 hq+s+hist", "Bs", "P3 select", "P3 tail", "P4 ffn", "By", "R red+h", "Bx"]
 acc = {k: [] for k in names}
 accm = {k: [] for k in names}
 tot = []
@@ -47,8 +47,8 @@ for s in rows:
         spans = {
             "P2 hq+s+hist": ph(0, 1),
             "Bs": br(1, a[:, 4]),
-            "P3 cuts": ph(4, 10),
-            "P3 lists": ph(10, 5),
+            "P3 select": ph(4, 10),
+            "P3 tail": ph(10, 5),
             "P4 ffn": ph(5, 6),
             "By": br(6, a[:, 7]),
             "R red+h": ph(7, 8),
@@ -68,7 +68,7 @@ print("P4 per-CTA us (mid layer): min %.2f median %.2f max %.2f argmax %d" % (
 G = rows[-1].shape[1]
 p4 = np.mean([(s[:, :, 6] - s[:, :, 5]) / 1e3 for s in rows], axis=(0, 1))  # per CTA
 print("P4 mean per CTA by sixths of the grid:", " ".join(f"{p4[i * G // 6:(i + 1) * G // 6].mean():.2f}" for i in range(6)))
-sub = {"P2 h+max": (0, 20), "P2 hq": (20, 21), "P2 dots": (21, 22), "P2 sort": (22, 1), "P3 load": (4, 2), "P3 cutbins": (2, 3), "P3 cand": (3, 16), "P3 rank": (16, 10), "P3 walk": (10, 18), "P3 exscan": (18, 19), "P3 write": (19, 11), "P3 tail": (11, 5), "P4 setup": (5, 14), "P4 gate/up": (14, 15), "P4 down": (15, 6)}
+sub = {"P2 h+max": (0, 20), "P2 hq+B": (20, 21), "P2 dots": (21, 22), "P2 atomics": (22, 1), "P3 hist load": (4, 2), "P3 scan": (2, 3), "P3 rank": (3, 10), "P3 tail": (10, 5), "P4 issue": (5, 14), "P4 gate/up": (14, 15), "P4 down": (15, 6)}
 for k, (i, j) in sub.items():
     v = np.mean([((s[:, :, j] - s[:, :, i]) / 1e3).mean() for s in rows])
     print(f"{k:12s} mean-CTA {v:.2f} us")
