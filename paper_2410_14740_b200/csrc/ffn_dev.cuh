@@ -238,6 +238,87 @@ __device__ __forceinline__ void down_acc(const uint8_t *e, const uint8_t *sc, in
     }
 }
 
+// ---- the same from global memory (whole-record layout), several records' loads in flight --
+template <int TIER>
+struct DownLd {
+    uint4 v;
+    float s;
+    uint32_t z;
+};
+template <int TIER>
+__device__ __forceinline__ void down_ldg(const uint8_t *rec, int d, DownLd<TIER> &o) {
+    const int t = threadIdx.x;
+    if (TIER == 0) {
+        o.v = __ldcg(reinterpret_cast<const uint4 *>(rec + 4 * d + 16 * t));
+    } else {
+        const int G = d >> 7, grp = t >> 4;
+        const int D = TIER == 1 ? d : d / 2;
+        const uint8_t *sc = rec + 3 * D;
+        if (TIER == 1) {
+            const uint2 w = __ldcg(reinterpret_cast<const uint2 *>(rec + 2 * d + 8 * t));
+            o.v = make_uint4(w.x, w.y, 0, 0);
+        } else {
+            o.v = make_uint4(__ldcg(reinterpret_cast<const unsigned *>(rec + d + 4 * t)), 0, 0, 0);
+        }
+        o.s = half_bits_f(__ldcg(reinterpret_cast<const unsigned short *>(sc + 2 * (2 * G + grp))));
+        o.z = __ldcg(sc + 6 * G + 2 * G + grp);
+    }
+}
+template <int TIER>
+__device__ __forceinline__ void down_fma(const DownLd<TIER> &o, float a, float (&y)[8]) {
+    if (TIER == 0) {
+        const uint32_t w[4] = {o.v.x, o.v.y, o.v.z, o.v.w};
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            y[2 * i] = fmaf(a, h2f_lo(w[i]), y[2 * i]);
+            y[2 * i + 1] = fmaf(a, h2f_hi(w[i]), y[2 * i + 1]);
+        }
+    } else {
+        const float as = a * o.s;
+        uint32_t p[4];
+        if (TIER == 1) {
+            deq8(o.v.x, o.v.y, zz2(o.z), p);
+#pragma unroll
+            for (int i = 0; i < 4; i++) {
+                y[2 * i] = fmaf(as, h2f_lo(p[i]), y[2 * i]);
+                y[2 * i + 1] = fmaf(as, h2f_hi(p[i]), y[2 * i + 1]);
+            }
+        } else {
+            deq4(o.v.x, zz2(o.z), zz2_16(o.z), p);
+            const float as16 = as * 0.0625f;
+            y[0] = fmaf(as, h2f_lo(p[0]), y[0]);
+            y[4] = fmaf(as, h2f_hi(p[0]), y[4]);
+            y[1] = fmaf(as16, h2f_lo(p[1]), y[1]);
+            y[5] = fmaf(as16, h2f_hi(p[1]), y[5]);
+            y[2] = fmaf(as, h2f_lo(p[2]), y[2]);
+            y[6] = fmaf(as, h2f_hi(p[2]), y[6]);
+            y[3] = fmaf(as16, h2f_lo(p[3]), y[3]);
+            y[7] = fmaf(as16, h2f_hi(p[3]), y[7]);
+        }
+    }
+}
+#ifndef M2C_DN_UNROLL
+#define M2C_DN_UNROLL 8
+#endif
+// records [ja, jb) of one tier from global memory, in order, kU records' loads in flight
+template <int TIER, class RecFn>
+__device__ __forceinline__ void down_seg_g(RecFn rec, const float *a_sm, int ja, int jb, int d, float (&y)[8]) {
+    constexpr int kU = TIER == 0 ? M2C_DN_UNROLL / 2 : M2C_DN_UNROLL;
+    int j = ja;
+    for (; j + kU <= jb; j += kU) {
+        DownLd<TIER> o[kU];
+#pragma unroll
+        for (int u = 0; u < kU; u++) down_ldg<TIER>(rec(j + u), d, o[u]);
+#pragma unroll
+        for (int u = 0; u < kU; u++) down_fma<TIER>(o[u], a_sm[j + u], y);
+    }
+    for (; j < jb; j++) {
+        DownLd<TIER> o;
+        down_ldg<TIER>(rec(j), d, o);
+        down_fma<TIER>(o, a_sm[j], y);
+    }
+}
+
 // this CTA's share [i0_t, i1_t) of each tier list, balanced on wt (computed by one thread)
 __device__ __forceinline__ void cta_ranges(const FfnArgs &a, int n0, int n1, int n2, int cta, int G,
                                            int (&r)[6]) {
@@ -314,6 +395,9 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
 //    entry as soon as its P units have arrived on it, then the down parts (+ tail); phase G
 //    runs on the other warps; in phase D every warp consumes the down entries in order and the
 //    producer re-issues freed space until every down entry is in.
+#ifndef M2C_DN_PF
+#define M2C_DN_PF 1
+#endif
 template <class SrcFn>
 __device__ __forceinline__ void ffn_run(const FfnArgs &a, int d, int act, int n_items, int c1, int c2,
                                         SrcFn src, uint8_t *ring, const uint4 *xs, float *a_sm,
@@ -327,67 +411,9 @@ __device__ __forceinline__ void ffn_run(const FfnArgs &a, int d, int act, int n_
     const int total = c1 * a.nb[0] + (c2 - c1) * a.nb[1] + (n_items - c2) * a.nb[2];
     const bool whole = (n_items <= kNS && total <= kRing) || NW == 1;
     const uint64_t pol = policy_evict_first();
-    const unsigned nf0 = pp.nf, ng0 = pp.ng, nd0 = pp.nd;
+    const unsigned nf0 = pp.nf, ng0 = pp.ng;
     auto fslot = [&](unsigned e) { return (nf0 + e) % kNS; };
     auto fpar = [&](unsigned e) { return ((nf0 + e) / kNS) & 1u; };
-    // streaming producer state (warp NW - 1; warp-uniform, lane 0 issues)
-    int head = 0, tailg = 0, taild = 0, wpos = 0, used = 0;
-    const int n2 = 2 * n_items;  // FIFO entries: gate/up 0..n-1, then down n..2n-1
-    auto entry_size = [&](int e) {
-        const int j = e < n_items ? e : e - n_items, t = tier_of(j), D = Dof(t);
-        return e < n_items ? 2 * D + (a.nb[t] - 3 * D) : a.nb[t] - 2 * D;
-    };
-    // free the oldest entry: gate/up entries are consumed before any down entry (FIFO)
-    auto free_tail = [&](bool allow_down) -> bool {
-        if (tailg < n_items && tailg < head) {
-            const unsigned s = (ng0 + tailg) % kNS;
-            mbar_wait(&sm.emptyG[s], ((ng0 + tailg) / kNS) & 1u);
-            used -= __shfl_sync(0xffffffffu, sm.span[fslot(tailg)], 0);
-            tailg++;
-        } else if (allow_down && tailg == n_items && n_items + taild < head) {
-            const unsigned s = (nd0 + taild) % kNS;
-            mbar_wait(&sm.emptyD[s], ((nd0 + taild) / kNS) & 1u);
-            used -= __shfl_sync(0xffffffffu, sm.span[fslot(n_items + taild)], 0);
-            taild++;
-        } else {
-            return false;
-        }
-        if (lane == 0) fence_proxy_async();  // consumers' generic reads precede the new copies
-        return true;
-    };
-    // issue entries up to `until` (exclusive); block on frees only where allowed
-    auto produce = [&](int until, bool block_down) {
-        while (head < until) {
-            const int sz = entry_size(head);
-            const bool wrap = wpos + sz > kRing;
-            const int need = (wrap ? kRing - wpos : 0) + sz;
-            const int inflight = head - (tailg + taild);
-            if (used + need <= kRing && inflight < kNS) {
-                const unsigned s = fslot(head);
-                const int off = wrap ? 0 : wpos;
-                used += need;
-                wpos = off + sz;
-                if (lane == 0) {
-                    const int j = head < n_items ? head : head - n_items, t = tier_of(j), D = Dof(t);
-                    const uint8_t *g = src(j);
-                    sm.roff[s] = off;
-                    sm.span[s] = need;
-                    mbar_expect_tx(&sm.full[s], (uint32_t)sz);
-                    if (head < n_items) {
-                        bulk_g2s(ring + off, g, (uint32_t)(2 * D), &sm.full[s], pol);
-                        if (a.nb[t] > 3 * D)
-                            bulk_g2s(ring + off + 2 * D, g + 3 * D, (uint32_t)(a.nb[t] - 3 * D), &sm.full[s], pol);
-                    } else {
-                        bulk_g2s(ring + off, g + 2 * D, (uint32_t)sz, &sm.full[s], pol);
-                    }
-                }
-                head++;
-            } else if (!free_tail(block_down)) {
-                break;  // (phase G: only down entries left to free -- wait for phase D)
-            }
-            __syncwarp();
-        }
-    };
     if (whole) {
         // every record at once: warp 0, lane j -> records j, j + 32 (offsets by warp scans)
         if (warp == 0) {
@@ -411,8 +437,41 @@ __device__ __forceinline__ void ffn_run(const FfnArgs &a, int d, int act, int n_
             }
         }
     } else if (warp == NW - 1) {
-        produce(n2, false);  // gate/up entries (blocking on their frees), then down entries
-    }                        // as long as space is free
+        // streaming: the producer warp (decisions warp-uniform, lane 0 issues) streams the
+        // gate/up part (+ scale/zero tail) of each record through the ring in order, re-using
+        // an entry as soon as its P units have arrived on it; the record's down part is
+        // prefetched into L2 right behind (phase D reads it from global memory)
+        int head = 0, tail = 0, wpos = 0, used = 0;
+        while (head < n_items) {
+            const int t = tier_of(head), D = Dof(t), tailb = a.nb[t] - 3 * D;
+            const int sz = 2 * D + tailb;
+            const bool wrap = wpos + sz > kRing;
+            const int need = (wrap ? kRing - wpos : 0) + sz;
+            if (used + need <= kRing && head - tail < kNS) {
+                const unsigned s = fslot(head);
+                const int off = wrap ? 0 : wpos;
+                used += need;
+                wpos = off + sz;
+                if (lane == 0) {
+                    const uint8_t *g = src(head);
+                    sm.roff[s] = off;
+                    sm.span[s] = need;
+                    mbar_expect_tx(&sm.full[s], (uint32_t)sz);
+                    bulk_g2s(ring + off, g, (uint32_t)(2 * D), &sm.full[s], pol);
+                    if (tailb) bulk_g2s(ring + off + 2 * D, g + 3 * D, (uint32_t)tailb, &sm.full[s], pol);
+                    if (M2C_DN_PF) prefetch_l2(g + 2 * D, (uint32_t)(a.nb[t] - 2 * D));
+                }
+                head++;
+            } else {
+                const unsigned s = (ng0 + tail) % kNS;
+                mbar_wait(&sm.emptyG[s], ((ng0 + tail) / kNS) & 1u);
+                used -= __shfl_sync(0xffffffffu, sm.span[fslot(tail)], 0);
+                tail++;
+                if (lane == 0) fence_proxy_async();  // consumers' generic reads precede new copies
+            }
+            __syncwarp();
+        }
+    }
     if (stamps && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(stamps[0]));
     // ---- phase G: gate/up units (record j, part p), round-robin over the compute warps ----
     const int NWc = whole ? NW : NW - 1;
@@ -450,45 +509,31 @@ __device__ __forceinline__ void ffn_run(const FfnArgs &a, int d, int act, int n_
             if (!whole && lane == 0) mbar_arrive(&sm.emptyG[(ng0 + j) % kNS]);
         }
     }
-    __syncthreads();  // every a_j is in a_sm; the producer has issued what fit
+    __syncthreads();  // every a_j is in a_sm (and the producer is done)
     if (stamps && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(stamps[1]));
     // ---- phase D: y[8t, 8t+8) += a_j deq(down_j), records in share order -------------------
     float y[8];
 #pragma unroll
     for (int i = 0; i < 8; i++) y[i] = 0.f;
-    for (int j = 0; j < n_items; j++) {
-        const int t = tier_of(j), D = Dof(t);
-        const uint8_t *e, *sc;
-        if (whole) {
+    if (whole) {
+        for (int j = 0; j < n_items; j++) {
+            const int t = tier_of(j), D = Dof(t);
             const uint8_t *rec = ring + sm.roff[fslot(j)];
-            e = rec + 2 * D;
-            sc = rec + 3 * D;
-        } else {
-            if (warp == NW - 1 && head <= n_items + j) produce(n_items + j + 1, true);
-            const unsigned s = fslot(n_items + j);
-            mbar_wait(&sm.full[s], fpar(n_items + j));
-            e = ring + sm.roff[s];
-            sc = e + D;
+            const float aj = a_sm[j];
+            if (t == 0) down_acc<0>(rec + 2 * D, rec + 3 * D, d, aj, y);
+            else if (t == 1) down_acc<1>(rec + 2 * D, rec + 3 * D, d, aj, y);
+            else down_acc<2>(rec + 2 * D, rec + 3 * D, d, aj, y);
         }
-        const float aj = a_sm[j];
-        if (t == 0) down_acc<0>(e, sc, d, aj, y);
-        else if (t == 1) down_acc<1>(e, sc, d, aj, y);
-        else down_acc<2>(e, sc, d, aj, y);
-        if (!whole) {
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&sm.emptyD[(nd0 + j) % kNS]);
-        }
+    } else {
+        down_seg_g<0>(src, a_sm, 0, c1, d, y);
+        down_seg_g<1>(src, a_sm, c1, c2, d, y);
+        down_seg_g<2>(src, a_sm, c2, n_items, d, y);
     }
     float *out = partial + (int64_t)blockIdx.x * d + 8 * threadIdx.x;
     reinterpret_cast<float4 *>(out)[0] = make_float4(y[0], y[1], y[2], y[3]);
     reinterpret_cast<float4 *>(out)[1] = make_float4(y[4], y[5], y[6], y[7]);
-    if (whole) {
-        pp.nf += (unsigned)n_items;
-    } else {
-        pp.nf += (unsigned)n2;
-        pp.ng += (unsigned)n_items;
-        pp.nd += (unsigned)n_items;
-    }
+    pp.nf += (unsigned)n_items;
+    if (!whole) pp.ng += (unsigned)n_items;
     __syncthreads();  // the ring's entries are consumed
 }
 

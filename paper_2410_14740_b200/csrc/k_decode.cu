@@ -577,20 +577,19 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
                 float(*rf)[33] = reinterpret_cast<float(*)[33]>(S.ring + kRfOff);  // [nc * gw][33]
                 const int g = warp / gw, v = warp - g * gw;
                 const int e = (cta + (q0 + g) * G) * 32 + lane;
-                if (g < nc) {  // group g reduces chunk q0 + g: virtual warp v sums rows v::gw
+                if (g < nc) {  // group g reduces chunk q0 + g: virtual warp v sums rows v::gw,
+                    // up to 12 rows' loads in flight before the (fixed-order) sum
                     float acc = 0.f;
-                    int rw = v;
-                    for (; rw + 3 * gw < G; rw += 4 * gw) {
-                        const float a0 = __ldcg(p.partial + (int64_t)rw * d + e);
-                        const float a1 = __ldcg(p.partial + (int64_t)(rw + gw) * d + e);
-                        const float a2 = __ldcg(p.partial + (int64_t)(rw + 2 * gw) * d + e);
-                        const float a3 = __ldcg(p.partial + (int64_t)(rw + 3 * gw) * d + e);
-                        acc += a0;
-                        acc += a1;
-                        acc += a2;
-                        acc += a3;
+                    for (int rw0 = v; rw0 < G; rw0 += 12 * gw) {
+                        float pv[12];
+#pragma unroll
+                        for (int i = 0; i < 12; i++) {
+                            const int rw = rw0 + i * gw;
+                            pv[i] = rw < G ? __ldcg(p.partial + (int64_t)rw * d + e) : 0.f;
+                        }
+#pragma unroll
+                        for (int i = 0; i < 12; i++) acc += pv[i];
                     }
-                    for (; rw < G; rw += gw) acc += __ldcg(p.partial + (int64_t)rw * d + e);
                     rf[g * gw + v][lane] = acc;
                 }
                 __syncthreads();
