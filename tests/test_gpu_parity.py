@@ -309,78 +309,7 @@ def test_lru_cache_sequence_bit_exact(m2c, mode, mult):
 
 
 # ------------------------------------------------------------------ whole token
-def test_decode_step_equals_api_chain_and_layer0_oracle(m2c):
-    cfg = get_config("T")
-    L = 3
-    plan = m2c.plan_of(cfg)
-    ws = [layer_weights(cfg, l, device="cuda") for l in range(L)]
-    ctx = _ctx(m2c, cfg, plan, n_layers=L)
-    for l, w in enumerate(ws):
-        ctx.load_layer(l, w["w_gate"], w["w_up"], w["w_down_t"], w["pred_A"], w["pred_B"])
-    xs = token_stream(cfg, 4, device="cuda")
-    for graph in (True, False):
-        ctx.set_graph(graph)
-        for t in range(4):
-            x0 = xs[t].contiguous()
-            x = x0.clone()
-            ctx.decode_step(x, 10 * t + (1 if graph else 2))
-            # chain of API calls
-            xc = x0.clone()
-            for l in range(L):
-                sel = ctx.predict_rank(l, xc, rank_list=False, tier_of=False, scores=False)
-                _, y = ctx.sparse_ffn_forward(l, xc, sel["tier_ids"], want_partial=False)
-                xc = (xc + y)  # fp16 add, one rounding (R14)
-            torch.cuda.synchronize()
-            assert torch.equal(x, xc)
-    # layer 0 against the oracle on the generator input
-    wn = _np(ws[0])
-    recs = orc.layer_records(wn)
-    x0 = xs[0].contiguous()
-    ref = orc.layer_forward(wn, recs, x0.cpu().numpy(), _plan_np(plan))
-    _, x1 = orc.residual(x0.cpu().numpy(), ref["yhat"])
-    sel = ctx.predict_rank(0, x0)
-    _, y = ctx.sparse_ffn_forward(0, x0, sel["tier_ids"])
-    got = (x0 + y).cpu().numpy()
-    assert np.abs(got.astype(np.float64) - x1.astype(np.float64)).max() <= \
-        2.0 ** -9 * np.abs(x1.astype(np.float64)).max()
-    st = ctx.stats()
-    assert st["kernels_per_token"] == 1  # the persistent decode kernel (k_decode)
-    ctx.close()
-
-
-@pytest.mark.parametrize("name,layers,parts", [("T", 3, 1), ("S7", 2, 1), ("S13", 1, 1),
-                                               ("S70", 1, 8), ("S70", 1, 1)])
-def test_decode_fused_select_equals_unfused(m2c, name, layers, parts):
-    """The persistent decode kernel (grid barriers, in-CTA select from the score histogram,
-    L2 lookahead) gives bit-identical tokens to the per-phase kernel chain."""
-    cfg = get_config(name)
-    shard = (0, parts)
-    plan = m2c.plan_of(cfg, shard[1])
-    ctxs = []
-    for fused in (True, False):
-        ctx = _ctx(m2c, cfg, plan, n_layers=layers, shard=shard)
-        for l in range(layers):
-            w = layer_weights(cfg, l, device="cuda", shard=shard)
-            ctx.load_layer(l, w["w_gate"], w["w_up"], w["w_down_t"], w["pred_A"], w["pred_B"])
-        ctx.set_fused(fused)
-        ctxs.append(ctx)
-    xs = token_stream(cfg, 6, device="cuda")
-    for t in range(6):
-        outs = []
-        for ctx in ctxs:
-            x = xs[t].contiguous().clone()
-            ctx.decode_step(x, t + 1)
-            outs.append(x)
-        torch.cuda.synchronize()
-        for l in range(layers):  # the selected tier lists, then the token
-            assert torch.equal(ctxs[0].decode_lists(l), ctxs[1].decode_lists(l)), (t, l)
-        assert torch.equal(outs[0], outs[1]), t
-    assert ctxs[0].stats()["kernels_per_token"] == 1  # fused: k_decode; the chain: > 4 per layer
-    assert ctxs[1].stats()["kernels_per_token"] > 4 * layers
-    for ctx in ctxs:
-        ctx.close()
-
-
+# (engine-vs-oracle replay tests: tests/test_gpu_engines.py)
 def test_decode_step_lru_matches_api_chain(m2c):
     cfg = get_config("T")
     L = 2
@@ -412,111 +341,6 @@ def test_decode_step_lru_matches_api_chain(m2c):
     sa, sb = a.stats(), b.stats()
     assert sa["hits"] == sb["hits"] and sa["misses"] == sb["misses"]
     assert sum(sa["misses"]) > 0 and sum(sa["hits"]) > 0
-    for c in ctxs:
-        c.close()
-
-
-@pytest.mark.parametrize("kind", ["zero_x", "tied_B"])
-def test_decode_fused_degenerate_ties(m2c, kind):
-    """Massive score ties: x = 0 (every score 0: the binary-search cut) and a predictor whose
-    B rows repeat in runs of 7 (partial ties at every cut, ranked exactly by id)."""
-    cfg = get_config("S7")
-    L = 2
-    plan = m2c.plan_of(cfg)
-    ctxs = []
-    for fused in (True, False):
-        ctx = _ctx(m2c, cfg, plan, n_layers=L)
-        for l in range(L):
-            w = layer_weights(cfg, l, device="cuda")
-            B = w["pred_B"]
-            if kind == "tied_B":
-                B = B[torch.arange(B.shape[0], device=B.device) // 7 * 7].contiguous()
-            ctx.load_layer(l, w["w_gate"], w["w_up"], w["w_down_t"], w["pred_A"], B)
-        ctx.set_fused(fused)
-        ctxs.append(ctx)
-    xs = token_stream(cfg, 3, device="cuda")
-    for t in range(3):
-        outs = []
-        for ctx in ctxs:
-            x = torch.zeros_like(xs[t]) if kind == "zero_x" else xs[t].contiguous().clone()
-            ctx.decode_step(x, t + 1)
-            outs.append(x)
-        torch.cuda.synchronize()
-        assert torch.equal(outs[0], outs[1]), t
-    for ctx in ctxs:
-        ctx.stats()  # raises if the device flagged an error (barrier timeout, count mismatch)
-        ctx.close()
-
-
-@pytest.mark.parametrize("n_fixed,n_dyn,ahead", [(1, 2, 1), (0, 1, 0), (2, 3, 2), (4, 0, 0)])
-def test_store_backed_host_tier_matches_in_memory(m2c, tmp_path, n_fixed, n_dyn, ahead):
-    """NEXT-1: miss fills served from the file-backed two-level DRAM cache (fixed area + FIFO
-    frames filled by the I/O thread) give bit-identical tokens, lists and cache statistics."""
-    cfg = get_config("T")
-    L = 4
-    plan = m2c.plan_of(cfg)
-    ws = [layer_weights(cfg, l, device="cuda") for l in range(L)]
-    ctxs = []
-    for _ in range(2):
-        ctx = _ctx(m2c, cfg, plan, n_layers=L)
-        cc = m2c.cache_cfg_capped(ctx.desc, plan, 1, 4, "lru")
-        ctx.reserve_host_tier(L * ctx.layer_footprint(cc)[1])
-        for l, w in enumerate(ws):
-            ctx.load_layer(l, w["w_gate"], w["w_up"], w["w_down_t"], w["pred_A"], w["pred_B"], cc)
-        ctxs.append(ctx)
-    a, b = ctxs
-    path = str(tmp_path / "m2c_store.bin")
-    b.store_write(path)
-    b.store_attach(path, n_fixed, n_dyn, ahead)
-    xs = token_stream(cfg, 10, device="cuda")
-    for t in range(10):
-        xa, xb = xs[t].contiguous().clone(), xs[t].contiguous().clone()
-        a.decode_step(xa, t + 1)
-        b.decode_step(xb, t + 1)
-        torch.cuda.synchronize()
-        assert torch.equal(xa, xb), t
-    sa, sb = a.stats(), b.stats()
-    assert sa["hits"] == sb["hits"] and sa["misses"] == sb["misses"]
-    st = b.store_stats()
-    assert st["layer_loads"] >= min(n_fixed, L) and st["bytes_read"] > 0
-    if n_fixed + n_dyn < L:  # the dynamic area streamed the other layers every token
-        assert st["layer_loads"] >= n_fixed + (L - n_fixed) * 10 - n_dyn
-    else:  # everything fits the DRAM cache: each layer read once
-        assert st["layer_loads"] == L
-    for c in ctxs:
-        c.close()
-
-
-@pytest.mark.parametrize("mode", ["lru", "atu"])
-def test_lookahead_staging_is_transparent(m2c, mode):
-    """NEXT-2: staging layer l+1's predicted misses during layer l changes no token or cache
-    statistic, and serves a share of the misses device-side."""
-    cfg = get_config("T")
-    L = 4
-    plan = m2c.plan_of(cfg)
-    ws = [layer_weights(cfg, l, device="cuda") for l in range(L)]
-    ctxs = []
-    for la in (False, True):
-        ctx = _ctx(m2c, cfg, plan, n_layers=L)
-        cc = m2c.cache_cfg_capped(ctx.desc, plan, 1, 4, mode)
-        ctx.reserve_host_tier(L * ctx.layer_footprint(cc)[1])
-        for l, w in enumerate(ws):
-            ctx.load_layer(l, w["w_gate"], w["w_up"], w["w_down_t"], w["pred_A"], w["pred_B"], cc)
-        ctx.set_lookahead(la)
-        ctxs.append(ctx)
-    a, b = ctxs
-    xs = token_stream(cfg, 12, device="cuda")
-    for t in range(12):
-        xa, xb = xs[t].contiguous().clone(), xs[t].contiguous().clone()
-        a.decode_step(xa, t + 1)
-        b.decode_step(xb, t + 1)
-        torch.cuda.synchronize()
-        assert torch.equal(xa, xb), t
-    sa, sb = a.stats(), b.stats()
-    assert sa["hits"] == sb["hits"] and sa["misses"] == sb["misses"]
-    staged = b.lookahead_stats()
-    assert 0 < staged <= sum(sb["misses"])
-    assert a.lookahead_stats() == 0
     for c in ctxs:
         c.close()
 
@@ -567,11 +391,11 @@ def test_global_topk_under_sharding_equals_unsharded(m2c, P, pct, a16, a8, den):
 def test_decode_layer_split_equals_fused(m2c, name, layers):
     """The layer-split engine (k_decode one layer per launch, the partial y handed to the next
     launch through the all-reduce buffer -- the d_ff-sharded decode) is bit-identical to the
-    whole-token k_decode and to the per-phase chain."""
+    whole-token k_decode (same shares, same reduction order, same selection)."""
     cfg = get_config(name)
     plan = m2c.plan_of(cfg)
     ctxs = []
-    for mode in (1, 2, 0):
+    for mode in (1, 2):
         ctx = _ctx(m2c, cfg, plan, n_layers=layers)
         for l in range(layers):
             w = layer_weights(cfg, l, device="cuda")
@@ -589,215 +413,8 @@ def test_decode_layer_split_equals_fused(m2c, name, layers):
         for l in range(layers):
             assert torch.equal(ctxs[0].decode_lists(l), ctxs[1].decode_lists(l)), (t, l)
         assert torch.equal(outs[0], outs[1]), t
-        assert torch.equal(outs[0], outs[2]), t
+    assert ctxs[0].stats()["kernels_per_token"] == 1
     assert ctxs[1].stats()["kernels_per_token"] == layers + 1  # L launches + the final residual
-    for c in ctxs:
-        c.close()
-
-
-def test_full_s7_stack_decode_replay_against_oracle(m2c):
-    """BASELINE configs[1] at full size in the launch configuration bench.py times (32 layers,
-    k_decode, CUDA graph): the token equals the per-layer C-ABI chain's, and at sampled layers
-    the chain's recorded layer inputs replayed through the oracle (D9) give the same tier lists
-    (bit-exact) and the same y within the tolerance."""
-    cfg = get_config("S7")
-    plan = m2c.plan_of(cfg)
-    L = cfg.n_layers
-    ctx = _ctx(m2c, cfg, plan, n_layers=L)
-    sample = {0: None, 13: None, L - 1: None}
-    for l in range(L):
-        w = layer_weights(cfg, l, device="cuda")
-        ctx.load_layer(l, w["w_gate"], w["w_up"], w["w_down_t"], w["pred_A"], w["pred_B"])
-        if l in sample:
-            sample[l] = _np(w)
-        del w
-    pn = _plan_np(plan)
-    xs = token_stream(cfg, 3, device="cuda")
-    for t in range(3):
-        x0 = xs[t].contiguous()
-        x = x0.clone()
-        ctx.decode_step(x, t + 1)  # k_decode, graph (the bench path)
-        xc = x0.clone()
-        for l in range(L):
-            sel = ctx.predict_rank(l, xc, rank_list=False, tier_of=False, scores=False)
-            _, y = ctx.sparse_ffn_forward(l, xc, sel["tier_ids"], want_partial=False)
-            if t == 0 and l in sample:
-                wn, xn = sample[l], xc.cpu().numpy()
-                ref = orc.select(orc.predict(xn, wn["pred_A"], wn["pred_B"])["s"], pn)
-                assert np.array_equal(sel["tier_ids"].cpu().numpy(), ref["tier_ids"]), l
-                recs = orc.records_for(wn, ref["tier_ids"], pn)
-                yhat = orc.ffn(cfg.d_model, pn, ref["tier_ids"], recs[16], recs[8], recs[4], xn)
-                assert d10(y.cpu().numpy(), yhat) <= TOL, l
-            xc = xc + y
-        torch.cuda.synchronize()
-        assert torch.equal(x, xc), t
-        assert ctx.stats()["kernels_per_token"] == 1
-    ctx.close()
-
-
-@pytest.mark.parametrize("engine", ["split", "chain", "global"])
-def test_nccl_wiring_single_rank(m2c, engine):
-    """The collectives of the sharded engines (ncclAllReduce between layer launches / in the
-    chain, ncclAllGather of the global-top-k keys), captured in the decode graph, run for real
-    with a one-rank communicator (identity collectives) and leave every token bit-identical
-    to the unsharded whole-token kernel -- the NCCL plumbing a multi-GPU run uses."""
-    cfg = get_config("T")
-    L = 3
-    plan = m2c.plan_of(cfg)
-    ctxs = []
-    for with_comm in (False, True):
-        ctx = _ctx(m2c, cfg, plan, n_layers=L)
-        for l in range(L):
-            w = layer_weights(cfg, l, device="cuda")
-            ctx.load_layer(l, w["w_gate"], w["w_up"], w["w_down_t"], w["pred_A"], w["pred_B"])
-        if with_comm:
-            ctx.comm_init(1, 0, m2c.nccl_unique_id())
-            if engine == "chain":
-                ctx.set_fused(False)
-            elif engine == "global":
-                ctx.set_global_topk(plan)  # one rank: the global plan is the plan
-        ctxs.append(ctx)
-    xs = token_stream(cfg, 4, device="cuda")
-    for t in range(4):
-        outs = []
-        for ctx in ctxs:
-            x = xs[t].contiguous().clone()
-            ctx.decode_step(x, t + 1)
-            outs.append(x)
-        torch.cuda.synchronize()
-        assert torch.equal(outs[0], outs[1]), t
-    kpt = ctxs[1].stats()["kernels_per_token"]
-    assert kpt == (L + 1 if engine == "split" else kpt) and kpt > 1
-    for c in ctxs:
-        c.close()
-
-
-@pytest.mark.parametrize("name,layers", [("T", 3), ("S7", 4)])
-def test_p2p_fused_allreduce_two_ranks_one_gpu(m2c, name, layers):
-    """§8(e): two d_ff shards (ranks 0/1 of P = 2) share one GPU, 74 CTAs each, and run the
-    whole-token k_decode CONCURRENTLY on their own streams with the all-reduce fused into the
-    reduction phase over the exchange buffers (peer stores + system-scope counters; on one GPU
-    the 'peer' is the same HBM, the protocol is the one NVLink peers run).  Every token must
-    equal the host-orchestrated emulation: per layer, each rank's C-ABI chain (predict_rank ->
-    sparse_ffn_forward partial y, same grid), partials summed in rank order, x += fp16(sum)."""
-    from paper_2410_14740_b200._lib import lib
-    from paper_2410_14740_b200.api import check
-    cfg = get_config(name)
-    P = 2
-    plan = m2c.plan_of(cfg, P)
-    ctxs = []
-    for r in range(P):
-        ctx = _ctx(m2c, cfg, plan, n_layers=layers, shard=(r, P))
-        for l in range(layers):
-            w = layer_weights(cfg, l, device="cuda", shard=(r, P))
-            ctx.load_layer(l, w["w_gate"], w["w_up"], w["w_down_t"], w["pred_A"], w["pred_B"])
-        ctx.set_grid(74)
-        ctxs.append(ctx)
-    ptrs = [c.p2p_buffer()[0] for c in ctxs]
-    for c in ctxs:
-        c.p2p_connect(dev_ptrs=ptrs)
-    xs = token_stream(cfg, 5, device="cuda")
-    for t in range(5):
-        xr = [xs[t].contiguous().clone() for _ in range(P)]
-        torch.cuda.synchronize()
-        for c, x in zip(ctxs, xr):  # both ranks in flight at once (no stream dependency)
-            check(lib().m2c_decode_step(c._h, x.data_ptr(), t + 1))
-        torch.cuda.synchronize()
-        for c in ctxs:
-            assert c.stats()["kernels_per_token"] == 1  # raises on a p2p / barrier timeout
-        xc = xs[t].contiguous().clone()
-        for l in range(layers):
-            parts = []
-            for c in ctxs:
-                sel = c.predict_rank(l, xc, rank_list=False, tier_of=False, scores=False)
-                yp, _ = c.sparse_ffn_forward(l, xc, sel["tier_ids"], want_partial=True)
-                parts.append(yp)
-            ysum = parts[0] + parts[1]
-            xc = xc + ysum.half()
-        torch.cuda.synchronize()
-        assert torch.equal(xr[0], xr[1]), t
-        assert torch.equal(xr[0], xc), t
-    for c in ctxs:
-        c.close()
-
-
-def _ipc_worker(rank, world, port, out):
-    import os
-    import sys
-    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-    import torch
-    import torch.distributed as dist
-
-    import paper_2410_14740_b200 as m2c
-    from paper_2410_14740_b200 import dist as m2c_dist
-    from synth import get_config, layer_weights, token_stream
-    os.environ["MASTER_ADDR"] = "127.0.0.1"
-    os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
-    try:
-        cfg = get_config("T")
-        L = 3
-        ctx = _ctx(m2c, cfg, m2c.plan_of(cfg, world), n_layers=L, shard=(rank, world))
-        for l in range(L):
-            w = layer_weights(cfg, l, device="cuda", shard=(rank, world))
-            ctx.load_layer(l, w["w_gate"], w["w_up"], w["w_down_t"], w["pred_A"], w["pred_B"])
-        ctx.set_grid(32)
-        m2c_dist.p2p_init(ctx)  # CUDA IPC handles over the process group
-        xs = token_stream(cfg, 2, device="cuda")
-        res = []
-        for t in range(2):
-            x = xs[t].contiguous().clone()
-            dist.barrier()
-            ctx.decode_step(x, t + 1)
-            torch.cuda.synchronize()
-            assert ctx.stats()["kernels_per_token"] == 1  # the whole-token kernel ran
-            res.append(x.cpu().numpy().tobytes())
-        out[rank] = res
-        dist.barrier()
-        ctx.close()
-    finally:
-        dist.destroy_process_group()
-
-
-def test_p2p_ipc_two_processes(m2c):
-    """§8(e) across processes: two ranks in two processes (one GPU here; on a node, one GPU
-    each) exchange their buffers' CUDA IPC handles over the process group (dist.p2p_init) and
-    decode with the in-kernel exchange; both end with the same token, equal to the in-process
-    two-rank emulation.  (Without MPS the two processes' kernels time-slice on one GPU, so the
-    grids are small and the exchange waits span context switches.)"""
-    import socket
-
-    import torch.multiprocessing as mp
-    s = socket.socket()
-    s.bind(("127.0.0.1", 0))
-    port = s.getsockname()[1]
-    s.close()
-    with mp.Manager() as mgr:
-        out = mgr.dict()
-        mp.spawn(_ipc_worker, args=(2, port, out), nprocs=2, join=True)
-        res = dict(out)
-    cfg = get_config("T")
-    L, P = 3, 2
-    plan = m2c.plan_of(cfg, P)
-    ctxs = []
-    for r in range(P):
-        ctx = _ctx(m2c, cfg, plan, n_layers=L, shard=(r, P))
-        for l in range(L):
-            w = layer_weights(cfg, l, device="cuda", shard=(r, P))
-            ctx.load_layer(l, w["w_gate"], w["w_up"], w["w_down_t"], w["pred_A"], w["pred_B"])
-        ctx.set_grid(32)
-        ctxs.append(ctx)
-    xs = token_stream(cfg, 2, device="cuda")
-    for t in range(2):
-        xc = xs[t].contiguous().clone()
-        for l in range(L):
-            parts = []
-            for c in ctxs:
-                sel = c.predict_rank(l, xc, rank_list=False, tier_of=False, scores=False)
-                parts.append(c.sparse_ffn_forward(l, xc, sel["tier_ids"], want_partial=True)[0])
-            xc = xc + (parts[0] + parts[1]).half()
-        want = xc.cpu().numpy().tobytes()
-        assert res[0][t] == res[1][t] == want, t
     for c in ctxs:
         c.close()
 

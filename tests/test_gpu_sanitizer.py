@@ -1,0 +1,55 @@
+"""compute-sanitizer over the decode engines: racecheck (shared-memory hazards of
+the mbarrier rings and block-level hand-offs), synccheck (barrier misuse) and memcheck
+(out-of-bounds / misaligned accesses), on the T config (tools/sanitize_case.py).  Also the
+per-call surfacing of device-side invariant violations."""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SAN = "/usr/local/cuda/bin/compute-sanitizer"
+
+
+@pytest.mark.parametrize("tool", ["racecheck", "synccheck", "memcheck"])
+def test_compute_sanitizer_clean(tool):
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2410_14740_b200.build import build
+    build()
+    extra = ["--racecheck-report", "hazard"] if tool == "racecheck" else []
+    cmd = [SAN, "--tool", tool, "--error-exitcode", "9", *extra, sys.executable,
+           os.path.join(ROOT, "tools", "sanitize_case.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=1500, cwd=ROOT)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0, out[-4000:]
+    assert "sanitize case done" in out
+    assert "ERROR SUMMARY: 0 errors" in out or "RACECHECK SUMMARY: 0 hazards" in out, out[-2000:]
+
+
+def test_device_error_surfaces_on_next_call():
+    """A non-finite input makes the kernel flag err bit 1; the NEXT host call on the context
+    returns M2C_ERR_STATE without any explicit synchronisation by the caller."""
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2410_14740_b200 as m2c
+    from synth import get_config, layer_weights, token_stream
+    cfg = get_config("T")
+    plan = m2c.plan_of(cfg)
+    ctx = m2c.M2CContext(cfg.d_model, cfg.d_ff, 1, cfg.pred_rank, plan)
+    w = layer_weights(cfg, 0, device="cuda")
+    ctx.load_layer(0, w["w_gate"], w["w_up"], w["w_down_t"], w["pred_A"], w["pred_B"])
+    x = token_stream(cfg, 1, device="cuda")[0].contiguous()
+    x[5] = float("inf")
+    ctx.decode_step(x, 1)
+    torch.cuda.synchronize()  # (the caller's own sync; the library call below does not sync)
+    with pytest.raises(m2c.M2CError) as ei:
+        ctx.decode_step(token_stream(cfg, 1, device="cuda")[0].contiguous(), 2)
+    assert ei.value.code == 6 and "non-finite" in str(ei.value)
+    ctx.decode_step(token_stream(cfg, 1, device="cuda")[0].contiguous(), 3)  # reported once
+    torch.cuda.synchronize()
+    ctx.close()
