@@ -245,23 +245,47 @@ struct DownLd {
     float s;
     uint32_t z;
 };
+#ifndef M2C_DN_LD
+#define M2C_DN_LD 1  // 0: ld.global.cg (strong, L2); 1: ld.global.nc (read-only path, weak)
+#endif
+__device__ __forceinline__ uint4 ld_dn16(const void *p) {
+    uint4 v;
+    if (M2C_DN_LD) asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                                : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    else v = __ldcg(reinterpret_cast<const uint4 *>(p));
+    return v;
+}
+__device__ __forceinline__ uint2 ld_dn8(const void *p) {
+    uint2 v;
+    if (M2C_DN_LD) asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+    else v = __ldcg(reinterpret_cast<const uint2 *>(p));
+    return v;
+}
+__device__ __forceinline__ unsigned ld_dn4(const void *p) {
+    unsigned v;
+    if (M2C_DN_LD) asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
+    else v = __ldcg(reinterpret_cast<const unsigned *>(p));
+    return v;
+}
 template <int TIER>
 __device__ __forceinline__ void down_ldg(const uint8_t *rec, int d, DownLd<TIER> &o) {
     const int t = threadIdx.x;
     if (TIER == 0) {
-        o.v = __ldcg(reinterpret_cast<const uint4 *>(rec + 4 * d + 16 * t));
+        o.v = ld_dn16(rec + 4 * d + 16 * t);
     } else {
         const int G = d >> 7, grp = t >> 4;
         const int D = TIER == 1 ? d : d / 2;
         const uint8_t *sc = rec + 3 * D;
         if (TIER == 1) {
-            const uint2 w = __ldcg(reinterpret_cast<const uint2 *>(rec + 2 * d + 8 * t));
+            const uint2 w = ld_dn8(rec + 2 * d + 8 * t);
             o.v = make_uint4(w.x, w.y, 0, 0);
         } else {
-            o.v = make_uint4(__ldcg(reinterpret_cast<const unsigned *>(rec + d + 4 * t)), 0, 0, 0);
+            o.v = make_uint4(ld_dn4(rec + d + 4 * t), 0, 0, 0);
         }
-        o.s = half_bits_f(__ldcg(reinterpret_cast<const unsigned short *>(sc + 2 * (2 * G + grp))));
-        o.z = __ldcg(sc + 6 * G + 2 * G + grp);
+        const unsigned short *sp = reinterpret_cast<const unsigned short *>(sc + 2 * (2 * G + grp));
+        const unsigned char *zp = sc + 6 * G + 2 * G + grp;
+        o.s = half_bits_f(M2C_DN_LD ? __ldg(sp) : __ldcg(sp));
+        o.z = M2C_DN_LD ? __ldg(zp) : __ldcg(zp);
     }
 }
 template <int TIER>
@@ -398,6 +422,9 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
 #ifndef M2C_DN_PF
 #define M2C_DN_PF 1
 #endif
+#ifndef M2C_DN_TMA
+#define M2C_DN_TMA 0
+#endif
 template <class SrcFn>
 __device__ __forceinline__ void ffn_run(const FfnArgs &a, int d, int act, int n_items, int c1, int c2,
                                         SrcFn src, uint8_t *ring, const uint4 *xs, float *a_sm,
@@ -524,10 +551,71 @@ __device__ __forceinline__ void ffn_run(const FfnArgs &a, int d, int act, int n_
             else if (t == 1) down_acc<1>(rec + 2 * D, rec + 3 * D, d, aj, y);
             else down_acc<2>(rec + 2 * D, rec + 3 * D, d, aj, y);
         }
+    } else if (M2C_DN_TMA) {
+        // the down parts [2D, nb) (prefetched into L2 during phase G) -> the now free ring by
+        // TMA, warp 0 issuing one bulk copy per record (lane j -> record j), as many records
+        // per round as fit; then consumed from shared memory
+        for (int j0 = 0; j0 < n_items;) {
+            int j1 = j0, off = 0;
+            while (j1 < n_items && j1 - j0 < kNS) {  // (every thread computes the same split)
+                const int t = tier_of(j1), sz = a.nb[t] - 2 * Dof(t);
+                if (off + sz > kRing) break;
+                off += sz;
+                j1++;
+            }
+            const unsigned e0 = (unsigned)n_items + (unsigned)j0;  // full-barrier uses after the GU entries
+            if (warp == 0) {
+                fence_proxy_async();  // the ring's earlier generic reads precede these copies
+                int base = 0;
+                for (int q0 = j0; q0 < j1; q0 += 32) {
+                    const int j = q0 + lane;
+                    const int t = j < j1 ? tier_of(j) : 0;
+                    const int sz = j < j1 ? a.nb[t] - 2 * Dof(t) : 0;
+                    int inc = sz;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const int yv = __shfl_up_sync(0xffffffffu, inc, o);
+                        if (lane >= o) inc += yv;
+                    }
+                    if (j < j1) {
+                        const unsigned sl = fslot(e0 + (unsigned)(j - j0));
+                        sm.roff[sl] = base + inc - sz;
+                        mbar_expect_tx(&sm.full[sl], (uint32_t)sz);
+                        bulk_g2s(ring + base + inc - sz, src(j) + 2 * Dof(t), (uint32_t)sz, &sm.full[sl], pol);
+                    }
+                    base += __shfl_sync(0xffffffffu, inc, 31);
+                }
+            }
+            for (int j = j0; j < j1; j++) {
+                const unsigned e = e0 + (unsigned)(j - j0);
+                const unsigned sl = fslot(e);
+                mbar_wait(&sm.full[sl], fpar(e));
+                const int t = tier_of(j), D = Dof(t);
+                const uint8_t *ent = ring + sm.roff[sl];
+                if (t == 0) down_acc<0>(ent, ent + D, d, a_sm[j], y);
+                else if (t == 1) down_acc<1>(ent, ent + D, d, a_sm[j], y);
+                else down_acc<2>(ent, ent + D, d, a_sm[j], y);
+            }
+            pp.nf += (unsigned)(j1 - j0);  // (this round's full-barrier uses)
+            j0 = j1;
+            if (j0 < n_items) __syncthreads();  // the round is consumed before the next copies
+        }
     } else {
         down_seg_g<0>(src, a_sm, 0, c1, d, y);
         down_seg_g<1>(src, a_sm, c1, c2, d, y);
         down_seg_g<2>(src, a_sm, c2, n_items, d, y);
+#ifdef M2C_EXP_DN_TWICE  // measurement build only: a second pass over the (now L2-resident) columns
+        if (stamps && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(stamps[2]));
+        float y2[8];
+#pragma unroll
+        for (int i = 0; i < 8; i++) y2[i] = 0.f;
+        down_seg_g<0>(src, a_sm, 0, c1, d, y2);
+        down_seg_g<1>(src, a_sm, c1, c2, d, y2);
+        down_seg_g<2>(src, a_sm, c2, n_items, d, y2);
+#pragma unroll
+        for (int i = 0; i < 8; i++) y[i] += 0.f * y2[i];
+        if (stamps && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(stamps[3]));
+#endif
     }
     float *out = partial + (int64_t)blockIdx.x * d + 8 * threadIdx.x;
     reinterpret_cast<float4 *>(out)[0] = make_float4(y[0], y[1], y[2], y[3]);
@@ -557,7 +645,10 @@ __device__ __forceinline__ SmemPtrs carve(uint8_t *smem) {
 // balancing weight of one record, in 16-B units: bytes + lambda * 3d weights.  lambda = 6 B per
 // weight fits the per-CTA FFN times measured inside k_decode (round 1: ~0.9 us of dequant +
 // FMA per record at any precision plus ~12 ns per KB), i.e. the split is close to per-record.
-constexpr int kLambda = 6;
+#ifndef M2C_FFN_LAMBDA
+#define M2C_FFN_LAMBDA 6
+#endif
+constexpr int kLambda = M2C_FFN_LAMBDA;
 static inline int ffn_weight(int64_t nb, int d) { return (int)((nb + (int64_t)kLambda * 3 * d) / 16); }
 static inline void fill_args(m2c_ctx *c, const LayerState &L, const m2c_tier_plan &p, FfnArgs &a) {
     const int d = c->desc.d_model;
