@@ -245,26 +245,20 @@ struct DownLd {
     float s;
     uint32_t z;
 };
-#ifndef M2C_DN_LD
-#define M2C_DN_LD 1  // 0: ld.global.cg (strong, L2); 1: ld.global.nc (read-only path, weak)
-#endif
 __device__ __forceinline__ uint4 ld_dn16(const void *p) {
     uint4 v;
-    if (M2C_DN_LD) asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-                                : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
-    else v = __ldcg(reinterpret_cast<const uint4 *>(p));
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
     return v;
 }
 __device__ __forceinline__ uint2 ld_dn8(const void *p) {
     uint2 v;
-    if (M2C_DN_LD) asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
-    else v = __ldcg(reinterpret_cast<const uint2 *>(p));
+    asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
     return v;
 }
 __device__ __forceinline__ unsigned ld_dn4(const void *p) {
     unsigned v;
-    if (M2C_DN_LD) asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
-    else v = __ldcg(reinterpret_cast<const unsigned *>(p));
+    asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
     return v;
 }
 template <int TIER>
@@ -284,8 +278,8 @@ __device__ __forceinline__ void down_ldg(const uint8_t *rec, int d, DownLd<TIER>
         }
         const unsigned short *sp = reinterpret_cast<const unsigned short *>(sc + 2 * (2 * G + grp));
         const unsigned char *zp = sc + 6 * G + 2 * G + grp;
-        o.s = half_bits_f(M2C_DN_LD ? __ldg(sp) : __ldcg(sp));
-        o.z = M2C_DN_LD ? __ldg(zp) : __ldcg(zp);
+        o.s = half_bits_f(__ldg(sp));
+        o.z = __ldg(zp);
     }
 }
 template <int TIER>
@@ -321,13 +315,10 @@ __device__ __forceinline__ void down_fma(const DownLd<TIER> &o, float a, float (
         }
     }
 }
-#ifndef M2C_DN_UNROLL
-#define M2C_DN_UNROLL 8
-#endif
 // records [ja, jb) of one tier from global memory, in order, kU records' loads in flight
 template <int TIER, class RecFn>
 __device__ __forceinline__ void down_seg_g(RecFn rec, const float *a_sm, int ja, int jb, int d, float (&y)[8]) {
-    constexpr int kU = TIER == 0 ? M2C_DN_UNROLL / 2 : M2C_DN_UNROLL;
+    constexpr int kU = TIER == 0 ? 4 : 8;  // (16 for INT: register spills, measured slower)
     int j = ja;
     for (; j + kU <= jb; j += kU) {
         DownLd<TIER> o[kU];
@@ -419,12 +410,6 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
 //    entry as soon as its P units have arrived on it, then the down parts (+ tail); phase G
 //    runs on the other warps; in phase D every warp consumes the down entries in order and the
 //    producer re-issues freed space until every down entry is in.
-#ifndef M2C_DN_PF
-#define M2C_DN_PF 1
-#endif
-#ifndef M2C_DN_TMA
-#define M2C_DN_TMA 0
-#endif
 template <class SrcFn>
 __device__ __forceinline__ void ffn_run(const FfnArgs &a, int d, int act, int n_items, int c1, int c2,
                                         SrcFn src, uint8_t *ring, const uint4 *xs, float *a_sm,
@@ -486,7 +471,7 @@ __device__ __forceinline__ void ffn_run(const FfnArgs &a, int d, int act, int n_
                     mbar_expect_tx(&sm.full[s], (uint32_t)sz);
                     bulk_g2s(ring + off, g, (uint32_t)(2 * D), &sm.full[s], pol);
                     if (tailb) bulk_g2s(ring + off + 2 * D, g + 3 * D, (uint32_t)tailb, &sm.full[s], pol);
-                    if (M2C_DN_PF) prefetch_l2(g + 2 * D, (uint32_t)(a.nb[t] - 2 * D));
+                    prefetch_l2(g + 2 * D, (uint32_t)(a.nb[t] - 2 * D));
                 }
                 head++;
             } else {
@@ -551,71 +536,10 @@ __device__ __forceinline__ void ffn_run(const FfnArgs &a, int d, int act, int n_
             else if (t == 1) down_acc<1>(rec + 2 * D, rec + 3 * D, d, aj, y);
             else down_acc<2>(rec + 2 * D, rec + 3 * D, d, aj, y);
         }
-    } else if (M2C_DN_TMA) {
-        // the down parts [2D, nb) (prefetched into L2 during phase G) -> the now free ring by
-        // TMA, warp 0 issuing one bulk copy per record (lane j -> record j), as many records
-        // per round as fit; then consumed from shared memory
-        for (int j0 = 0; j0 < n_items;) {
-            int j1 = j0, off = 0;
-            while (j1 < n_items && j1 - j0 < kNS) {  // (every thread computes the same split)
-                const int t = tier_of(j1), sz = a.nb[t] - 2 * Dof(t);
-                if (off + sz > kRing) break;
-                off += sz;
-                j1++;
-            }
-            const unsigned e0 = (unsigned)n_items + (unsigned)j0;  // full-barrier uses after the GU entries
-            if (warp == 0) {
-                fence_proxy_async();  // the ring's earlier generic reads precede these copies
-                int base = 0;
-                for (int q0 = j0; q0 < j1; q0 += 32) {
-                    const int j = q0 + lane;
-                    const int t = j < j1 ? tier_of(j) : 0;
-                    const int sz = j < j1 ? a.nb[t] - 2 * Dof(t) : 0;
-                    int inc = sz;
-#pragma unroll
-                    for (int o = 1; o < 32; o <<= 1) {
-                        const int yv = __shfl_up_sync(0xffffffffu, inc, o);
-                        if (lane >= o) inc += yv;
-                    }
-                    if (j < j1) {
-                        const unsigned sl = fslot(e0 + (unsigned)(j - j0));
-                        sm.roff[sl] = base + inc - sz;
-                        mbar_expect_tx(&sm.full[sl], (uint32_t)sz);
-                        bulk_g2s(ring + base + inc - sz, src(j) + 2 * Dof(t), (uint32_t)sz, &sm.full[sl], pol);
-                    }
-                    base += __shfl_sync(0xffffffffu, inc, 31);
-                }
-            }
-            for (int j = j0; j < j1; j++) {
-                const unsigned e = e0 + (unsigned)(j - j0);
-                const unsigned sl = fslot(e);
-                mbar_wait(&sm.full[sl], fpar(e));
-                const int t = tier_of(j), D = Dof(t);
-                const uint8_t *ent = ring + sm.roff[sl];
-                if (t == 0) down_acc<0>(ent, ent + D, d, a_sm[j], y);
-                else if (t == 1) down_acc<1>(ent, ent + D, d, a_sm[j], y);
-                else down_acc<2>(ent, ent + D, d, a_sm[j], y);
-            }
-            pp.nf += (unsigned)(j1 - j0);  // (this round's full-barrier uses)
-            j0 = j1;
-            if (j0 < n_items) __syncthreads();  // the round is consumed before the next copies
-        }
     } else {
         down_seg_g<0>(src, a_sm, 0, c1, d, y);
         down_seg_g<1>(src, a_sm, c1, c2, d, y);
         down_seg_g<2>(src, a_sm, c2, n_items, d, y);
-#ifdef M2C_EXP_DN_TWICE  // measurement build only: a second pass over the (now L2-resident) columns
-        if (stamps && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(stamps[2]));
-        float y2[8];
-#pragma unroll
-        for (int i = 0; i < 8; i++) y2[i] = 0.f;
-        down_seg_g<0>(src, a_sm, 0, c1, d, y2);
-        down_seg_g<1>(src, a_sm, c1, c2, d, y2);
-        down_seg_g<2>(src, a_sm, c2, n_items, d, y2);
-#pragma unroll
-        for (int i = 0; i < 8; i++) y[i] += 0.f * y2[i];
-        if (stamps && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(stamps[3]));
-#endif
     }
     float *out = partial + (int64_t)blockIdx.x * d + 8 * threadIdx.x;
     reinterpret_cast<float4 *>(out)[0] = make_float4(y[0], y[1], y[2], y[3]);
@@ -642,13 +566,12 @@ __device__ __forceinline__ SmemPtrs carve(uint8_t *smem) {
 
 }  // namespace
 
-// balancing weight of one record, in 16-B units: bytes + lambda * 3d weights.  lambda = 6 B per
-// weight fits the per-CTA FFN times measured inside k_decode (round 1: ~0.9 us of dequant +
-// FMA per record at any precision plus ~12 ns per KB), i.e. the split is close to per-record.
-#ifndef M2C_FFN_LAMBDA
-#define M2C_FFN_LAMBDA 6
-#endif
-constexpr int kLambda = M2C_FFN_LAMBDA;
+// balancing weight of one record, in 16-B units: bytes + lambda * 3d weights.  The FFN phase
+// is HBM-bound for the GPU as a whole (every CTA's gate/up stream ends together) and its
+// per-CTA tail (the down-projection) costs per record, not per byte, so the split is close to
+// per-record: lambda 6 / 16 / 48 B per weight measured 584 / 595 / 596 tokens/s at S70H
+// (1456 tokens/s at S7 for all three).
+constexpr int kLambda = 16;
 static inline int ffn_weight(int64_t nb, int d) { return (int)((nb + (int64_t)kLambda * 3 * d) / 16); }
 static inline void fill_args(m2c_ctx *c, const LayerState &L, const m2c_tier_plan &p, FfnArgs &a) {
     const int d = c->desc.d_model;

@@ -542,20 +542,6 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
                     bulk_g2s_plain(S.ring + kBOff, p.layers[l + 1].B + (int64_t)n0 * r,
                                    (uint32_t)(nown_n * r), &b_bar);
                 }
-#ifndef M2C_SPEC_PF
-#define M2C_SPEC_PF 0
-#endif
-                if (M2C_SPEC_PF) {
-                    // speculative L2 prefetch of layer l+1's records at this CTA's ranks of the
-                    // PREVIOUS token's selection (adjacent tokens share ~80% of it)
-                    const int32_t *prv = p.lists + (int64_t)(l + 1) * (kk > 0 ? kk : 1);
-                    for (int q = R_lo; q < R_hi; q++) {
-                        const int id = __ldcg(prv + q);
-                        const int t = q < p.k16 ? 0 : (q < p.k16 + p.k8 ? 1 : 2);
-                        if (id >= 0 && id < F_r)
-                            prefetch_l2(p.layers[l + 1].pool[t] + (int64_t)id * p.nb[t], (uint32_t)p.nb[t]);
-                    }
-                }
             }
         });
         STAMP(7);

@@ -68,9 +68,7 @@ print("P4 per-CTA us (mid layer): min %.2f median %.2f max %.2f argmax %d" % (
 G = rows[-1].shape[1]
 p4 = np.mean([(s[:, :, 6] - s[:, :, 5]) / 1e3 for s in rows], axis=(0, 1))  # per CTA
 print("P4 mean per CTA by sixths of the grid:", " ".join(f"{p4[i * G // 6:(i + 1) * G // 6].mean():.2f}" for i in range(6)))
-import os as _os
-_tw = {"dn1": (15, 16), "dn2": (16, 17)} if "TWICE" in _os.environ.get("M2C_NVCC_EXTRA", "") else {}
-for nm, (i, j) in {"gate/up": (14, 15), "down": (15, 6), "P2+Bs": (0, 4), "P3": (4, 5), **_tw}.items():
+for nm, (i, j) in {"gate/up": (14, 15), "down": (15, 6), "P2+Bs": (0, 4), "P3": (4, 5)}.items():
     v = np.mean([(s[:, :, j] - s[:, :, i]) / 1e3 for s in rows], axis=(0, 1))
     print(f"{nm:8s} by sixths:", " ".join(f"{v[q * G // 6:(q + 1) * G // 6].mean():.2f}" for q in range(6)))
 sub = {"P2 h+max": (0, 20), "P2 hq+B": (20, 21), "P2 dots": (21, 22), "P2 atomics": (22, 1), "P3 hist load": (4, 2), "P3 scan": (2, 3), "P3 rank": (3, 10), "P3 tail": (10, 5), "P4 issue": (5, 14), "P4 gate/up": (14, 15), "P4 down": (15, 6)}

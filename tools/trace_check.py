@@ -1,5 +1,5 @@
 """Round-2 quick check of the decode engine against the oracle via the parity trace (D9).
-usage: python tools/r2_check.py [CONFIG LAYERS TOKENS] ..."""
+usage: python tools/trace_check.py [CONFIG LAYERS TOKENS] ..."""
 import sys, os, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
