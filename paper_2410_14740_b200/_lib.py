@@ -9,7 +9,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libm2c.so")
+# (M2C_LIB: another build of the same library, for same-box A/B measurements in tools/)
+LIB_PATH = os.environ.get("M2C_LIB") or os.path.join(_HERE, "libm2c.so")
 
 
 class M2CError(RuntimeError):

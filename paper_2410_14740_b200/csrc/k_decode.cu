@@ -56,7 +56,6 @@ constexpr int kStamps = kDecodeStamps;
 // ring offsets of the between-FFN phases (bytes)
 constexpr int kRfOff = 0;          // R: partial-row sums [nc * gw][33] f32; P2: hq [r]
 constexpr int kHistOff = 16384;    // P3: histogram copy [4096] i32
-constexpr int kAboveOff = 32768;   // P3: keys above bin b [4096] i32
 constexpr int kNeedOff = 49152;    // P3: needed bins / fallback candidates (16 KB)
 constexpr int kAtOff = 32768;      // R: A^T chunks of the next layer (<= 32 KB, staged at By)
 constexpr int kBOff = 65536;       // P2: this CTA's B slice (staged one layer ahead)
@@ -366,7 +365,6 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
 
         // ================= P3: this CTA's share of the selection, in rank order ============
         int *hs = reinterpret_cast<int *>(S.ring + kHistOff);
-        int *above = reinterpret_cast<int *>(S.ring + kAboveOff);
         int *need = reinterpret_cast<int *>(S.ring + kNeedOff);
         if (tid == 0) {
             // order the ring's earlier generic accesses (and the acquired global data) before
@@ -377,29 +375,52 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
             nneed = 0;
             ovf = 0;
         }
-        // next token's histogram scale for this layer: |s| < 2048 << sh (no clamped bins)
-        if (cta == 0 && warp == 0) {
-            unsigned m = 0;
-            for (int c = lane; c < G; c += 32) m = max(m, __ldcg(p.sabs + c));
-            m = __reduce_max_sync(0xffffffffu, m);
-            int sh = 0;
-            while ((m >> sh) >= 2048u) sh++;
-            if (lane == 0) p.bin_sh[l] = sh;
-            for (int c = lane; c < G; c += 32) p.sabs[c] = 0;  // read: reset for the next layer
-        }
-        // h of this layer was consumed in P2: clear it for layer l+2 (accumulated after By of l+1)
-        if (cta == 0)
-            for (int i = tid; i < r; i += NT) hcur[(int64_t)i * kHStride] = 0;
-        // the other histogram buffer was last read in layer l-1's P3: clear it for layer l+1
-        if (cta == G - 1)
-            for (int i = tid; i < kBins; i += NT) p.ghist[((l + 1) & 1) * kBins + i] = 0;
+        // per-layer bookkeeping, after Bs (every CTA's P2 is done), on three CTAs: the next
+        // token's histogram scale for this layer (|s| < 2048 << sh: no clamped bins) and the
+        // reset of the per-CTA max |s|; h of this layer (consumed in P2) cleared for layer
+        // l+2; the other histogram (last read in layer l-1's P3) cleared for layer l+1.  It
+        // runs in R on the last three CTAs when they own no R chunk (G > d/32 + 2: S7), else
+        // here in P3 on the first three (their FP16-heavy FFN shares finish first: S70H)
+        const bool bk_in_r = !p.select_only && G >= 3 && G - 3 >= nchunk;
+        const int bk0 = bk_in_r ? G - 3 : 0;
+        auto bookkeeping = [&] {
+            if (cta == min(bk0, G - 1) && warp == 0) {
+                unsigned m = 0;
+                for (int c = lane; c < G; c += 32) m = max(m, __ldcg(p.sabs + c));
+                m = __reduce_max_sync(0xffffffffu, m);
+                int sh = 0;
+                while ((m >> sh) >= 2048u) sh++;
+                if (lane == 0) p.bin_sh[l] = sh;
+                for (int c = lane; c < G; c += 32) p.sabs[c] = 0;
+            }
+            if (cta == min(bk0 + 1, G - 1))
+                for (int i = tid; i < r; i += NT) hcur[(int64_t)i * kHStride] = 0;
+            if (cta == min(bk0 + 2, G - 1))
+                for (int i = tid; i < kBins; i += NT) p.ghist[((l + 1) & 1) * kBins + i] = 0;
+        };
+        if (!bk_in_r) bookkeeping();
         mbar_wait(&sel_bar, (uint32_t)(l & 1));
         STAMP(2);
-        {  // above[b] = #keys in bins > b: per-thread chunks of bins (descending), block scan
+        {  // keys above each bin: per-thread runs of BPT bins (descending), block scan (warp
+            // prefixes by shuffles, not a serial walk over the warps); the bins holding ranks of
+            // the share go to need[] with their "above" counts at need[2048 + i]
             const int BPT = (kBins + NT - 1) / NT;  // 4 (1024 threads) .. 128 (32 threads)
             const int b_hi = max(kBins - tid * BPT, 0), b_lo = max(b_hi - BPT, 0);
+            int cv[8];
             int sum = 0;
-            for (int b = b_hi - 1; b >= b_lo; b--) sum += hs[b];
+            if (BPT == 8) {  // (512 threads) two LDS.128, the run stays in registers
+                const int4 v0 = reinterpret_cast<const int4 *>(hs + b_lo)[0];
+                const int4 v1 = reinterpret_cast<const int4 *>(hs + b_lo)[1];
+                cv[0] = v1.w; cv[1] = v1.z; cv[2] = v1.y; cv[3] = v1.x;
+                cv[4] = v0.w; cv[5] = v0.z; cv[6] = v0.y; cv[7] = v0.x;
+                sum = (cv[0] + cv[1]) + (cv[2] + cv[3]) + ((cv[4] + cv[5]) + (cv[6] + cv[7]));
+            } else if (BPT == 4) {  // (1024 threads) one LDS.128
+                const int4 v0 = *reinterpret_cast<const int4 *>(hs + b_lo);
+                cv[0] = v0.w; cv[1] = v0.z; cv[2] = v0.y; cv[3] = v0.x;
+                sum = (cv[0] + cv[1]) + (cv[2] + cv[3]);
+            } else {
+                for (int b = b_hi - 1; b >= b_lo; b--) sum += hs[b];
+            }
             int inc = sum;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
@@ -408,16 +429,35 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
             }
             if (lane == 31) red_i[warp] = inc;
             __syncthreads();
-            int acc = inc - sum;  // keys in bins >= b_hi
-            for (int w = 0; w < warp; w++) acc += red_i[w];
-            for (int b = b_hi - 1; b >= b_lo; b--) {
-                const int c = hs[b];
-                above[b] = acc;
+            int wt = lane < NW ? red_i[lane] : 0;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, wt, o);
+                if (lane >= o) wt += y;
+            }
+            const int wpre = warp > 0 ? __shfl_sync(0xffffffffu, wt, warp - 1) : 0;
+            int acc = wpre + inc - sum;  // keys in bins >= b_hi
+            auto visit = [&](int b, int c) {  // bin b (c keys), acc = keys in bins > b
                 if (c > 0 && acc < R_hi && acc + c > R_lo) {  // bin b holds ranks of the share
-                    need[atomicAdd(&nneed, 1)] = b;
+                    const int at = atomicAdd(&nneed, 1);
+                    if (at < 2048) {
+                        need[at] = b;
+                        need[2048 + at] = acc;
+                    }
                     if (c > kCap) ovf = 1;
                 }
                 acc += c;
+            };
+            if (acc < R_hi && acc + sum > R_lo) {  // this run holds ranks of the share
+                if (BPT == 8) {
+#pragma unroll
+                    for (int k = 0; k < 8; k++) visit(b_hi - 1 - k, cv[k]);
+                } else if (BPT == 4) {
+#pragma unroll
+                    for (int k = 0; k < 4; k++) visit(b_hi - 1 - k, cv[k]);
+                } else {
+                    for (int b = b_hi - 1; b >= b_lo; b--) visit(b, hs[b]);
+                }
             }
         }
         __syncthreads();
@@ -425,9 +465,9 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
         if (!ovf) {
             // warp per needed bin: its keys (<= kCap, 4 per lane), exact rank of each inside
             // the bin by counting larger keys; global rank = above[b] + that
-            const int nn = nneed;
+            const int nn = min(nneed, 2048);
             for (int w = warp; w < nn; w += NW) {
-                const int b = need[w], c = hs[b], ab = above[b];
+                const int b = need[w], c = hs[b], ab = need[2048 + w];
                 const unsigned long long *bk = bkt + (size_t)b * kCap;
                 unsigned long long kv[4];
                 int rk[4];
@@ -545,8 +585,8 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
             }
         });
         STAMP(7);
-        if (l == p.n_layers - 1 && cta == G - 1)  // leave both histograms clear for the next token
-            for (int i = tid; i < kBins; i += NT) hist[i] = 0;
+        // (each layer's histogram is cleared by the previous layer's bookkeeping, layer 0's by
+        // the prologue)
 
         // ================= R: fixed-order reduction + residual + next layer's h ==============
         {
@@ -635,6 +675,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
                 }
             }
         }
+        if (bk_in_r) bookkeeping();
         STAMP(8);
         if (more) grid_sync(p.bar_flags, base + ++nbar, p.err);
     }

@@ -1,0 +1,6 @@
+#!/bin/bash
+cd "$GRAFT_REPO_ROOT" 2>/dev/null || cd /root/repo
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_engines.py tests/test_gpu_parity.py -x -q > gpurun_out/g6_tests.log 2>&1; echo "exit=$?" >> gpurun_out/g6_tests.log
+LIBS="build/ab_head/libm2c.so build/ab_new/libm2c.so" CFGS="S70H S7 S13" bash tools/abl.sh
+true
