@@ -301,19 +301,7 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
                  "r"(bytes)
                  : "memory");
 }
-#ifndef M2C_MBAR_HINT
-#define M2C_MBAR_HINT 0  // try_wait suspend-time hint (ns); 0 = the system default
-#endif
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
-#if M2C_MBAR_HINT > 0
-    asm volatile(
-        "{\n\t.reg .pred p;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
-        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-        "r"(parity), "n"(M2C_MBAR_HINT)
-        : "memory");
-#else
     asm volatile(
         "{\n\t.reg .pred p;\n"
         "WAIT_%=:\n\t"
@@ -321,7 +309,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
         "r"(parity)
         : "memory");
-#endif
 }
 // one non-blocking probe of an mbarrier phase
 __device__ __forceinline__ bool mbar_test(uint64_t *bar, uint32_t parity) {

@@ -28,7 +28,7 @@ for t in range(T):
     s = ctx.profile_stamps().astype(np.int64)  # [L, G, 10]
     rows.append(s)
 ctx.profile(False)
-names = ["P2 hq+s+hist", "Bs", "P3 select", "P3 tail", "P4 ffn", "P4->R", "R red+h", "Bx"]
+names = ["P2 hq+s+hist", "Bs", "P3 select", "P3 tail", "P4 ffn", "By", "R red+h", "Bx"]
 acc = {k: [] for k in names}
 accm = {k: [] for k in names}
 tot = []
@@ -50,7 +50,7 @@ for s in rows:
             "P3 select": ph(4, 10),
             "P3 tail": ph(10, 5),
             "P4 ffn": ph(5, 6),
-            "P4->R": ph(6, 7),
+            "By": br(6, a[:, 7]),
             "R red+h": ph(7, 8),
             "Bx": br(8, nxt0),
         }
