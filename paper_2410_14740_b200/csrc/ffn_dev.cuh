@@ -571,8 +571,12 @@ __device__ __forceinline__ SmemPtrs carve(uint8_t *smem) {
 // per-CTA tail (the down-projection) costs per record, not per byte, so the split is close to
 // per-record: lambda 6 / 16 / 48 B per weight measured 584 / 595 / 596 tokens/s at S70H
 // (1456 tokens/s at S7 for all three).
-constexpr int kLambda = 16;
-static inline int ffn_weight(int64_t nb, int d) { return (int)((nb + (int64_t)kLambda * 3 * d) / 16); }
+constexpr int kLambda = 16, kLambdaQ = 18;  // FP16 / INT8 + INT4 records (same-box A/B,
+                                           // profiles/r02_ffn_variants.txt: INT lambda 16/18/20/24)
+static inline int ffn_weight(int64_t nb, int d) {
+    const int64_t lam = nb >= 6 * (int64_t)d ? kLambda : kLambdaQ;  // FP16 records are 6d bytes
+    return (int)((nb + lam * 3 * d) / 16);
+}
 static inline void fill_args(m2c_ctx *c, const LayerState &L, const m2c_tier_plan &p, FfnArgs &a) {
     const int d = c->desc.d_model;
     const int seg[3] = {0, p.k_fp16, p.k_fp16 + p.k_int8};
