@@ -333,6 +333,8 @@ def main():
         ctx.stats(reset=True)
     if args.lookahead and cfg.cache_mode != "resident":
         ctx.lookahead_stats(reset=True)
+    if cfg.cache_mode != "resident":
+        ctx.requant_stats(reset=True)
 
     def barrier():
         if world > 1:
@@ -356,6 +358,7 @@ def main():
     ms = m2c_dist.max_over_ranks(ms, device=dev)
     st = ctx.stats()
     staged = ctx.lookahead_stats() if args.lookahead and cfg.cache_mode != "resident" else 0
+    requant = ctx.requant_stats(reset=True) if cfg.cache_mode != "resident" else [0, 0, 0]
     kpt = st["kernels_per_token"]
     tok_s = K / (ms / 1e3)
     ab = algorithmic_bytes(cfg, plan, P)
@@ -383,6 +386,7 @@ def main():
         if lru:
             fill_ms += sum(ctx.profile_fill())
     fill_misses = ctx.stats()["misses"] if lru else None
+    fill_requant = ctx.requant_stats(reset=True) if lru else [0, 0, 0]
     ctx.profile(False)
     phase_ms = [sum(prof[l][i] for l in range(cfg.n_layers)) for i in range(4)]
     if fused or split:
@@ -540,11 +544,14 @@ def main():
         if cfg.cache_mode != "resident":
             line["cache"] = {"hits": hits, "misses": miss, "lookahead": bool(args.lookahead),
                              "staged_fills": staged,
+                             "requant_fills": requant,
                              "hit_ratio": [h / max(1, h + m) for h, m in zip(hits, miss)]}
             # the H2D link bounds this config -- miss-fill bytes against the
             # box's pinned H2D peak, measured in the same run
             from paper_2410_14740_b200 import record_bytes
-            fill_b = sum(m * record_bytes(b, cfg.d_model) for m, b in zip(miss, (16, 8, 4))) / K
+            # (the requantised fills of INT misses come from the resident FP16 records: no PCIe)
+            fill_b = sum((m - q) * record_bytes(b, cfg.d_model)
+                         for m, q, b in zip(miss, requant, (16, 8, 4))) / K
             line["pcie"] = {"h2d_peak_gbs": h2d_peak, "fill_bytes_per_token": fill_b,
                             "fill_gbs_whole_token": fill_b * tok_s / 1e9,
                             "frac_of_h2d_peak": fill_b * tok_s / 1e9 / h2d_peak,
@@ -552,7 +559,8 @@ def main():
                                     "overlap the hit FFN); peak = 256 MiB pinned cudaMemcpyAsync"}
             # the dominant kernel of an LRU config is the miss fill (k_fill, ~65% of the launch
             # time): bound by the H2D link, not HBM -- its roofline is the measured H2D peak
-            fb = sum(m * record_bytes(b, cfg.d_model) for m, b in zip(fill_misses, (16, 8, 4)))
+            fb = sum((m - q) * record_bytes(b, cfg.d_model)
+                     for m, q, b in zip(fill_misses, fill_requant, (16, 8, 4)))
             n_fill = nprof * sum(1 for _ in range(cfg.n_layers))
             f_ach = fb / (fill_ms / 1e3) / 1e9 if fill_ms > 0 else None
             line["roofline_hbm_kernel"] = line["roofline"]  # (the FFN kernel, for reference)

@@ -271,6 +271,14 @@ m2c_status m2c_profile_read(m2c_ctx *ctx, float *ms, int32_t *ffn_launches_out);
  * profiling is off or the last step ran k_decode alone (no fills). */
 m2c_status m2c_profile_fill(m2c_ctx *ctx, float *ms_per_layer);
 m2c_status m2c_profile_stamps(m2c_ctx *ctx, uint64_t *out, int64_t cap, int64_t *n_out);
+/* m2c_profile_events: the last decode step's per-layer CUDA-event timeline (kernel-chain
+ * engines: resident chain, LRU/ATU), ms since layer 0's first mark, [n_layers][9]: compute
+ * stream 0 layer start, 1 predictor done, 2 select done, 3 FFN done, 4 reduce done; copy stream
+ * 5 miss fill start, 6 miss fill end; compute stream (early-fill LRU engine) 7 LRU update done,
+ * 8 hit FFN done (-1: not recorded).  The copy-versus-compute overlap of the LRU engine (P:11,
+ * P:396) is read from it.  *n_out = n_layers * 9 (out may be null);
+ * M2C_ERR_STATE if profiling is off or the last step was one k_decode launch. */
+m2c_status m2c_profile_events(m2c_ctx *ctx, float *out, int64_t cap, int64_t *n_out);
 
 /* Kernels launched by the last m2c_decode_step (per token), and cumulative cache counters
  * (hits, misses per tier) since the last reset (device counters; synchronises). */
@@ -311,6 +319,20 @@ m2c_status m2c_set_global_topk(m2c_ctx *ctx, const m2c_tier_plan *global_plan);
  * m2c_lookahead_stats: misses filled from staging so far (reset: zero it). */
 m2c_status m2c_set_lookahead(m2c_ctx *ctx, int32_t enable);
 m2c_status m2c_lookahead_stats(m2c_ctx *ctx, int64_t *staged_fills, int32_t reset);
+
+/* ---- a5 fill source: GPU requantisation of tier-churn misses (early-fill LRU/ATU engine) --
+ * A neuron selected in the INT8 or INT4 tier that misses that tier's pool but whose FP16
+ * record is resident in the layer's FP16 pool (it was active in the FP16 tier recently: ranks
+ * move across the tier cuts from token to token) gets its record by quantising
+ * the resident FP16 record on the GPU with the offline pack's function (R4, bit-identical to
+ * the host tier's record, O0) instead of a PCIe copy ("reduce the data movement").  The
+ * miss is still a miss: the cache state, the hit / miss / eviction counts and the outputs are
+ * unchanged; only the bytes crossing PCIe shrink.  On by default (decode engine only; the
+ * per-call m2c_cache_lookup_fill always copies from the host tier).
+ *   m2c_set_requant(ctx, 0 / 1): off / on (invalidates the captured decode graph).
+ *   m2c_requant_stats(ctx, out[3], reset): requantised fills per tier so far (out[0] = 0). */
+m2c_status m2c_set_requant(m2c_ctx *ctx, int32_t enable);
+m2c_status m2c_requant_stats(m2c_ctx *ctx, int64_t *requant_fills, int32_t reset);
 
 /* ---- NEXT-1: SSD -> DRAM tier (§5.4) -----------------
  * The paper keeps the whole model on SSD and stages it into DRAM layer-wise with a two-level

@@ -73,12 +73,15 @@ SIGNATURES = [
     ("m2c_profile", C.c_int, [_vp, _i32]),
     ("m2c_profile_read", C.c_int, [_vp, _P(C.c_float), _P(_i32)]),
     ("m2c_profile_fill", C.c_int, [_vp, _P(C.c_float)]),
+    ("m2c_profile_events", C.c_int, [_vp, _P(C.c_float), _i64, _P(_i64)]),
     ("m2c_profile_stamps", C.c_int, [_vp, _P(C.c_uint64), _i64, _P(_i64)]),
     ("m2c_predict_candidates", C.c_int, [_vp, _i32, _vp, _i32, _vp]),
     ("m2c_select_global", C.c_int, [_vp, _vp, _i32, _P(TierPlan), _vp, _vp]),
     ("m2c_set_global_topk", C.c_int, [_vp, _P(TierPlan)]),
     ("m2c_set_lookahead", C.c_int, [_vp, _i32]),
     ("m2c_lookahead_stats", C.c_int, [_vp, _P(_i64), _i32]),
+    ("m2c_set_requant", C.c_int, [_vp, _i32]),
+    ("m2c_requant_stats", C.c_int, [_vp, _P(_i64), _i32]),
     ("m2c_store_frame_bytes", _sz, [_P(ModelDesc), _P(CacheCfg)]),
     ("m2c_store_write", C.c_int, [_vp, C.c_char_p]),
     ("m2c_store_attach", C.c_int, [_vp, C.c_char_p, _i32, _i32, _i32, _vp, _sz]),

@@ -105,7 +105,10 @@ class M2CContext:
         self.plan = plan
         # a dedicated (non-default) stream: the decode step is CUDA-graph captured on it; calls
         # are ordered with the caller's current stream by event waits both ways (_call)
-        self.compute = compute_stream or torch.cuda.Stream(self.device)
+        # the compute stream outranks the copy stream: the miss fill's long-running CTAs must
+        # not delay the per-layer compute chain's CTAs (LRU engine, P:396 overlap)
+        prio = -1 if os.environ.get("M2C_PRIO", "1") != "0" else 0
+        self.compute = compute_stream or torch.cuda.Stream(self.device, priority=prio)
         self.copy = copy_stream or torch.cuda.Stream(self.device)
         h = C.c_void_p()
         check(lib().m2c_create(C.byref(self.desc), self.device.index,
@@ -181,6 +184,15 @@ class M2CContext:
     # ---- NEXT-2: cross-layer lookahead staging (include/m2c.h) ----
     def set_lookahead(self, enable: bool):
         self._call(lib().m2c_set_lookahead, self._h, 1 if enable else 0)
+
+    def set_requant(self, enable: bool = True):
+        """GPU requantisation of INT misses from resident FP16 records (include/m2c.h)."""
+        self._call(lib().m2c_set_requant, self._h, 1 if enable else 0)
+
+    def requant_stats(self, reset=False):
+        v = (C.c_int64 * 3)()
+        check(lib().m2c_requant_stats(self._h, v, 1 if reset else 0))
+        return [int(x) for x in v]
 
     def lookahead_stats(self, reset=False):
         v = C.c_int64()
@@ -344,6 +356,16 @@ class M2CContext:
         ms = (C.c_float * self.desc.n_layers)()
         check(lib().m2c_profile_fill(self._h, ms))
         return list(ms)
+
+    def profile_events(self):
+        """Per-layer CUDA-event timeline of the last (kernel-chain) decode step, ms since the
+        first mark: numpy float32 [n_layers, 9] (include/m2c.h m2c_profile_events)."""
+        import numpy as np
+        n = C.c_int64()
+        check(lib().m2c_profile_events(self._h, None, 0, C.byref(n)))
+        buf = (C.c_float * n.value)()
+        check(lib().m2c_profile_events(self._h, buf, n.value, C.byref(n)))
+        return np.frombuffer(buf, dtype=np.float32).copy().reshape(self.desc.n_layers, -1)
 
     def profile_stamps(self):
         """Raw k_decode stamps of the last decode step (profiling on): numpy uint64

@@ -167,7 +167,7 @@ static int32_t *step_ptr(m2c_ctx *c) { return c->ws.counts + 15; }
 // ---- the token: all layers on the compute stream (+ copy stream for LRU fills) ----
 // profiling events per layer: 5 compute-stream marks (phase boundaries) + 2 around the miss
 // fill on the copy stream
-constexpr int kProfEv = 7;
+constexpr int kProfEv = 9;  // (+ 7 after the LRU update, 8 after the hit FFN: early-fill engine)
 static cudaError_t mark_copy(m2c_ctx *c, int l, int i) {
     if (c->prof_ev.empty()) return cudaSuccess;
     return cudaEventRecordWithFlags(c->prof_ev[kProfEv * l + 5 + i], c->copy, cudaEventRecordExternal);
@@ -201,12 +201,19 @@ static bool early_fill_on(const m2c_ctx *c) {
     return env_on && c->early_fill && c->early_mem && !c->lookahead && !c->store;
 }
 
+// GPU requantisation of INT misses from resident FP16 records (early-fill engine);
+// M2C_REQUANT=0 disables it (A/B knob, results identical)
+static bool requant_on(const m2c_ctx *c) {
+    static const bool env_on = !(getenv("M2C_REQUANT") && atoi(getenv("M2C_REQUANT")) == 0);
+    return env_on && c->requant;
+}
+
 static cudaError_t early_fill_alloc(m2c_ctx *c) {
     if (c->early_mem) return cudaSuccess;
     const m2c_tier_plan &p = c->plan;
     const int k = p.k > 0 ? p.k : 1;
     const int kt[3] = {p.k_fp16, p.k_int8, p.k_int4};
-    size_t off = a256(4 * (16 + (size_t)k)) + a256(4 * (size_t)k), st_off[3];
+    size_t off = a256(4 * (16 + (size_t)k)) + 2 * a256(4 * (size_t)k), st_off[3];
     for (int t = 0; t < 3; t++) {
         st_off[t] = off;
         off += a256((size_t)(kt[t] > 0 ? kt[t] : 1) * c->nb[t]);
@@ -216,6 +223,7 @@ static cudaError_t early_fill_alloc(m2c_ctx *c) {
     uint8_t *b = static_cast<uint8_t *>(c->early_mem);
     c->mq = reinterpret_cast<int32_t *>(b);
     c->ident = reinterpret_cast<int32_t *>(b + a256(4 * (16 + (size_t)k)));
+    c->mq_src = reinterpret_cast<int32_t *>(b + a256(4 * (16 + (size_t)k)) + a256(4 * (size_t)k));
     for (int t = 0; t < 3; t++) c->mstage[t] = b + st_off[t];
     std::vector<int32_t> id(k, 0);
     for (int t = 0, seg = 0; t < 3; seg += kt[t], t++)
@@ -304,12 +312,18 @@ static cudaError_t enqueue_layer(m2c_ctx *c, int l, __half *x) {
         // early fill: the misses (ids without a slot) are queued first and their host-tier
         // copies start into the staging area while k_lru chooses the victims; the miss FFN
         // reads the staging area; the copy stream then scatters the records into their slots
-        if ((e = launch_missq(c, L, ids, p, st))) return e;
+        // An INT8 / INT4 miss whose neuron is resident in the FP16 pool is filled by quantising
+        // that record on the GPU (k_requant, the offline pack's function) instead of over PCIe
+        const bool rq = requant_on(c);
+        if ((e = launch_missq(c, L, ids, p, st, rq ? c->mq_src : nullptr))) return e;
         if ((e = cudaEventRecord(c->ev_q, st))) return e;
         if ((e = cudaStreamWaitEvent(c->copy, c->ev_q, 0))) return e;
         if ((e = mark_copy(c, l, 0))) return e;
         const uint8_t *hsrc[3] = {L.host_rec[0], L.host_rec[1], L.host_rec[2]};
-        if ((e = launch_copy_recs(c, hsrc, c->mstage, p, c->mq, c->mq + 16, c->ident, c->copy))) return e;
+        if ((e = launch_copy_recs(c, hsrc, c->mstage, p, c->mq, c->mq + 16, c->ident, c->copy,
+                                  rq ? c->mq_src : nullptr)))
+            return e;
+        if (rq && (e = launch_requant(c, L, p, st))) return e;
         if ((e = mark_copy(c, l, 1))) return e;
         if ((e = cudaEventRecord(c->ev_fill, c->copy))) return e;
         // the previous layer's scatter (copy stream) reads ws.counts[8..10] and ws.miss_items,
@@ -318,6 +332,7 @@ static cudaError_t enqueue_layer(m2c_ctx *c, int l, __half *x) {
         if (c->scat_pending && (e = cudaStreamWaitEvent(st, c->ev_scat, 0))) return e;
         e = launch_lru(c, L, step_ptr(c), ids, p, c->ws.slots, c->ws.hit_bits, nullptr, nullptr, st);
         if (e) return e;
+        if ((e = mark(c, l, 7))) return e;
         if ((e = cudaEventRecord(c->ev_lookup, st))) return e;
         if ((e = cudaStreamWaitEvent(c->copy, c->ev_lookup, 0))) return e;
         const uint8_t *ssrc[3] = {c->mstage[0], c->mstage[1], c->mstage[2]};
@@ -328,6 +343,7 @@ static cudaError_t enqueue_layer(m2c_ctx *c, int l, __half *x) {
         c->scat_pending = true;
         e = launch_ffn(c, L, x, c->ws.hit_items, c->ws.counts + 4, p, c->ws.partial, st);
         if (e) return e;
+        if ((e = mark(c, l, 8))) return e;
         if ((e = cudaStreamWaitEvent(st, c->ev_fill, 0))) return e;
         LayerState Ls = L;
         for (int t = 0; t < 3; t++) Ls.pool[t] = c->mstage[t];
@@ -549,7 +565,7 @@ m2c_status m2c_create(const m2c_model_desc *desc, int32_t device, m2c_stream_t c
                  o_hit = take(4 * (size_t)F_r), o_miss = take(4 * (size_t)F_r),
                  o_mid = take(4 * (size_t)F_r), o_cnt = take(4 * 16),
                  o_part = take(4 * (size_t)2 * c->G * d), o_y = take(4 * (size_t)d),
-                 o_x = take(2 * (size_t)d), o_stats = take(8 * 8), o_err = take(16),
+                 o_x = take(2 * (size_t)d), o_stats = take(8 * 16), o_err = take(16),
                  o_hist = take(4 * 2 * 4096), o_sst = take(8 * (size_t)select_blocks(F_r)),
                  o_sdone = take(4), o_sepoch = take(4), o_bflags = take(4 * (size_t)c->G),
                  o_bepoch = take(4), o_dlay = take(decode_layer_table_bytes(desc->n_layers)),
@@ -1199,6 +1215,28 @@ m2c_status m2c_profile_fill(m2c_ctx *c, float *ms) {
     return M2C_OK;
 }
 
+m2c_status m2c_profile_events(m2c_ctx *c, float *ms, int64_t cap, int64_t *n_out) {
+    if (!c || !n_out) return fail(M2C_ERR_INVALID_ARG, "null argument");
+    const int64_t n = (int64_t)kProfEv * c->desc.n_layers;
+    *n_out = n;
+    if (!ms) return M2C_OK;
+    if (cap < n) return fail(M2C_ERR_INVALID_ARG, "profile_events: buffer too small");
+    if (c->prof_ev.empty()) return fail(M2C_ERR_STATE, "profiling not enabled");
+    if (c->last_token_fused || c->last_token_split)
+        return fail(M2C_ERR_STATE, "profile_events: the last step was one k_decode launch (use m2c_profile_stamps)");
+    M2C_CUDA(cudaStreamSynchronize(c->copy));
+    M2C_CUDA(cudaStreamSynchronize(c->compute));
+    for (int l = 0; l < c->desc.n_layers; l++)
+        for (int i = 0; i < kProfEv; i++) {
+            float v = -1.f;  // (a mark the layer's engine did not record)
+            if (i < 5 || (c->layers[l].mode != 0 && (i < 7 || early_fill_on(c))))
+                if (cudaEventElapsedTime(&v, c->prof_ev[0], c->prof_ev[kProfEv * l + i]) != cudaSuccess) v = -1.f;
+            ms[kProfEv * l + i] = v;
+        }
+    cudaGetLastError();  // (an unrecorded mark leaves a sticky-free error)
+    return M2C_OK;
+}
+
 m2c_status m2c_profile_stamps(m2c_ctx *c, uint64_t *out, int64_t cap, int64_t *n_out) {
     if (!c || !n_out) return fail(M2C_ERR_INVALID_ARG, "null argument");
     const int64_t n = (int64_t)kDecodeStamps * c->G * c->desc.n_layers;
@@ -1311,6 +1349,27 @@ m2c_status m2c_set_lookahead(m2c_ctx *c, int32_t enable) {
     }
     c->lookahead = enable != 0;
     if (c->graph) {
+        cudaGraphExecDestroy(c->graph);
+        c->graph = nullptr;
+    }
+    return M2C_OK;
+}
+
+m2c_status m2c_requant_stats(m2c_ctx *c, int64_t *requant_fills, int32_t reset) {
+    if (!c || !requant_fills) return fail(M2C_ERR_INVALID_ARG, "null argument");
+    M2C_CHECK_DEVICE_FLAG(c);
+    unsigned long long v[3] = {0, 0, 0};
+    M2C_CUDA(cudaStreamSynchronize(c->compute));
+    M2C_CUDA(cudaMemcpy(v, c->ws.stats + 8, sizeof(v), cudaMemcpyDeviceToHost));
+    for (int t = 0; t < 3; t++) requant_fills[t] = (int64_t)v[t];
+    if (reset) M2C_CUDA(cudaMemset(c->ws.stats + 8, 0, sizeof(v)));
+    return M2C_OK;
+}
+
+m2c_status m2c_set_requant(m2c_ctx *c, int32_t enable) {
+    if (!c) return fail(M2C_ERR_INVALID_ARG, "null ctx");
+    c->requant = enable != 0;
+    if (c->graph) {  // (the captured decode graph bakes the engine's launches in)
         cudaGraphExecDestroy(c->graph);
         c->graph = nullptr;
     }

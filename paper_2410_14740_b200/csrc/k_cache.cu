@@ -186,8 +186,11 @@ __global__ void __launch_bounds__(NT, 1)
 // start into a staging area while k_lru runs; the miss FFN reads the staging area and the
 // records are scattered into their victim slots afterwards (copy stream).
 __global__ void __launch_bounds__(NT, 1)
-    k_missq(LruArgs a, const int32_t *__restrict__ tier_ids, int32_t *__restrict__ q) {
-    // q: [16] header (q[8 + t] = misses of tier t) | ids [k] (segments as tier_ids)
+    k_missq(LruArgs a, const int32_t *__restrict__ tier_ids, int32_t *__restrict__ q,
+            int32_t *__restrict__ qsrc) {
+    // q: [16] header (q[8 + t] = misses of tier t) | ids [k] (segments as tier_ids);
+    // qsrc (or null): per entry the neuron's FP16-pool slot for an INT8 / INT4 miss whose FP16
+    // record is resident (filled by requantisation, k_requant), else -1
     __shared__ int scan_sm[NW];
     griddep_wait();
     const int tau = blockIdx.x;
@@ -201,7 +204,10 @@ __global__ void __launch_bounds__(NT, 1)
     int tot;
     int pos = block_scan1(nm, &tot, scan_sm);
     for (int i = i0; i < i1; i++)
-        if (slot_of[R[i]] < 0) q[16 + seg + pos++] = R[i];
+        if (slot_of[R[i]] < 0) {
+            if (qsrc) qsrc[seg + pos] = tau > 0 ? a.slot_of[0][R[i]] : -1;
+            q[16 + seg + pos++] = R[i];
+        }
     if (threadIdx.x == 0) q[8 + tau] = tot;
 }
 
@@ -215,6 +221,9 @@ struct StageArgs {
     int seg[3], cnt[3];
 };
 
+#ifndef M2C_FILL_U
+#define M2C_FILL_U 4  // 16-B loads in flight per lane in k_fill (r02 sweep: 4 x 32 CTAs best)
+#endif
 struct FillArgs {
     const uint8_t *host[3];
     uint8_t *pool[3];
@@ -224,6 +233,7 @@ struct FillArgs {
     const int32_t *stage_of[3];
     const uint8_t *stage[3];
     unsigned long long *staged;  // count of misses filled from the staging buffers
+    const int32_t *skip;         // or null: entries with skip[seg + m] >= 0 are not copied
 };
 
 // a5: SM-driven gather of the missed records from the pinned host tier (UVA-mapped) into
@@ -240,6 +250,7 @@ __global__ void __launch_bounds__(256) k_fill(FillArgs a, const int32_t *__restr
     for (int w = gw; w < total; w += nwarps) {
         const int tau = w < c0 ? 0 : (w < c0 + c1 ? 1 : 2);
         const int m = w - (tau == 0 ? 0 : (tau == 1 ? c0 : c0 + c1));
+        if (a.skip && a.skip[a.seg[tau] + m] >= 0) continue;  // (requantised on the GPU)
         const int id = miss_ids[a.seg[tau] + m];
         const int sl = miss_items[a.seg[tau] + m];
         const int64_t nv = a.nb[tau] / 16;
@@ -248,15 +259,15 @@ __global__ void __launch_bounds__(256) k_fill(FillArgs a, const int32_t *__restr
         const uint4 *src = reinterpret_cast<const uint4 *>(
             si >= 0 ? a.stage[tau] + (int64_t)si * a.nb[tau] : a.host[tau] + (int64_t)id * a.nb[tau]);
         uint4 *dst = reinterpret_cast<uint4 *>(a.pool[tau] + (int64_t)sl * a.nb[tau]);
-        for (int64_t base = 0; base < nv; base += 32 * 8) {
-            uint4 v[8];
+        for (int64_t base = 0; base < nv; base += 32 * M2C_FILL_U) {
+            uint4 v[M2C_FILL_U];
 #pragma unroll
-            for (int j = 0; j < 8; j++) {
+            for (int j = 0; j < M2C_FILL_U; j++) {
                 const int64_t c = base + lane + 32 * j;
                 if (c < nv) v[j] = src[c];
             }
 #pragma unroll
-            for (int j = 0; j < 8; j++) {
+            for (int j = 0; j < M2C_FILL_U; j++) {
                 const int64_t c = base + lane + 32 * j;
                 if (c < nv) dst[c] = v[j];
             }
@@ -295,15 +306,15 @@ __global__ void __launch_bounds__(256) k_stage_fill(StageArgs a) {
         const int64_t nv = a.nb[tau] / 16;
         const uint4 *src = reinterpret_cast<const uint4 *>(a.host[tau] + (int64_t)id * a.nb[tau]);
         uint4 *dst = reinterpret_cast<uint4 *>(a.stage[tau] + (int64_t)(i - a.seg[tau]) * a.nb[tau]);
-        for (int64_t base = 0; base < nv; base += 32 * 8) {
-            uint4 v[8];
+        for (int64_t base = 0; base < nv; base += 32 * M2C_FILL_U) {
+            uint4 v[M2C_FILL_U];
 #pragma unroll
-            for (int j = 0; j < 8; j++) {
+            for (int j = 0; j < M2C_FILL_U; j++) {
                 const int64_t c = base + lane + 32 * j;
                 if (c < nv) v[j] = src[c];
             }
 #pragma unroll
-            for (int j = 0; j < 8; j++) {
+            for (int j = 0; j < M2C_FILL_U; j++) {
                 const int64_t c = base + lane + 32 * j;
                 if (c < nv) dst[c] = v[j];
             }
@@ -399,7 +410,7 @@ cudaError_t launch_stage_clear(m2c_ctx *c, const LayerState &Ln, int par, cudaSt
 }
 
 cudaError_t launch_missq(m2c_ctx *c, const LayerState &L, const int32_t *tier_ids,
-                         const m2c_tier_plan &p, cudaStream_t st) {
+                         const m2c_tier_plan &p, cudaStream_t st, int32_t *qsrc) {
     LruArgs a;
     const int cnt[3] = {p.k_fp16, p.k_int8, p.k_int4};
     const int seg[3] = {0, p.k_fp16, p.k_fp16 + p.k_int8};
@@ -408,7 +419,7 @@ cudaError_t launch_missq(m2c_ctx *c, const LayerState &L, const int32_t *tier_id
         a.seg[t] = seg[t];
         a.cnt[t] = cnt[t];
     }
-    cudaError_t e = launch_k(k_missq, dim3(3), dim3(NT), 0, st, a, tier_ids, c->mq);
+    cudaError_t e = launch_k(k_missq, dim3(3), dim3(NT), 0, st, a, tier_ids, c->mq, qsrc);
     c->launch_counter++;
     return e;
 }
@@ -417,7 +428,7 @@ cudaError_t launch_missq(m2c_ctx *c, const LayerState &L, const int32_t *tier_id
 // counts[8 + t] entries of each tier (k_fill without the lookahead)
 cudaError_t launch_copy_recs(m2c_ctx *c, const uint8_t *const src[3], uint8_t *const dst[3],
                              const m2c_tier_plan &p, const int32_t *counts, const int32_t *srci,
-                             const int32_t *dsti, cudaStream_t st) {
+                             const int32_t *dsti, cudaStream_t st, const int32_t *skip) {
     FillArgs a;
     const int seg[3] = {0, p.k_fp16, p.k_fp16 + p.k_int8};
     for (int t = 0; t < 3; t++) {
@@ -429,7 +440,8 @@ cudaError_t launch_copy_recs(m2c_ctx *c, const uint8_t *const src[3], uint8_t *c
         a.stage[t] = nullptr;
     }
     a.staged = c->ws.stats + 6;
-    static const int fill_ctas = getenv("M2C_FILL_CTAS") ? atoi(getenv("M2C_FILL_CTAS")) : 64;
+    a.skip = skip;
+    static const int fill_ctas = getenv("M2C_FILL_CTAS") ? atoi(getenv("M2C_FILL_CTAS")) : 32;
     cudaError_t e = launch_k(k_fill, dim3(fill_ctas), dim3(256), 0, st, a, counts, srci, dsti);
     c->launch_counter++;
     return e;
@@ -448,7 +460,8 @@ cudaError_t launch_fill(m2c_ctx *c, const LayerState &L, const m2c_tier_plan &p,
         a.stage[t] = stage_par >= 0 ? c->stage_buf[stage_par][t] : nullptr;
     }
     a.staged = c->ws.stats + 6;
-    static const int fill_ctas = getenv("M2C_FILL_CTAS") ? atoi(getenv("M2C_FILL_CTAS")) : 64;  // tuning knob
+    a.skip = nullptr;
+    static const int fill_ctas = getenv("M2C_FILL_CTAS") ? atoi(getenv("M2C_FILL_CTAS")) : 32;  // tuning knob
     cudaError_t e = launch_k(k_fill, dim3(fill_ctas), dim3(256), 0, st, a, c->ws.counts, c->ws.miss_ids,
                              c->ws.miss_items);
     c->launch_counter++;

@@ -12,6 +12,64 @@
 namespace m2c {
 namespace {
 
+// One 128-group gi of row w (matrix m) into an INT record: the warp's lanes hold 4 values
+// each; min/max by shuffles; codes, fp16 scale and u8 zero-point written at their places.
+template <int BITS>
+__device__ __forceinline__ void pack_group(const __half *w, int d, int m, int gi, uint8_t *rec, uint8_t *scales,
+                                           uint8_t *zeros) {
+    constexpr int maxq = (1 << BITS) - 1;
+    const int G = d / 128, lane = threadIdx.x & 31;
+    const uint2 raw = *reinterpret_cast<const uint2 *>(w + gi * 128 + lane * 4);
+    float v[4];
+    {
+        __half2 a = *reinterpret_cast<const __half2 *>(&raw.x);
+        __half2 b = *reinterpret_cast<const __half2 *>(&raw.y);
+        v[0] = __low2float(a);
+        v[1] = __high2float(a);
+        v[2] = __low2float(b);
+        v[3] = __high2float(b);
+    }
+    float lo = 0.f, hi = 0.f;  // range extended to include 0
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+        lo = fminf(lo, v[j]);
+        hi = fmaxf(hi, v[j]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    }
+    unsigned short s16;
+    if (lo == hi) {
+        s16 = 0x3c00;  // 1.0
+    } else {
+        const float s32 = __fdiv_rn(__fsub_rn(hi, lo), (float)maxq);
+        s16 = __half_as_ushort(__float2half_rn(s32));
+        if ((s16 & 0x7fff) == 0) s16 = 0x0001;  // underflow -> 2^-24
+    }
+    const float s = __half2float(__ushort_as_half(s16));
+    int z = __float2int_rn(__fdiv_rn(-lo, s));
+    z = min(max(z, 0), maxq);
+    int q[4];
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+        int qi = __float2int_rn(__fdiv_rn(v[j], s)) + z;
+        q[j] = min(max(qi, 0), maxq);
+    }
+    if (BITS == 8) {
+        uint32_t word = (uint32_t)q[0] | ((uint32_t)q[1] << 8) | ((uint32_t)q[2] << 16) | ((uint32_t)q[3] << 24);
+        *reinterpret_cast<uint32_t *>(rec + (int64_t)m * d + gi * 128 + lane * 4) = word;
+    } else {
+        uint16_t hw = (uint16_t)(q[0] | (q[1] << 4) | (q[2] << 8) | (q[3] << 12));
+        *reinterpret_cast<uint16_t *>(rec + (int64_t)m * (d / 2) + gi * 64 + lane * 2) = hw;
+    }
+    if (lane == 0) {
+        *reinterpret_cast<unsigned short *>(scales + 2 * (m * G + gi)) = s16;
+        zeros[m * G + gi] = (uint8_t)z;
+    }
+}
+
 // One warp per 128-group; blockIdx.y = matrix (0 gate, 1 up, 2 down), blockIdx.x = neuron.
 template <int BITS>
 __global__ void __launch_bounds__(128) k_pack_q(int d, const __half *__restrict__ g,
@@ -19,7 +77,6 @@ __global__ void __launch_bounds__(128) k_pack_q(int d, const __half *__restrict_
                                                 const __half *__restrict__ dn, int64_t n0,
                                                 int64_t nb, uint8_t *__restrict__ out) {
     griddep_wait();
-    constexpr int maxq = (1 << BITS) - 1;
     const int m = blockIdx.y;
     const int64_t n = n0 + blockIdx.x;
     const int G = d / 128;
@@ -28,61 +85,40 @@ __global__ void __launch_bounds__(128) k_pack_q(int d, const __half *__restrict_
     const int64_t data_bytes = (BITS == 8) ? 3LL * d : 3LL * d / 2;
     uint8_t *scales = rec + data_bytes;
     uint8_t *zeros = scales + 6 * G;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int gi = warp; gi < G; gi += blockDim.x / 32) {
-        const uint2 raw = *reinterpret_cast<const uint2 *>(w + gi * 128 + lane * 4);
-        float v[4];
-        {
-            __half2 a = *reinterpret_cast<const __half2 *>(&raw.x);
-            __half2 b = *reinterpret_cast<const __half2 *>(&raw.y);
-            v[0] = __low2float(a);
-            v[1] = __high2float(a);
-            v[2] = __low2float(b);
-            v[3] = __high2float(b);
-        }
-        float lo = 0.f, hi = 0.f;  // range extended to include 0
-#pragma unroll
-        for (int j = 0; j < 4; j++) {
-            lo = fminf(lo, v[j]);
-            hi = fmaxf(hi, v[j]);
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            lo = fminf(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-            hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-        }
-        unsigned short s16;
-        if (lo == hi) {
-            s16 = 0x3c00;  // 1.0
-        } else {
-            const float s32 = __fdiv_rn(__fsub_rn(hi, lo), (float)maxq);
-            s16 = __half_as_ushort(__float2half_rn(s32));
-            if ((s16 & 0x7fff) == 0) s16 = 0x0001;  // underflow -> 2^-24
-        }
-        const float s = __half2float(__ushort_as_half(s16));
-        int z = __float2int_rn(__fdiv_rn(-lo, s));
-        z = min(max(z, 0), maxq);
-        int q[4];
-#pragma unroll
-        for (int j = 0; j < 4; j++) {
-            int qi = __float2int_rn(__fdiv_rn(v[j], s)) + z;
-            q[j] = min(max(qi, 0), maxq);
-        }
-        if (BITS == 8) {
-            uint32_t word = (uint32_t)q[0] | ((uint32_t)q[1] << 8) | ((uint32_t)q[2] << 16) |
-                            ((uint32_t)q[3] << 24);
-            *reinterpret_cast<uint32_t *>(rec + (int64_t)m * d + gi * 128 + lane * 4) = word;
-        } else {
-            uint16_t hw = (uint16_t)(q[0] | (q[1] << 4) | (q[2] << 8) | (q[3] << 12));
-            *reinterpret_cast<uint16_t *>(rec + (int64_t)m * (d / 2) + gi * 64 + lane * 2) = hw;
-        }
-        if (lane == 0) {
-            *reinterpret_cast<unsigned short *>(scales + 2 * (m * G + gi)) = s16;
-            zeros[m * G + gi] = (uint8_t)z;
-        }
-    }
+    for (int gi = threadIdx.x >> 5; gi < G; gi += blockDim.x / 32) pack_group<BITS>(w, d, m, gi, rec, scales, zeros);
     if (m == 2 && threadIdx.x == 0) {  // zero the 16-B padding tail
         for (int64_t b = data_bytes + 9 * G; b < nb; b++) rec[b] = 0;
+    }
+}
+
+// Early-fill LRU engine: a miss of the INT8 / INT4 pool whose neuron sits in the layer's FP16
+// pool (tier churn: ranks move across the tier cuts between tokens) gets its record by
+// quantising that FP16 record on the GPU -- the same function as the offline pack (k_pack_q,
+// bit-identical to the oracle's O0) -- instead of a PCIe copy of the host tier's record.  The
+// record bytes, the cache state and the outputs are unchanged; only the source of the bytes
+// is.  blockIdx.x = miss-queue entry, blockIdx.y = matrix; entries with src_slot < 0 (or past
+// the queue's count) are the host copy's.
+template <int BITS>
+__global__ void __launch_bounds__(128) k_requant(int d, const uint8_t *__restrict__ pool16, int64_t nb16,
+                                                 const int32_t *__restrict__ q, int tau, int seg,
+                                                 const int32_t *__restrict__ src_slot, uint8_t *__restrict__ stage,
+                                                 int64_t nb, unsigned long long *__restrict__ stat) {
+    griddep_wait();
+    const int mi = blockIdx.x;
+    if (mi >= q[8 + tau]) return;
+    const int sl = src_slot[seg + mi];
+    if (sl < 0) return;
+    const int m = blockIdx.y;
+    const int G = d / 128;
+    const __half *w = reinterpret_cast<const __half *>(pool16 + (int64_t)sl * nb16) + (int64_t)m * d;
+    uint8_t *rec = stage + (int64_t)mi * nb;
+    const int64_t data_bytes = (BITS == 8) ? 3LL * d : 3LL * d / 2;
+    uint8_t *scales = rec + data_bytes;
+    uint8_t *zeros = scales + 6 * G;
+    for (int gi = threadIdx.x >> 5; gi < G; gi += blockDim.x / 32) pack_group<BITS>(w, d, m, gi, rec, scales, zeros);
+    if (m == 2 && threadIdx.x == 0) {
+        for (int64_t b = data_bytes + 9 * G; b < nb; b++) rec[b] = 0;
+        atomicAdd(stat, 1ull);
     }
 }
 
@@ -124,6 +160,28 @@ __global__ void __launch_bounds__(256) k_transpose_i8(int r, int d, const int8_t
 cudaError_t launch_transpose_i8(int r, int d, const int8_t *A, int8_t *At, cudaStream_t st) {
     k_transpose_i8<<<dim3((d + 31) / 32, (r + 31) / 32), 256, 0, st>>>(r, d, A, At);
     return cudaGetLastError();
+}
+
+// the requantised fills of one layer step (after k_missq; compute stream, before k_lru: the
+// FP16 pool's slots are read before this step's scatter can overwrite a victim)
+cudaError_t launch_requant(m2c_ctx *c, const LayerState &L, const m2c_tier_plan &p, cudaStream_t st) {
+    const int d = c->desc.d_model;
+    const int kt[3] = {p.k_fp16, p.k_int8, p.k_int4};
+    const int seg[3] = {0, p.k_fp16, p.k_fp16 + p.k_int8};
+    cudaError_t e = cudaSuccess;
+    for (int t = 1; t < 3 && e == cudaSuccess; t++) {
+        if (kt[t] <= 0) continue;
+        if (t == 1)
+            e = launch_k(k_requant<8>, dim3((unsigned)kt[t], 3), dim3(128), 0, st, d, (const uint8_t *)L.pool[0],
+                         c->nb[0], (const int32_t *)c->mq, 1, seg[1], (const int32_t *)c->mq_src, c->mstage[1],
+                         c->nb[1], c->ws.stats + 9);
+        else
+            e = launch_k(k_requant<4>, dim3((unsigned)kt[t], 3), dim3(128), 0, st, d, (const uint8_t *)L.pool[0],
+                         c->nb[0], (const int32_t *)c->mq, 2, seg[2], (const int32_t *)c->mq_src, c->mstage[2],
+                         c->nb[2], c->ws.stats + 10);
+        c->launch_counter++;
+    }
+    return e;
 }
 
 cudaError_t launch_pack(int d, int bits, const __half *g, const __half *u, const __half *dn,

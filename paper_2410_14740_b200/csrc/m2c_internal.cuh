@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -72,7 +73,8 @@ struct Workspace {
     float *partial = nullptr;      // [2][G][d]
     float *y32 = nullptr;          // [d]
     __half *xbuf = nullptr;        // [d]
-    unsigned long long *stats = nullptr;  // [8] hits[3], misses[3], staged fills, - (cumulative)
+    unsigned long long *stats = nullptr;  // [16] hits[3], misses[3], staged fills, -, requantised
+                                          // fills per tier [8..10] (cumulative)
     uint32_t *err = nullptr;       // device error flag word; err + 2 holds the host mirror's
                                    // device address (flag_error)
 };
@@ -145,6 +147,8 @@ struct m2c_ctx {
     // early fill (decode engine, LRU/ATU layers): miss queue, identity list, staging area
     int32_t *mq = nullptr;        // [16 + k]: q[8 + t] = misses of tier t; ids from q + 16
     int32_t *ident = nullptr;     // [k]: ident[seg_t + m] = m
+    int32_t *mq_src = nullptr;    // [k]: FP16-pool slot of an INT miss filled by requantisation, or -1
+    bool requant = true;          // early-fill engine: INT misses from resident FP16 records
     uint8_t *mstage[3] = {nullptr, nullptr, nullptr};  // [k_t][nb_t]
     void *early_mem = nullptr;
     bool early_fill = true;
@@ -202,10 +206,11 @@ cudaError_t launch_select_global(m2c_ctx *c, const long long *keys, int n, const
                                  int32_t *tier_ids, int32_t *counts, cudaStream_t st);
 int select_blocks(int F_r);
 cudaError_t launch_missq(m2c_ctx *c, const LayerState &L, const int32_t *tier_ids,
-                         const m2c_tier_plan &p, cudaStream_t st);
+                         const m2c_tier_plan &p, cudaStream_t st, int32_t *qsrc = nullptr);
+cudaError_t launch_requant(m2c_ctx *c, const LayerState &L, const m2c_tier_plan &p, cudaStream_t st);
 cudaError_t launch_copy_recs(m2c_ctx *c, const uint8_t *const src[3], uint8_t *const dst[3],
                              const m2c_tier_plan &p, const int32_t *counts, const int32_t *srci,
-                             const int32_t *dsti, cudaStream_t st);
+                             const int32_t *dsti, cudaStream_t st, const int32_t *skip = nullptr);
 cudaError_t launch_lru(m2c_ctx *c, LayerState &L, const int32_t *step_dev, const int32_t *tier_ids,
                        const m2c_tier_plan &p, int32_t *slots, uint32_t *hit_bits,
                        int32_t *miss_log, int32_t *evict_log, cudaStream_t st);
@@ -264,7 +269,8 @@ cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    static const bool pdl = !(getenv("M2C_PDL") && getenv("M2C_PDL")[0] == '0');  // (A/B knob)
+    cfg.numAttrs = pdl ? 1 : 0;
     return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 

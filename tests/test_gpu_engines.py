@@ -420,3 +420,38 @@ def test_p2p_ipc_two_processes_against_oracle(m2c):
                 assert np.frombuffer(res[r][t][2][l], np.int32).tolist() == ids.tolist(), (t, l, r)
                 ysum += yhat
             assert d10(ty[l], ysum) <= TOL, (t, l)
+
+
+def test_requant_fills_equal_host_fills(m2c):
+    """a5 fill source (include/m2c.h m2c_set_requant): an INT8 / INT4 miss whose neuron is resident
+    in the FP16 pool is filled by quantising that record on the GPU (the offline pack's function,
+    bit-identical to O0) instead of copying the host tier's record.  At full S13 width, 3 layers
+    x 24 tokens: the same token stream with the requantised fills on and off gives bit-identical
+    layer inputs / outputs and cache state, the same miss counts, and requantised fills > 0."""
+    cfg = get_config("S13")
+    plan = m2c.plan_of(cfg)
+    L, T = 3, 24
+    runs = []
+    for rq in (True, False):
+        ctx, ws, cc = _stack(m2c, cfg, plan, L, cc_mode="lru")
+        ctx.set_requant(rq)
+        ctx.set_trace(True)
+        xs = token_stream(cfg, T, device="cuda")
+        tr = []
+        for t in range(T):
+            x = xs[t].contiguous().clone()
+            ctx.decode_step(x, 5 + 3 * t)
+            torch.cuda.synchronize()
+            tr.append((ctx.trace_x.clone(), ctx.trace_y.clone()))
+        state = [[tuple(v.cpu() for v in ctx.cache_state(l, tau)) for tau in range(3)] for l in range(L)]
+        runs.append((tr, state, ctx.stats()["misses"], ctx.requant_stats()))
+        ctx.close()
+    (tr1, s1, m1, q1), (tr0, s0, m0, q0) = runs
+    assert q1[0] == 0 and q1[1] + q1[2] > 0, q1
+    assert q0 == [0, 0, 0]
+    assert m1 == m0
+    for (x1, y1), (x0, y0) in zip(tr1, tr0):
+        assert torch.equal(x1, x0) and torch.equal(y1, y0)
+    for l in range(L):
+        for tau in range(3):
+            assert all(torch.equal(a, b) for a, b in zip(s1[l][tau], s0[l][tau]))
