@@ -8,6 +8,9 @@
 //   5: atom.add.acq_rel arrive (returns old), last arriver st.release a flag word on another
 //      line, the rest poll the flag with ld.relaxed + fence after
 //   6: like 2, poller is lane 0 of every warp (no trailing __syncthreads)
+//   7: no atomics: every CTA st.release its own flag line; warp 0 polls all G flags (ld.relaxed,
+//      lanes over CTAs), one fence.acq_rel after
+//   8: arrival counters split 8 ways (cta % 8, own lines); thread 0 polls the 8 sums
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/mb_gridsync2 tools/mb_gridsync2.cu
 #include <cstdio>
 #include <cuda_runtime.h>
@@ -41,6 +44,35 @@ __global__ void k_bar(unsigned *buf, float *sink, int iters, int nstore, unsigne
                 asm volatile("fence.acq_rel.gpu;" ::: "memory");
             }
             __syncwarp();
+            continue;
+        }
+        if (MODE == 7) {
+            __syncthreads();
+            unsigned *fl = buf + 2048;  // flags, one per CTA, 64 B apart? (index * 16 u32)
+            if (threadIdx.x == 0)
+                asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(fl + 16 * blockIdx.x), "r"((unsigned)it) : "memory");
+            if (threadIdx.x < 32) {
+                for (int c = threadIdx.x; c < G; c += 32)
+                    while ((int)(ld_relaxed(fl + 16 * c) - (unsigned)it) < 0) {
+                    }
+                __syncwarp();
+                asm volatile("fence.acq_rel.gpu;" ::: "memory");
+            }
+            __syncthreads();
+            continue;
+        }
+        if (MODE == 8) {
+            __syncthreads();
+            if (threadIdx.x == 0)
+                asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(cnt + 32 * (blockIdx.x & 7)) : "memory");
+            if (threadIdx.x < 8) {
+                const unsigned want8 = (unsigned)(it * ((G - threadIdx.x + 7) / 8));
+                while ((int)(ld_relaxed(cnt + 32 * threadIdx.x) - want8) < 0) {
+                }
+                __syncwarp(0xffu);
+                asm volatile("fence.acq_rel.gpu;" ::: "memory");
+            }
+            __syncthreads();
             continue;
         }
         __syncthreads();
@@ -88,16 +120,16 @@ int main() {
     unsigned *buf;
     float *sink;
     unsigned long long *out, h;
-    cudaMalloc(&buf, 4 * 4096);
+    cudaMalloc(&buf, 4 * 8192);
     cudaMalloc(&sink, (size_t)sms * 8 * 1024 * 4);
     cudaMalloc(&out, 8);
     const int iters = 2000;
-    void *fns[7] = {nullptr, (void *)k_bar<1>, (void *)k_bar<2>, (void *)k_bar<3>,
-                    (void *)k_bar<4>, (void *)k_bar<5>, (void *)k_bar<6>};
+    void *fns[9] = {nullptr, (void *)k_bar<1>, (void *)k_bar<2>, (void *)k_bar<3>,
+                    (void *)k_bar<4>, (void *)k_bar<5>, (void *)k_bar<6>, (void *)k_bar<7>, (void *)k_bar<8>};
     for (int nstore : {0, 8})
-        for (int mode = 1; mode <= 6; mode++)
+        for (int mode = 1; mode <= 8; mode++)
             for (int nt : {512, 1024}) {
-                cudaMemset(buf, 0, 4 * 4096);
+                cudaMemset(buf, 0, 4 * 8192);
                 void *args[] = {&buf, &sink, (void *)&iters, (void *)&nstore, &out};
                 cudaEvent_t e0, e1;
                 cudaEventCreate(&e0);
