@@ -11,16 +11,19 @@
 //  * Work split: each CTA owns a contiguous share of the active records (tier order FP16,
 //    INT8, INT4), balanced on bytes + lambda * weights (an INT4 record has 1/4 of the bytes
 //    of an FP16 one but the same 3d weights to dequantise).
-//  * Two phases per share.  G: the gate/up dot products, in units (record j, part p of d,
-//    1024 elements) dealt round-robin to the compute warps, each ending in warp shuffles; the
-//    warp completing a record's last part combines the parts in a fixed order into
-//    a_j = act(g_j) u_j.  D: the down-projection, thread t owning y[8t, 8t+8) in registers,
-//    records in share order -- every element's sum has a fixed order (bit-reproducible).
+//  * Two phases per share.  G: the gate/up dot products, in units (record j, part p: 2 KB of
+//    each row's codes, i.e. 1024 FP16 / 2048 INT8 / 4096 INT4 elements, gu_unit) dealt
+//    round-robin to the compute warps, each ending in warp shuffles; the warp completing a
+//    record's last part combines the parts in a fixed order into a_j = act(g_j) u_j.  D: the
+//    down-projection, thread t owning y[8t, 8t+8) in registers, records in share order --
+//    every element's sum has a fixed order (bit-reproducible).
 //  * Data movement by the TMA engine (cp.async.bulk, SASS UBLKCP) into a 192 KB shared-memory
 //    ring with full / empty mbarriers per entry (whole mode: every record at once;
-//    streaming mode: a producer warp streams the gate/up parts, then the down parts, FIFO,
-//    re-using each entry as soon as its consumers arrive) -- see ffn_run.  (Measured
-//    alternatives: plain LDG streaming of gate/up and L2-prefetched down columns were slower,
+//    streaming mode: a producer warp streams the gate/up rows (+ tail) FIFO, re-using each
+//    entry as soon as its units arrive, and prefetches the down rows into L2 for phase D's
+//    loads) -- see ffn_run.  (Measured alternatives -- LDG streaming with and without software
+//    pipelining, speculative gate/up on the previous token's share, L2 prefetch of predicted
+//    records, the down rows by TMA into the freed ring, split G/D warp groups -- were slower:
 //    profiles/r02_ffn_variants.txt.)
 //  * Dequant in registers, ~2 instructions per weight: codes become the fp16 value 1024 + q
 //    (or 1024 + 16q for odd INT4 nibbles) by PRMT/LOP3 (magic-exponent trick); HSUB2 removes
@@ -36,7 +39,7 @@ namespace {
 
 constexpr int kRing = 192 * 1024;
 constexpr int kNS = 64;          // pipeline entries in flight (full / empty mbarrier pairs)
-constexpr int kPMax = 8;         // gate/up parts per record (d / 1024 for d <= 8192)
+constexpr int kPMax = 8;         // gate/up parts per record (<= 8 for d <= 8192, gu_parts)
 constexpr int kMaxLocal = 1024;  // records one CTA may own
 constexpr int kXsBytes = 16384;  // x (fp16, d <= 8192)
 // dynamic smem: ring | xs | loc[kMaxLocal] | a[kMaxLocal]
@@ -94,106 +97,123 @@ __device__ __forceinline__ uint32_t zz2_16(uint32_t z) {  // fp16x2 (1024 + 16 z
     return h | (h << 16);
 }
 
-// ---- one 8-element chunk c of the gate and up rows (in shared memory) into (ag, au) -------
-// rec: the record's gate data; so: byte offset of its scale/zero tail (3D in a whole record,
-// 2D in a streamed gate/up entry)
-template <int TIER>
-__device__ __forceinline__ void gu_one(const uint8_t *rec, int so, const uint4 *xs, int d, int c, float &ag,
-                                       float &au) {
-    const int G = d >> 7;
-    const uint4 xv = xs[c];
-    const uint32_t xw[4] = {xv.x, xv.y, xv.z, xv.w};
-    if (TIER == 0) {
-        const uint4 gv = *reinterpret_cast<const uint4 *>(rec + 16 * c);
-        const uint4 uv = *reinterpret_cast<const uint4 *>(rec + 2 * d + 16 * c);
-        const uint32_t gw[4] = {gv.x, gv.y, gv.z, gv.w}, uw[4] = {uv.x, uv.y, uv.z, uv.w};
-#pragma unroll
-        for (int i = 0; i < 4; i++) {
-            hfma32(ag, gw[i], xw[i], 0, 0);
-            hfma32(ag, gw[i], xw[i], 1, 1);
-            hfma32(au, uw[i], xw[i], 0, 0);
-            hfma32(au, uw[i], xw[i], 1, 1);
-        }
-    } else {
-        const uint8_t *scales = rec + so;
-        const uint8_t *zeros = scales + 6 * G;
-        const int grp = c >> 4;
-        const float sg = half_bits_f(*reinterpret_cast<const uint16_t *>(scales + 2 * grp));
-        const float su = half_bits_f(*reinterpret_cast<const uint16_t *>(scales + 2 * (G + grp)));
-        const uint32_t zg = zeros[grp], zu = zeros[G + grp];
-        float tg = 0.f, tu = 0.f;
-        if (TIER == 1) {
-            const uint2 gv = *reinterpret_cast<const uint2 *>(rec + 8 * c);
-            const uint2 uv = *reinterpret_cast<const uint2 *>(rec + d + 8 * c);
-            uint32_t pg_[4], pu_[4];
-            deq8(gv.x, gv.y, zz2(zg), pg_);
-            deq8(uv.x, uv.y, zz2(zu), pu_);
-#pragma unroll
-            for (int i = 0; i < 4; i++) {
-                hfma32(tg, pg_[i], xw[i], 0, 0);
-                hfma32(tg, pg_[i], xw[i], 1, 1);
-                hfma32(tu, pu_[i], xw[i], 0, 0);
-                hfma32(tu, pu_[i], xw[i], 1, 1);
-            }
-        } else {
-            const uint32_t gw = *reinterpret_cast<const uint32_t *>(rec + 4 * c);
-            const uint32_t uw = *reinterpret_cast<const uint32_t *>(rec + (d >> 1) + 4 * c);
-            uint32_t pg_[4], pu_[4];
-            deq4(gw, zz2(zg), zz2_16(zg), pg_);
-            deq4(uw, zz2(zu), zz2_16(zu), pu_);
-            // x pairs: (e0, e4) = (xw0.lo, xw2.lo), (e1, e5) = (xw0.hi, xw2.hi),
-            //          (e2, e6) = (xw1.lo, xw3.lo), (e3, e7) = (xw1.hi, xw3.hi)
-            float tg16 = 0.f, tu16 = 0.f;
-            hfma32(tg, pg_[0], xw[0], 0, 0);
-            hfma32(tg, pg_[0], xw[2], 1, 0);
-            hfma32(tg16, pg_[1], xw[0], 0, 1);
-            hfma32(tg16, pg_[1], xw[2], 1, 1);
-            hfma32(tg, pg_[2], xw[1], 0, 0);
-            hfma32(tg, pg_[2], xw[3], 1, 0);
-            hfma32(tg16, pg_[3], xw[1], 0, 1);
-            hfma32(tg16, pg_[3], xw[3], 1, 1);
-            hfma32(tu, pu_[0], xw[0], 0, 0);
-            hfma32(tu, pu_[0], xw[2], 1, 0);
-            hfma32(tu16, pu_[1], xw[0], 0, 1);
-            hfma32(tu16, pu_[1], xw[2], 1, 1);
-            hfma32(tu, pu_[2], xw[1], 0, 0);
-            hfma32(tu, pu_[2], xw[3], 1, 0);
-            hfma32(tu16, pu_[3], xw[1], 0, 1);
-            hfma32(tu16, pu_[3], xw[3], 1, 1);
-            tg = fmaf(tg16, 0.0625f, tg);
-            tu = fmaf(tu16, 0.0625f, tu);
-        }
-        ag = fmaf(sg, tg, ag);
-        au = fmaf(su, tu, au);
-    }
+// ---- gate/up units --------------------------------------------------------------------
+// A "chunk" is 16 B of one row's codes: 8 (FP16), 16 (INT8) or 32 (INT4) elements, inside one
+// 128-element quantisation group.  A unit (record, part p) covers chunks [128 p, 128 p + 128)
+// of the gate row and of the up row: lane L takes chunks 128 p + L + 32 u, u < 4 (LDS.128 of
+// consecutive 16 B across the lanes: conflict-free), one scale / zero-point per chunk and row,
+// x read from its natural fp16 copy (2 / 4 blocks of 16 B per INT8 / INT4 chunk; permuted
+// conflict-free copies of x measured slower: their 32 KB came out of the ring).  Round 1 used
+// 8-element chunks for every tier: 4 / 8-B code loads and a scale per 8 INT elements -- ~3.75
+// instructions per INT4 weight, the INT-heavy shares' P4 being issue-bound at S70H
+// (profiles/r02_ffn_variants.txt).
+__device__ __forceinline__ int row_bytes(int t, int d) { return t == 0 ? 2 * d : (t == 1 ? d : d / 2); }
+__device__ __forceinline__ int gu_parts(int t, int d) { return (row_bytes(t, d) / 16 + 127) >> 7; }
+__device__ __forceinline__ void fma16x2(float &acc, uint32_t a, uint32_t b) {  // acc += a.lo b.lo + a.hi b.hi
+    hfma32(acc, a, b, 0, 0);
+    hfma32(acc, a, b, 1, 1);
 }
-
-// warp-local partial dot products of one record over chunks [c0, c1) (8 elements each),
-// lane-interleaved (consecutive lanes read consecutive 16 B: no bank conflicts)
-template <int TIER>
-__device__ __forceinline__ void gu_chunks(const uint8_t *rec, int so, const uint4 *xs, int d, int c0, int c1,
-                                          float &pg, float &pu) {
+// INT4 word w (elements 0..7 in nibbles 0..7) against the x block xb (elements 0..7): deq4
+// pairs (e0,e4), 16(e1,e5), (e2,e6), 16(e3,e7) (exact fp16 q - z); the 16x terms go to t16
+__device__ __forceinline__ void int4_word(uint32_t w, uint32_t zz, uint32_t zz16, const uint4 &xb, float &t,
+                                          float &t16) {
+    uint32_t q[4];
+    deq4(w, zz, zz16, q);
+    hfma32(t, q[0], xb.x, 0, 0);
+    hfma32(t, q[0], xb.z, 1, 0);
+    hfma32(t16, q[1], xb.x, 0, 1);
+    hfma32(t16, q[1], xb.z, 1, 1);
+    hfma32(t, q[2], xb.y, 0, 0);
+    hfma32(t, q[2], xb.w, 1, 0);
+    hfma32(t16, q[3], xb.y, 0, 1);
+    hfma32(t16, q[3], xb.w, 1, 1);
+}
+// gr / ur: the record's gate / up row in shared memory (row_bytes each); tail: its scale /
+// zero tail (scales fp16[3G] | zeros u8[3G]).  (pg, pu): the part's dot products, warp-summed.
+template <int T>
+__device__ __forceinline__ void gu_unit(const uint8_t *gr, const uint8_t *ur, const uint8_t *tail, int d, int p,
+                                        const uint4 *x16, float &pg, float &pu) {
     const int lane = threadIdx.x & 31;
-    if (c1 - c0 == 128) {  // the 1024-element part: 4 chunks per lane, independent chains
-        float g0 = 0.f, u0 = 0.f, g1 = 0.f, u1 = 0.f, g2 = 0.f, u2 = 0.f, g3 = 0.f, u3 = 0.f;
-        gu_one<TIER>(rec, so, xs, d, c0 + lane, g0, u0);
-        gu_one<TIER>(rec, so, xs, d, c0 + lane + 32, g1, u1);
-        gu_one<TIER>(rec, so, xs, d, c0 + lane + 64, g2, u2);
-        gu_one<TIER>(rec, so, xs, d, c0 + lane + 96, g3, u3);
-        pg = (g0 + g1) + (g2 + g3);
-        pu = (u0 + u1) + (u2 + u3);
-        return;
+    const int nch = row_bytes(T, d) >> 4, G = d >> 7;
+    const int c0 = p << 7;
+    float ag[4], au[4];
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+        const int c = c0 + lane + 32 * u;
+        const bool in = c < nch;
+        const int cc = in ? c : 0;
+        const uint4 gv = *reinterpret_cast<const uint4 *>(gr + 16 * cc);
+        const uint4 uv = *reinterpret_cast<const uint4 *>(ur + 16 * cc);
+        if (T == 0) {
+            const uint4 xv = x16[cc];
+            float g = 0.f, v = 0.f;
+            fma16x2(g, gv.x, xv.x);
+            fma16x2(g, gv.y, xv.y);
+            fma16x2(g, gv.z, xv.z);
+            fma16x2(g, gv.w, xv.w);
+            fma16x2(v, uv.x, xv.x);
+            fma16x2(v, uv.y, xv.y);
+            fma16x2(v, uv.z, xv.z);
+            fma16x2(v, uv.w, xv.w);
+            ag[u] = in ? g : 0.f;
+            au[u] = in ? v : 0.f;
+        } else {
+            const int grp = T == 1 ? cc >> 3 : cc >> 2;
+            const uint16_t *s16 = reinterpret_cast<const uint16_t *>(tail);
+            const uint8_t *z8 = tail + 6 * G;
+            const float sg = half_bits_f(s16[grp]), su = half_bits_f(s16[G + grp]);
+            const uint32_t zg = z8[grp], zu = z8[G + grp];
+            float tg = 0.f, tu = 0.f;
+            if (T == 1) {
+                const uint4 xa = x16[2 * cc], xc = x16[2 * cc + 1];
+                uint32_t qg[4], qu[4];
+                const uint32_t zzg = zz2(zg), zzu = zz2(zu);
+                deq8(gv.x, gv.y, zzg, qg);
+                deq8(uv.x, uv.y, zzu, qu);
+                fma16x2(tg, qg[0], xa.x);
+                fma16x2(tg, qg[1], xa.y);
+                fma16x2(tg, qg[2], xa.z);
+                fma16x2(tg, qg[3], xa.w);
+                fma16x2(tu, qu[0], xa.x);
+                fma16x2(tu, qu[1], xa.y);
+                fma16x2(tu, qu[2], xa.z);
+                fma16x2(tu, qu[3], xa.w);
+                deq8(gv.z, gv.w, zzg, qg);
+                deq8(uv.z, uv.w, zzu, qu);
+                fma16x2(tg, qg[0], xc.x);
+                fma16x2(tg, qg[1], xc.y);
+                fma16x2(tg, qg[2], xc.z);
+                fma16x2(tg, qg[3], xc.w);
+                fma16x2(tu, qu[0], xc.x);
+                fma16x2(tu, qu[1], xc.y);
+                fma16x2(tu, qu[2], xc.z);
+                fma16x2(tu, qu[3], xc.w);
+            } else {
+                const uint4 *xb = x16 + 4 * cc;
+                const uint32_t zzg = zz2(zg), zzg16 = zz2_16(zg), zzu = zz2(zu), zzu16 = zz2_16(zu);
+                float tg16 = 0.f, tu16 = 0.f;
+                const uint32_t gw[4] = {gv.x, gv.y, gv.z, gv.w}, uw[4] = {uv.x, uv.y, uv.z, uv.w};
+#pragma unroll
+                for (int k = 0; k < 4; k++) {
+                    const uint4 xk = xb[k];
+                    int4_word(gw[k], zzg, zzg16, xk, tg, tg16);
+                    int4_word(uw[k], zzu, zzu16, xk, tu, tu16);
+                }
+                tg = fmaf(tg16, 0.0625f, tg);
+                tu = fmaf(tu16, 0.0625f, tu);
+            }
+            ag[u] = in ? sg * tg : 0.f;
+            au[u] = in ? su * tu : 0.f;
+        }
     }
-    float ag = 0.f, au = 0.f;
-    for (int c = c0 + lane; c < c1; c += 32) gu_one<TIER>(rec, so, xs, d, c, ag, au);
-    pg = ag;
-    pu = au;
+    pg = warp_sum_f((ag[0] + ag[1]) + (ag[2] + ag[3]));
+    pu = warp_sum_f((au[0] + au[1]) + (au[2] + au[3]));
 }
-__device__ __forceinline__ void gu_any(int tier, const uint8_t *rec, int so, const uint4 *xs, int d, int c0,
-                                       int c1, float &pg, float &pu) {
-    if (tier == 0) gu_chunks<0>(rec, so, xs, d, c0, c1, pg, pu);
-    else if (tier == 1) gu_chunks<1>(rec, so, xs, d, c0, c1, pg, pu);
-    else gu_chunks<2>(rec, so, xs, d, c0, c1, pg, pu);
+__device__ __forceinline__ void gu_unit_any(int t, const uint8_t *gr, const uint8_t *ur, const uint8_t *tail, int d,
+                                            int p, const uint4 *x16, float &pg, float &pu) {
+    if (t == 0) gu_unit<0>(gr, ur, tail, d, p, x16, pg, pu);
+    else if (t == 1) gu_unit<1>(gr, ur, tail, d, p, x16, pg, pu);
+    else gu_unit<2>(gr, ur, tail, d, p, x16, pg, pu);
 }
 
 // ---- y[8t .. 8t+8) += a * deq(down column) from shared memory --------------------------
@@ -360,41 +380,28 @@ __device__ __forceinline__ void cta_ranges(const FfnArgs &a, int n0, int n1, int
 struct FfnShared {
     uint64_t full[kNS];
     uint64_t emptyG[kNS];
-    uint64_t emptyD[kNS];
     int roff[kNS];          // ring offset of the entry (published before its expect_tx)
     int span[kNS];          // ring bytes the entry holds (incl. wrap waste)
     int pcnt[kNS];          // gate/up parts of a record done (record j -> slot j % kNS)
     float gpart[kNS][kPMax][2];
-    int cb[kPMax + 1];      // chunk bounds of the parts of this d
-    int P;                  // gate/up parts per record
     int rng[8];             // CTA ranges (6)
 };
 struct FfnPipe {            // per-CTA counters (registers of the calling kernel, across layers)
     unsigned nf = 0, ng = 0, nd = 0;
 };
 
-__device__ __forceinline__ int ffn_parts(int d) {
-    const int P = d / 1024;
-    return P < 1 ? 1 : (P > kPMax ? kPMax : P);
-}
-
 // thread 0, before any use
 __device__ __forceinline__ void ffn_init(FfnShared &sm, int d) {
-    const int P = ffn_parts(d), NW = blockDim.x >> 5;
     for (int i = 0; i < kNS; i++) {
         mbar_init(&sm.full[i], 1);
-        mbar_init(&sm.emptyG[i], (uint32_t)P);
-        mbar_init(&sm.emptyD[i], (uint32_t)NW);
+        mbar_init(&sm.emptyG[i], (uint32_t)kPMax);  // (a record's units arrive kPMax in total)
         sm.pcnt[i] = 0;
     }
-    const int nchunk = d / 8;
-    for (int p = 0; p <= P; p++) sm.cb[p] = nchunk * p / P;
-    sm.P = P;
     fence_mbar_init();
 }
 
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
-    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar, uint32_t count = 1) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
 
 // The FFN over this CTA's n_items records (item j: tier 0 for j < c1, 1 for j < c2, else 2;
@@ -417,7 +424,6 @@ __device__ __forceinline__ void ffn_run(const FfnArgs &a, int d, int act, int n_
                                         unsigned long long *stamps = nullptr) {
     const int NW = blockDim.x >> 5;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int P = sm.P;
     auto tier_of = [&](int j) { return j < c1 ? 0 : (j < c2 ? 1 : 2); };
     auto Dof = [&](int t) { return t == 0 ? 2 * d : (t == 1 ? d : d / 2); };
     const int total = c1 * a.nb[0] + (c2 - c1) * a.nb[1] + (n_items - c2) * a.nb[2];
@@ -485,32 +491,35 @@ __device__ __forceinline__ void ffn_run(const FfnArgs &a, int d, int act, int n_
         }
     }
     if (stamps && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(stamps[0]));
-    // ---- phase G: gate/up units (record j, part p), round-robin over the compute warps ----
+    // ---- phase G: gate/up units (record j, part q), round-robin over the compute warps ----
     const int NWc = whole ? NW : NW - 1;
     if (warp < NWc) {
-        for (int u = warp; u < n_items * P; u += NWc) {
-            const int j = u / P, p = u - j * P;
+        const int P0 = gu_parts(0, d), P1 = gu_parts(1, d), P2 = gu_parts(2, d);
+        const int U0 = c1 * P0, U1 = U0 + (c2 - c1) * P1, U = U1 + (n_items - c2) * P2;
+        for (int u = warp; u < U; u += NWc) {
+            int j, q, t, Pt;
+            if (u < U0) { j = u / P0; q = u - j * P0; t = 0; Pt = P0; }
+            else if (u < U1) { j = c1 + (u - U0) / P1; q = (u - U0) - (j - c1) * P1; t = 1; Pt = P1; }
+            else { j = c2 + (u - U1) / P2; q = (u - U1) - (j - c2) * P2; t = 2; Pt = P2; }
             const unsigned s = fslot(j);
             mbar_wait(&sm.full[s], fpar(j));
-            const int t = tier_of(j);
             const int D = Dof(t);
+            const uint8_t *rec = ring + sm.roff[s];
             float pg, pu;
-            gu_any(t, ring + sm.roff[s], whole ? 3 * D : 2 * D, xs, d, sm.cb[p], sm.cb[p + 1], pg, pu);
-            pg = warp_sum_f(pg);
-            pu = warp_sum_f(pu);
+            gu_unit_any(t, rec, rec + D, rec + (whole ? 3 * D : 2 * D), d, q, xs, pg, pu);
             if (lane == 0) {
-                if (P == 1) {
+                if (Pt == 1) {
                     a_sm[j] = (act == 1) ? fmaxf(pg, 0.f) * pu : pg / (1.f + expf(-pg)) * pu;
                 } else {
-                    sm.gpart[s][p][0] = pg;
-                    sm.gpart[s][p][1] = pu;
+                    sm.gpart[s][q][0] = pg;
+                    sm.gpart[s][q][1] = pu;
                     __threadfence_block();
-                    if (atomicAdd(&sm.pcnt[s], 1) == P - 1) {  // last part: combine in order
+                    if (atomicAdd(&sm.pcnt[s], 1) == Pt - 1) {  // last part: combine in order
                         __threadfence_block();
                         float g = 0.f, uu = 0.f;
-                        for (int q = 0; q < P; q++) {
-                            g += sm.gpart[s][q][0];
-                            uu += sm.gpart[s][q][1];
+                        for (int k = 0; k < Pt; k++) {
+                            g += sm.gpart[s][k][0];
+                            uu += sm.gpart[s][k][1];
                         }
                         sm.pcnt[s] = 0;
                         a_sm[j] = (act == 1) ? fmaxf(g, 0.f) * uu : g / (1.f + expf(-g)) * uu;
@@ -518,7 +527,10 @@ __device__ __forceinline__ void ffn_run(const FfnArgs &a, int d, int act, int n_
                 }
             }
             __syncwarp();
-            if (!whole && lane == 0) mbar_arrive(&sm.emptyG[(ng0 + j) % kNS]);
+            if (!whole && lane == 0) {  // the record's Pt units arrive kPMax in total
+                const uint32_t share = kPMax / Pt;
+                mbar_arrive(&sm.emptyG[(ng0 + j) % kNS], q < Pt - 1 ? share : kPMax - (Pt - 1) * share);
+            }
         }
     }
     __syncthreads();  // every a_j is in a_sm (and the producer is done)
@@ -571,12 +583,9 @@ __device__ __forceinline__ SmemPtrs carve(uint8_t *smem) {
 // per-CTA tail (the down-projection) costs per record, not per byte, so the split is close to
 // per-record: lambda 6 / 16 / 48 B per weight measured 584 / 595 / 596 tokens/s at S70H
 // (1456 tokens/s at S7 for all three).
-constexpr int kLambda = 16, kLambdaQ = 18;  // FP16 / INT8 + INT4 records (same-box A/B,
-                                           // profiles/r02_ffn_variants.txt: INT lambda 16/18/20/24)
-static inline int ffn_weight(int64_t nb, int d) {
-    const int64_t lam = nb >= 6 * (int64_t)d ? kLambda : kLambdaQ;  // FP16 records are 6d bytes
-    return (int)((nb + lam * 3 * d) / 16);
-}
+constexpr int kLambda = 16;  // (16-B gate/up units: INT lambda 14 / 16 / 18 and FP16 20 A/B'd,
+                             // profiles/r02_ffn_variants.txt)
+static inline int ffn_weight(int64_t nb, int d) { return (int)((nb + (int64_t)kLambda * 3 * d) / 16); }
 static inline void fill_args(m2c_ctx *c, const LayerState &L, const m2c_tier_plan &p, FfnArgs &a) {
     const int d = c->desc.d_model;
     const int seg[3] = {0, p.k_fp16, p.k_fp16 + p.k_int8};
