@@ -69,15 +69,14 @@ def main(rnd, cfg):
         lines.append(src)
         with open(os.path.join(pdir, f"{rnd}_ncu_k_decode_{cfg}.txt"), "w") as f:
             f.write("\n".join(lines) + "\n")
-        # dram traffic per launch for bench.py's roofline.traffic (units as ncu reports them)
-        units = rows[1] if len(rows) > 2 else None
-        scale = 1.0
-        if units:
-            u = dict(zip(hdr, units)).get("dram__bytes_read.sum", "byte")
-            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
+        # dram traffic per launch for bench.py's roofline.traffic (each metric in its own unit)
+        units = dict(zip(hdr, rows[1])) if len(rows) > 2 else {}
+        scale_of = lambda k: {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(units.get(k, "byte"), 1)
+        rd *= scale_of("dram__bytes_read.sum")
+        wr *= scale_of("dram__bytes_write.sum")
         tpath = os.path.join(pdir, "traffic.json")
         t = json.load(open(tpath)) if os.path.exists(tpath) else {}
-        t[cfg] = {"bytes_per_launch": (rd + wr) * scale, "kernel": "k_decode", "round": rnd,
+        t[cfg] = {"bytes_per_launch": rd + wr, "kernel": "k_decode", "round": rnd,
                   "source": f"profiles/{rnd}_ncu_k_decode_{cfg}.txt"}
         json.dump(t, open(tpath, "w"), indent=1)
     for name in (f"timeline_{cfg}.log", f"bench_{cfg}.log"):
