@@ -272,11 +272,11 @@ m2c_status m2c_profile_read(m2c_ctx *ctx, float *ms, int32_t *ffn_launches_out);
 m2c_status m2c_profile_fill(m2c_ctx *ctx, float *ms_per_layer);
 m2c_status m2c_profile_stamps(m2c_ctx *ctx, uint64_t *out, int64_t cap, int64_t *n_out);
 /* m2c_profile_events: the last decode step's per-layer CUDA-event timeline (kernel-chain
- * engines: resident chain, LRU/ATU), ms since layer 0's first mark, [n_layers][9]: compute
+ * engines: resident chain, LRU/ATU), ms since layer 0's first mark, [n_layers][11]: compute
  * stream 0 layer start, 1 predictor done, 2 select done, 3 FFN done, 4 reduce done; copy stream
  * 5 miss fill start, 6 miss fill end; compute stream (early-fill LRU engine) 7 LRU update done,
- * 8 hit FFN done (-1: not recorded).  The copy-versus-compute overlap of the LRU engine (P:11,
- * P:396) is read from it.  *n_out = n_layers * 9 (out may be null);
+ * 8 hit FFN done, 9 miss queue done, 10 requantisation done (-1: not recorded).  The copy-versus-compute overlap of the LRU engine (P:11,
+ * P:396) is read from it.  *n_out = n_layers * 11 (out may be null);
  * M2C_ERR_STATE if profiling is off or the last step was one k_decode launch. */
 m2c_status m2c_profile_events(m2c_ctx *ctx, float *out, int64_t cap, int64_t *n_out);
 

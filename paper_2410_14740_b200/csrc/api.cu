@@ -167,7 +167,8 @@ static int32_t *step_ptr(m2c_ctx *c) { return c->ws.counts + 15; }
 // ---- the token: all layers on the compute stream (+ copy stream for LRU fills) ----
 // profiling events per layer: 5 compute-stream marks (phase boundaries) + 2 around the miss
 // fill on the copy stream
-constexpr int kProfEv = 9;  // (+ 7 after the LRU update, 8 after the hit FFN: early-fill engine)
+constexpr int kProfEv = 11;  // (early-fill engine: + 7 after the LRU update, 8 after the hit FFN,
+                             // 9 after the miss queue, 10 after the requantisation)
 static cudaError_t mark_copy(m2c_ctx *c, int l, int i) {
     if (c->prof_ev.empty()) return cudaSuccess;
     return cudaEventRecordWithFlags(c->prof_ev[kProfEv * l + 5 + i], c->copy, cudaEventRecordExternal);
@@ -213,7 +214,7 @@ static cudaError_t early_fill_alloc(m2c_ctx *c) {
     const m2c_tier_plan &p = c->plan;
     const int k = p.k > 0 ? p.k : 1;
     const int kt[3] = {p.k_fp16, p.k_int8, p.k_int4};
-    size_t off = a256(4 * (16 + (size_t)k)) + 2 * a256(4 * (size_t)k), st_off[3];
+    size_t off = a256(4 * (16 + (size_t)k)) + 3 * a256(4 * (size_t)k), st_off[3];
     for (int t = 0; t < 3; t++) {
         st_off[t] = off;
         off += a256((size_t)(kt[t] > 0 ? kt[t] : 1) * c->nb[t]);
@@ -224,6 +225,7 @@ static cudaError_t early_fill_alloc(m2c_ctx *c) {
     c->mq = reinterpret_cast<int32_t *>(b);
     c->ident = reinterpret_cast<int32_t *>(b + a256(4 * (16 + (size_t)k)));
     c->mq_src = reinterpret_cast<int32_t *>(b + a256(4 * (16 + (size_t)k)) + a256(4 * (size_t)k));
+    c->mq_job = reinterpret_cast<int32_t *>(b + a256(4 * (16 + (size_t)k)) + 2 * a256(4 * (size_t)k));
     for (int t = 0; t < 3; t++) c->mstage[t] = b + st_off[t];
     std::vector<int32_t> id(k, 0);
     for (int t = 0, seg = 0; t < 3; seg += kt[t], t++)
@@ -316,6 +318,7 @@ static cudaError_t enqueue_layer(m2c_ctx *c, int l, __half *x) {
         // that record on the GPU (k_requant, the offline pack's function) instead of over PCIe
         const bool rq = requant_on(c);
         if ((e = launch_missq(c, L, ids, p, st, rq ? c->mq_src : nullptr))) return e;
+        if ((e = mark(c, l, 9))) return e;
         if ((e = cudaEventRecord(c->ev_q, st))) return e;
         if ((e = cudaStreamWaitEvent(c->copy, c->ev_q, 0))) return e;
         if ((e = mark_copy(c, l, 0))) return e;
@@ -324,6 +327,7 @@ static cudaError_t enqueue_layer(m2c_ctx *c, int l, __half *x) {
                                   rq ? c->mq_src : nullptr)))
             return e;
         if (rq && (e = launch_requant(c, L, p, st))) return e;
+        if ((e = mark(c, l, 10))) return e;
         if ((e = mark_copy(c, l, 1))) return e;
         if ((e = cudaEventRecord(c->ev_fill, c->copy))) return e;
         // the previous layer's scatter (copy stream) reads ws.counts[8..10] and ws.miss_items,
@@ -1229,7 +1233,7 @@ m2c_status m2c_profile_events(m2c_ctx *c, float *ms, int64_t cap, int64_t *n_out
     for (int l = 0; l < c->desc.n_layers; l++)
         for (int i = 0; i < kProfEv; i++) {
             float v = -1.f;  // (a mark the layer's engine did not record)
-            if (i < 5 || (c->layers[l].mode != 0 && (i < 7 || early_fill_on(c))))
+            if (i < 5 || (c->layers[l].mode != 0 && (i < 7 || early_fill_on(c))))  // (10: requant on)
                 if (cudaEventElapsedTime(&v, c->prof_ev[0], c->prof_ev[kProfEv * l + i]) != cudaSuccess) v = -1.f;
             ms[kProfEv * l + i] = v;
         }

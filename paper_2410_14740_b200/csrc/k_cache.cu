@@ -68,11 +68,18 @@ __global__ void __launch_bounds__(NT, 1)
           int32_t *__restrict__ miss_log, int32_t *__restrict__ evict_log,
           int32_t *__restrict__ counts, unsigned long long *__restrict__ stats, int P2) {
     extern __shared__ __align__(16) uint8_t smraw[];
-    // smem: new order [C] | victims [C] | miss positions [cnt] | slot bitmaps hit, tail [C/32]
+    // smem: new order [C] | victims [C] | miss positions [cnt] | the LRU order [C] | the tier's
+    // ids [cnt] | their slots [cnt] | slot bitmaps hit, tail [C/32].  Every global array is read
+    // once, coalesced, into shared memory up front: three dependent round trips in all (the
+    // list + order, the list's slots, the victims' occupants), whatever the L2 latency while
+    // the concurrent miss fill loads the memory system (round 2: ~10 before)
     int32_t *nord = reinterpret_cast<int32_t *>(smraw);
     int32_t *vict = nord + P2;
     int32_t *mpos = vict + P2;
-    uint32_t *hmask = reinterpret_cast<uint32_t *>(mpos + P2);
+    int32_t *sord = mpos + P2;
+    int32_t *sR = sord + P2;
+    int32_t *ssl = sR + P2;
+    uint32_t *hmask = reinterpret_cast<uint32_t *>(ssl + P2);
     uint32_t *tmask = hmask + P2 / 32;
     __shared__ int scan_sm[NW];
     const int tau = blockIdx.x;
@@ -82,6 +89,10 @@ __global__ void __launch_bounds__(NT, 1)
     const int t = *step_ptr;
     int32_t *occ = a.occ[tau], *last = a.last[tau], *slot_of = a.slot_of[tau], *ord = a.ord[tau];
     const int32_t *R = tier_ids + seg;
+    for (int i = threadIdx.x; i < n; i += NT) sR[i] = R[i];
+    for (int q = threadIdx.x; q < C; q += NT) sord[q] = ord[q];
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += NT) ssl[i] = slot_of[sR[i]];
     __syncthreads();
 
     // 1. hits: refresh their timestamp (a hit never moves slot)
@@ -89,7 +100,7 @@ __global__ void __launch_bounds__(NT, 1)
     const int i0 = min(n, (int)threadIdx.x * CH), i1 = min(n, i0 + CH);
     int nh = 0;
     for (int i = i0; i < i1; i++) {
-        const int sl = slot_of[R[i]];
+        const int sl = ssl[i];
         if (sl >= 0) {
             last[sl] = t;
             slots[seg + i] = sl;
@@ -102,7 +113,7 @@ __global__ void __launch_bounds__(NT, 1)
     int hpos = block_scan1(nh, &tot_h, scan_sm);  // (a barrier: hmask complete)
     int mp = i0 - hpos;  // misses before this chunk = i0 - hits before it
     for (int i = i0; i < i1; i++) {
-        const int sl = slot_of[R[i]];
+        const int sl = ssl[i];
         if (sl >= 0) hit_items[seg + hpos++] = sl;
         else mpos[mp++] = i;
     }
@@ -112,13 +123,13 @@ __global__ void __launch_bounds__(NT, 1)
     const int o0 = min(C, (int)threadIdx.x * OC), o1 = min(C, o0 + OC);
     int nk = 0;
     for (int q = o0; q < o1; q++) {
-        const int sl = ord[q];
+        const int sl = sord[q];
         nk += !((hmask[sl >> 5] >> (sl & 31)) & 1u);
     }
     int tot_k;
     int kpos = block_scan1(nk, &tot_k, scan_sm);  // non-hit rank of this thread's first entry
     for (int q = o0; q < o1; q++) {
-        const int sl = ord[q];
+        const int sl = sord[q];
         if ((hmask[sl >> 5] >> (sl & 31)) & 1u) continue;
         if (kpos < nm) {
             vict[kpos] = sl;
@@ -144,14 +155,18 @@ __global__ void __launch_bounds__(NT, 1)
     const int MC = (nm + NT - 1) / NT;
     const int m0 = min(nm, (int)threadIdx.x * MC), m1 = min(nm, m0 + MC);
     int ne = 0;
-    for (int m = m0; m < m1; m++) ne += occ[vict[m]] >= 0;
+    for (int m = m0; m < m1; m++) {
+        const int o = occ[vict[m]];
+        sord[m] = o;  // (the order was written out: its smem copy holds the victims' occupants)
+        ne += o >= 0;
+    }
     int tot_e;
     int epos = block_scan1(ne, &tot_e, scan_sm);
     for (int m = m0; m < m1; m++) {
         const int i = mpos[m];
-        const int id = R[i];
+        const int id = sR[i];
         const int sl = vict[m];
-        const int old = occ[sl];
+        const int old = sord[m];
         if (old >= 0) {
             slot_of[old] = -1;
             if (evict_log) {
@@ -187,7 +202,7 @@ __global__ void __launch_bounds__(NT, 1)
 // records are scattered into their victim slots afterwards (copy stream).
 __global__ void __launch_bounds__(NT, 1)
     k_missq(LruArgs a, const int32_t *__restrict__ tier_ids, int32_t *__restrict__ q,
-            int32_t *__restrict__ qsrc) {
+            int32_t *__restrict__ qsrc, int32_t *__restrict__ qjob) {
     // q: [16] header (q[8 + t] = misses of tier t) | ids [k] (segments as tier_ids);
     // qsrc (or null): per entry the neuron's FP16-pool slot for an INT8 / INT4 miss whose FP16
     // record is resident (filled by requantisation, k_requant), else -1
@@ -203,11 +218,22 @@ __global__ void __launch_bounds__(NT, 1)
     for (int i = i0; i < i1; i++) nm += slot_of[R[i]] < 0;
     int tot;
     int pos = block_scan1(nm, &tot, scan_sm);
+    int nj = 0;  // requantisation jobs of this thread (INT misses resident in the FP16 pool)
+    const int pos0 = pos;
     for (int i = i0; i < i1; i++)
         if (slot_of[R[i]] < 0) {
-            if (qsrc) qsrc[seg + pos] = tau > 0 ? a.slot_of[0][R[i]] : -1;
+            const int s16 = (qsrc && tau > 0) ? a.slot_of[0][R[i]] : -1;
+            if (qsrc) qsrc[seg + pos] = s16;
+            nj += s16 >= 0;
             q[16 + seg + pos++] = R[i];
         }
+    if (qsrc) {  // the jobs' entry indices, compacted in entry order: qjob[seg + j], count q[12 + tau]
+        int totj;
+        int jpos = block_scan1(nj, &totj, scan_sm);
+        for (int m = pos0; m < pos; m++)
+            if (qsrc[seg + m] >= 0) qjob[seg + jpos++] = m;
+        if (threadIdx.x == 0) q[12 + tau] = totj;
+    }
     if (threadIdx.x == 0) q[8 + tau] = tot;
 }
 
@@ -335,7 +361,7 @@ __global__ void __launch_bounds__(256) k_stage_clear(StageArgs a) {
 
 }  // namespace
 
-size_t lru_smem_bytes(int P2, int maxcnt) { (void)maxcnt; return 12 * (size_t)P2 + 8 * (size_t)(P2 / 32); }
+size_t lru_smem_bytes(int P2, int maxcnt) { (void)maxcnt; return 24 * (size_t)P2 + 8 * (size_t)(P2 / 32); }
 
 cudaError_t init_cache_attrs() {
     return cudaFuncSetAttribute(k_lru, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -419,7 +445,8 @@ cudaError_t launch_missq(m2c_ctx *c, const LayerState &L, const int32_t *tier_id
         a.seg[t] = seg[t];
         a.cnt[t] = cnt[t];
     }
-    cudaError_t e = launch_k(k_missq, dim3(3), dim3(NT), 0, st, a, tier_ids, c->mq, qsrc);
+    cudaError_t e = launch_k(k_missq, dim3(3), dim3(NT), 0, st, a, tier_ids, c->mq, qsrc,
+                             qsrc ? c->mq_job : nullptr);
     c->launch_counter++;
     return e;
 }

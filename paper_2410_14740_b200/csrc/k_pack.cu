@@ -93,32 +93,47 @@ __global__ void __launch_bounds__(128) k_pack_q(int d, const __half *__restrict_
 
 // Early-fill LRU engine: a miss of the INT8 / INT4 pool whose neuron sits in the layer's FP16
 // pool (tier churn: ranks move across the tier cuts between tokens) gets its record by
-// quantising that FP16 record on the GPU -- the same function as the offline pack (k_pack_q,
+// quantising that FP16 record on the GPU -- the same function as the offline pack (pack_group,
 // bit-identical to the oracle's O0) -- instead of a PCIe copy of the host tier's record.  The
 // record bytes, the cache state and the outputs are unchanged; only the source of the bytes
-// is.  blockIdx.x = miss-queue entry, blockIdx.y = matrix; entries with src_slot < 0 (or past
-// the queue's count) are the host copy's.
-template <int BITS>
-__global__ void __launch_bounds__(128) k_requant(int d, const uint8_t *__restrict__ pool16, int64_t nb16,
-                                                 const int32_t *__restrict__ q, int tau, int seg,
-                                                 const int32_t *__restrict__ src_slot, uint8_t *__restrict__ stage,
-                                                 int64_t nb, unsigned long long *__restrict__ stat) {
+// is.  One launch for both tiers over the jobs k_missq compacted (INT8, then INT4): a block
+// per job in turn, its warps over the record's 3G groups.  (Round 2, first versions: a block
+// per queue entry, 1037 mostly empty blocks per S13 layer, 55 us on the compute chain under the
+// concurrent fill; warps striding over all entries' groups, skipping host-filled ones, 47 us.)
+struct RequantArgs {
+    const uint8_t *pool16;
+    int64_t nb16, nb8, nb4;
+    const int32_t *q, *src_slot, *job;
+    int seg8, seg4, k8, k4;
+    uint8_t *stage8, *stage4;
+    unsigned long long *stat;  // [2]: INT8, INT4 requantised fills
+};
+__global__ void __launch_bounds__(1024) k_requant(int d, RequantArgs a) {
+    // block per job (k_missq compacted them: INT8 jobs, then INT4), its warps over the job's
+    // 3G groups, every group's loads in flight at once
     griddep_wait();
-    const int mi = blockIdx.x;
-    if (mi >= q[8 + tau]) return;
-    const int sl = src_slot[seg + mi];
-    if (sl < 0) return;
-    const int m = blockIdx.y;
-    const int G = d / 128;
-    const __half *w = reinterpret_cast<const __half *>(pool16 + (int64_t)sl * nb16) + (int64_t)m * d;
-    uint8_t *rec = stage + (int64_t)mi * nb;
-    const int64_t data_bytes = (BITS == 8) ? 3LL * d : 3LL * d / 2;
-    uint8_t *scales = rec + data_bytes;
-    uint8_t *zeros = scales + 6 * G;
-    for (int gi = threadIdx.x >> 5; gi < G; gi += blockDim.x / 32) pack_group<BITS>(w, d, m, gi, rec, scales, zeros);
-    if (m == 2 && threadIdx.x == 0) {
-        for (int64_t b = data_bytes + 9 * G; b < nb; b++) rec[b] = 0;
-        atomicAdd(stat, 1ull);
+    const int G = d / 128, UG = 3 * G;
+    const int j8 = a.q[13], j4 = a.q[14];
+    for (int jb = blockIdx.x; jb < j8 + j4; jb += gridDim.x) {
+        const bool i8 = jb < j8;
+        const int seg = i8 ? a.seg8 : a.seg4;
+        const int mi = a.job[seg + (i8 ? jb : jb - j8)];
+        const int sl = a.src_slot[seg + mi];
+        const __half *w16 = reinterpret_cast<const __half *>(a.pool16 + (int64_t)sl * a.nb16);
+        const int64_t nb = i8 ? a.nb8 : a.nb4;
+        uint8_t *rec = (i8 ? a.stage8 : a.stage4) + (int64_t)mi * nb;
+        const int64_t data_bytes = i8 ? 3LL * d : 3LL * d / 2;
+        uint8_t *scales = rec + data_bytes;
+        uint8_t *zeros = scales + 6 * G;
+        for (int g = threadIdx.x >> 5; g < UG; g += blockDim.x >> 5) {
+            const int m = g / G, gi = g - m * G;
+            if (i8) pack_group<8>(w16 + (int64_t)m * d, d, m, gi, rec, scales, zeros);
+            else pack_group<4>(w16 + (int64_t)m * d, d, m, gi, rec, scales, zeros);
+        }
+        if (threadIdx.x == 0) {
+            for (int64_t b = data_bytes + 9 * G; b < nb; b++) rec[b] = 0;  // the padding tail
+            atomicAdd(a.stat + (i8 ? 0 : 1), 1ull);
+        }
     }
 }
 
@@ -166,21 +181,26 @@ cudaError_t launch_transpose_i8(int r, int d, const int8_t *A, int8_t *At, cudaS
 // FP16 pool's slots are read before this step's scatter can overwrite a victim)
 cudaError_t launch_requant(m2c_ctx *c, const LayerState &L, const m2c_tier_plan &p, cudaStream_t st) {
     const int d = c->desc.d_model;
-    const int kt[3] = {p.k_fp16, p.k_int8, p.k_int4};
-    const int seg[3] = {0, p.k_fp16, p.k_fp16 + p.k_int8};
-    cudaError_t e = cudaSuccess;
-    for (int t = 1; t < 3 && e == cudaSuccess; t++) {
-        if (kt[t] <= 0) continue;
-        if (t == 1)
-            e = launch_k(k_requant<8>, dim3((unsigned)kt[t], 3), dim3(128), 0, st, d, (const uint8_t *)L.pool[0],
-                         c->nb[0], (const int32_t *)c->mq, 1, seg[1], (const int32_t *)c->mq_src, c->mstage[1],
-                         c->nb[1], c->ws.stats + 9);
-        else
-            e = launch_k(k_requant<4>, dim3((unsigned)kt[t], 3), dim3(128), 0, st, d, (const uint8_t *)L.pool[0],
-                         c->nb[0], (const int32_t *)c->mq, 2, seg[2], (const int32_t *)c->mq_src, c->mstage[2],
-                         c->nb[2], c->ws.stats + 10);
-        c->launch_counter++;
-    }
+    const int nblk = p.k_int8 + p.k_int4;
+    if (nblk <= 0) return cudaSuccess;
+    RequantArgs a;
+    a.pool16 = L.pool[0];
+    a.nb16 = c->nb[0];
+    a.nb8 = c->nb[1];
+    a.nb4 = c->nb[2];
+    a.q = c->mq;
+    a.src_slot = c->mq_src;
+    a.job = c->mq_job;
+    a.seg8 = p.k_fp16;
+    a.seg4 = p.k_fp16 + p.k_int8;
+    a.k8 = p.k_int8;
+    a.k4 = p.k_int4;
+    a.stage8 = c->mstage[1];
+    a.stage4 = c->mstage[2];
+    a.stat = c->ws.stats + 9;
+    const int thr = 32 * (3 * (d / 128) < 32 ? 3 * (d / 128) : 32);
+    cudaError_t e = launch_k(k_requant, dim3((unsigned)c->num_sms), dim3(thr), 0, st, d, a);
+    c->launch_counter++;
     return e;
 }
 

@@ -148,6 +148,7 @@ struct m2c_ctx {
     int32_t *mq = nullptr;        // [16 + k]: q[8 + t] = misses of tier t; ids from q + 16
     int32_t *ident = nullptr;     // [k]: ident[seg_t + m] = m
     int32_t *mq_src = nullptr;    // [k]: FP16-pool slot of an INT miss filled by requantisation, or -1
+    int32_t *mq_job = nullptr;    // [k]: the requantisation jobs' queue entries (per tier segment)
     bool requant = true;          // early-fill engine: INT misses from resident FP16 records
     uint8_t *mstage[3] = {nullptr, nullptr, nullptr};  // [k_t][nb_t]
     void *early_mem = nullptr;

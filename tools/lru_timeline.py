@@ -86,6 +86,7 @@ print("per-layer means (ms): layer %.4f | select %.4f | fill start->end %.4f | a
          np.mean(ev[:, :, 6] - ev[:, :, 5]), np.mean(ev[:, :, 3] - ev[:, :, 6]), np.mean(ev[:, :, 4] - ev[:, :, 3])))
 lay = np.mean(np.diff(ev[:, :, 0], axis=1))
 fill = np.mean(ev[:, :, 6] - ev[:, :, 5])
+print("compute stream: select -> miss queue %.4f -> requant %.4f" % (np.mean(ev[:, :, 9] - ev[:, :, 2]), np.mean(ev[:, :, 10] - ev[:, :, 9])))
 print("compute stream: select -> LRU update %.4f, -> hit FFN done %.4f ms; miss FFN after max(fill, hit FFN) %.4f"
       % (np.mean(ev[:, :, 7] - ev[:, :, 2]), np.mean(ev[:, :, 8] - ev[:, :, 2]),
          np.mean(ev[:, :, 3] - np.maximum(ev[:, :, 6], ev[:, :, 8]))))
