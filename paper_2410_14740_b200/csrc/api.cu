@@ -296,8 +296,9 @@ static cudaError_t enqueue_layer(m2c_ctx *c, int l, __half *x) {
         if ((e = launch_decode(c, x, c->prof_ev.empty() ? nullptr : c->dec_prof, st, l, 1, nullptr,
                                nullptr, ids)))
             return e;
-        // (rank order -> ascending ids per tier: the order the LRU update pairs misses in, R7)
-        if ((e = launch_sort_tiers(c, ids, p, st))) return e;
+        // (rank order -> ascending ids per tier: the order the LRU update pairs misses in, R7;
+        // the early-fill engine's k_missq sorts them itself)
+        if (!early_fill_on(c) && (e = launch_sort_tiers(c, ids, p, st))) return e;
         if ((e = mark(c, l, 1))) return e;
         if ((e = mark(c, l, 2))) return e;
     } else {
@@ -317,7 +318,7 @@ static cudaError_t enqueue_layer(m2c_ctx *c, int l, __half *x) {
         // An INT8 / INT4 miss whose neuron is resident in the FP16 pool is filled by quantising
         // that record on the GPU (k_requant, the offline pack's function) instead of over PCIe
         const bool rq = requant_on(c);
-        if ((e = launch_missq(c, L, ids, p, st, rq ? c->mq_src : nullptr))) return e;
+        if ((e = launch_missq(c, L, ids, p, st, rq ? c->mq_src : nullptr, decode_select_ok(c)))) return e;
         if ((e = mark(c, l, 9))) return e;
         if ((e = cudaEventRecord(c->ev_q, st))) return e;
         if ((e = cudaStreamWaitEvent(c->copy, c->ev_q, 0))) return e;

@@ -201,17 +201,43 @@ __global__ void __launch_bounds__(NT, 1)
 // start into a staging area while k_lru runs; the miss FFN reads the staging area and the
 // records are scattered into their victim slots afterwards (copy stream).
 __global__ void __launch_bounds__(NT, 1)
-    k_missq(LruArgs a, const int32_t *__restrict__ tier_ids, int32_t *__restrict__ q,
-            int32_t *__restrict__ qsrc, int32_t *__restrict__ qjob) {
+    k_missq(LruArgs a, int32_t *__restrict__ tier_ids, int32_t *__restrict__ q,
+            int32_t *__restrict__ qsrc, int32_t *__restrict__ qjob, int F_r) {
     // q: [16] header (q[8 + t] = misses of tier t) | ids [k] (segments as tier_ids);
     // qsrc (or null): per entry the neuron's FP16-pool slot for an INT8 / INT4 miss whose FP16
     // record is resident (filled by requantisation, k_requant), else -1
     __shared__ int scan_sm[NW];
+    extern __shared__ uint32_t bm[];  // [ceil(F_r / 32)]: the tier's ids as a bitmap
     griddep_wait();
     const int tau = blockIdx.x;
     const int n = a.cnt[tau], seg = a.seg[tau];
     const int32_t *slot_of = a.slot_of[tau];
-    const int32_t *R = tier_ids + seg;
+    int32_t *R = tier_ids + seg;
+    if (F_r > 0 && n > 1) {
+        // the select leaves the tier lists in rank order; ascending ids first (R7: misses are
+        // paired with victims in ascending id order): distinct ids in [0, F_r) -> bitmap ->
+        // scan of the words' popcounts -> each thread writes its words' ids in order
+        const int W = (F_r + 31) >> 5;
+        for (int w = threadIdx.x; w < W; w += NT) bm[w] = 0u;
+        __syncthreads();
+        for (int i = threadIdx.x; i < n; i += NT) atomicOr(&bm[R[i] >> 5], 1u << (R[i] & 31));
+        __syncthreads();
+        const int per = (W + NT - 1) / NT;
+        const int w0 = min(W, (int)threadIdx.x * per), w1 = min(W, w0 + per);
+        int cnt = 0;
+        for (int w = w0; w < w1; w++) cnt += __popc(bm[w]);
+        int tot;
+        int at = block_scan1(cnt, &tot, scan_sm);
+        for (int w = w0; w < w1; w++) {
+            uint32_t b = bm[w];
+            while (b) {
+                const int k = __ffs(b) - 1;
+                b &= b - 1;
+                R[at++] = (w << 5) + k;
+            }
+        }
+        __syncthreads();  // (the block's global writes are visible to it after the barrier)
+    }
     const int CH = (n + NT - 1) / NT;
     const int i0 = min(n, (int)threadIdx.x * CH), i1 = min(n, i0 + CH);
     int nm = 0;
@@ -364,8 +390,11 @@ __global__ void __launch_bounds__(256) k_stage_clear(StageArgs a) {
 size_t lru_smem_bytes(int P2, int maxcnt) { (void)maxcnt; return 24 * (size_t)P2 + 8 * (size_t)(P2 / 32); }
 
 cudaError_t init_cache_attrs() {
-    return cudaFuncSetAttribute(k_lru, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)lru_smem_bytes(kMaxPoolSlots, kMaxPoolSlots));
+    cudaError_t e = cudaFuncSetAttribute(k_lru, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)lru_smem_bytes(kMaxPoolSlots, kMaxPoolSlots));
+    if (e == cudaSuccess)  // (k_missq's tier-sort bitmap: F_r <= 2^20)
+        e = cudaFuncSetAttribute(k_missq, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * (1 << 15));
+    return e;
 }
 
 cudaError_t launch_lru(m2c_ctx *c, LayerState &L, const int32_t *step_dev, const int32_t *tier_ids,
@@ -435,8 +464,8 @@ cudaError_t launch_stage_clear(m2c_ctx *c, const LayerState &Ln, int par, cudaSt
     return e;
 }
 
-cudaError_t launch_missq(m2c_ctx *c, const LayerState &L, const int32_t *tier_ids,
-                         const m2c_tier_plan &p, cudaStream_t st, int32_t *qsrc) {
+cudaError_t launch_missq(m2c_ctx *c, const LayerState &L, int32_t *tier_ids,
+                         const m2c_tier_plan &p, cudaStream_t st, int32_t *qsrc, bool sort) {
     LruArgs a;
     const int cnt[3] = {p.k_fp16, p.k_int8, p.k_int4};
     const int seg[3] = {0, p.k_fp16, p.k_fp16 + p.k_int8};
@@ -445,8 +474,9 @@ cudaError_t launch_missq(m2c_ctx *c, const LayerState &L, const int32_t *tier_id
         a.seg[t] = seg[t];
         a.cnt[t] = cnt[t];
     }
-    cudaError_t e = launch_k(k_missq, dim3(3), dim3(NT), 0, st, a, tier_ids, c->mq, qsrc,
-                             qsrc ? c->mq_job : nullptr);
+    const size_t smem = sort ? 4 * (size_t)((c->F_r + 31) / 32) : 0;
+    cudaError_t e = launch_k(k_missq, dim3(3), dim3(NT), smem, st, a, tier_ids, c->mq, qsrc,
+                             qsrc ? c->mq_job : nullptr, sort ? c->F_r : 0);
     c->launch_counter++;
     return e;
 }

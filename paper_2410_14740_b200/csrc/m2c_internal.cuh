@@ -206,8 +206,8 @@ cudaError_t launch_cand_keys(m2c_ctx *c, const int32_t *scores, const int32_t *r
 cudaError_t launch_select_global(m2c_ctx *c, const long long *keys, int n, const m2c_tier_plan &g,
                                  int32_t *tier_ids, int32_t *counts, cudaStream_t st);
 int select_blocks(int F_r);
-cudaError_t launch_missq(m2c_ctx *c, const LayerState &L, const int32_t *tier_ids,
-                         const m2c_tier_plan &p, cudaStream_t st, int32_t *qsrc = nullptr);
+cudaError_t launch_missq(m2c_ctx *c, const LayerState &L, int32_t *tier_ids, const m2c_tier_plan &p,
+                         cudaStream_t st, int32_t *qsrc = nullptr, bool sort = false);
 cudaError_t launch_requant(m2c_ctx *c, const LayerState &L, const m2c_tier_plan &p, cudaStream_t st);
 cudaError_t launch_copy_recs(m2c_ctx *c, const uint8_t *const src[3], uint8_t *const dst[3],
                              const m2c_tier_plan &p, const int32_t *counts, const int32_t *srci,
