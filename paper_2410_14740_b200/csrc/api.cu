@@ -294,8 +294,9 @@ static cudaError_t enqueue_layer(m2c_ctx *c, int l, __half *x) {
     if (L.mode != 0 && c->use_fused && decode_select_ok(c)) {
         // the predictor + exact select of k_decode in one launch (its P2/P3 phases)
         if ((e = launch_decode(c, x, c->prof_ev.empty() ? nullptr : c->dec_prof, st, l, 1, nullptr,
-                               nullptr, ids)))
+                               nullptr, ids, l > 0 && c->h_prepared)))
             return e;
+        c->h_prepared = false;
         // (rank order -> ascending ids per tier: the order the LRU update pairs misses in, R7;
         // the early-fill engine's k_missq sorts them itself)
         if (!early_fill_on(c) && (e = launch_sort_tiers(c, ids, p, st))) return e;
@@ -389,7 +390,13 @@ static cudaError_t enqueue_layer(m2c_ctx *c, int l, __half *x) {
             return e;
     } else {
         float *ytr = c->trace_y ? c->trace_y + (size_t)l * c->desc.d_model : nullptr;
-        if ((e = launch_reduce(c, np, c->ws.partial, x, ytr, nullptr, x, nullptr, st))) return e;
+        // the next layer's select-only k_decode: its h (and a clear histogram) from this reduce
+        const bool prep = l + 1 < c->desc.n_layers && c->layers[l + 1].mode != 0 && c->use_fused &&
+                          decode_select_ok(c) && !c->lookahead && !c->store;
+        if ((e = launch_reduce(c, np, c->ws.partial, x, ytr, nullptr, x, prep ? c->dec_hist : nullptr, st,
+                               prep ? c->layers[l + 1].A : nullptr)))
+            return e;
+        c->h_prepared = prep;
     }
     return mark(c, l, 4);
 }

@@ -89,6 +89,8 @@ struct DecArgs {
     const float *pre_y;         // [d] or null: the prologue first forms x = fp16(x + fp16(pre_y))
     float *post_y;              // [d] or null: R writes the reduced partial y here instead of x
     int select_only;            // 1: stop after P3 (one layer; the LRU engine follows)
+    int h_ready;                // select-only: h and the histogram were prepared by the previous
+                                // layer's k_reduce (no prologue, no prologue barrier)
     // §8(e) fused all-reduce over peer memory (d_ff-sharded whole-token decode):
     int nrank, rank;            // nrank > 1: the R phase exchanges the reduced y chunks
     unsigned long long *const *xpeer;  // [nrank] every rank's exchange buffer [2][nrank][d] (flag|f32)
@@ -268,7 +270,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
     STAMP(12);
 
     // ================= prologue: layer 0's h = A_0 x from this CTA's column chunks ==========
-    for (int ch = cta; ch < nchunk; ch += G) {
+    for (int ch = cta; ch < nchunk && !p.h_ready; ch += G) {
         if (tid < 32) {
             bool bad = false;
             int m, sh;
@@ -289,9 +291,11 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
     }
     // select-only launches leave their histogram dirty (no barrier after P3): every launch
     // clears layer 0's here, ordered before every CTA's P2 atomics by the barrier below
-    if (cta == G - 1)
-        for (int i = tid; i < kBins; i += NT) p.ghist[i] = 0;
-    grid_sync(p.bar_flags, base + ++nbar, p.err);
+    if (!p.h_ready) {
+        if (cta == G - 1)
+            for (int i = tid; i < kBins; i += NT) p.ghist[i] = 0;
+        grid_sync(p.bar_flags, base + ++nbar, p.err);
+    }
     STAMP(13);
 
     for (int l = 0; l < p.n_layers; l++) {
@@ -792,7 +796,7 @@ cudaError_t decode_write_layer_table(m2c_ctx *c, void *dev_table) {
 }
 
 cudaError_t launch_decode(m2c_ctx *c, __half *x, unsigned long long *prof, cudaStream_t st, int layer0,
-                          int nl, const float *pre_y, float *post_y, int32_t *lists_out) {
+                          int nl, const float *pre_y, float *post_y, int32_t *lists_out, bool h_ready) {
     const int d = c->desc.d_model;
     if (nl < 0) nl = c->desc.n_layers - layer0;
     DecArgs a;
@@ -819,6 +823,7 @@ cudaError_t launch_decode(m2c_ctx *c, __half *x, unsigned long long *prof, cudaS
     a.sdump = c->dec_sdump;
     a.lists = lists_out ? lists_out : c->prev_ids + (size_t)layer0 * (c->plan.k > 0 ? c->plan.k : 1);
     a.select_only = lists_out != nullptr;
+    a.h_ready = (lists_out && h_ready) ? 1 : 0;
     a.nrank = (c->p2p && !lists_out && !post_y) ? c->desc.shard_count : 1;
     a.rank = c->desc.shard_index;
     a.xpeer = c->p2p_xtab;

@@ -10,11 +10,12 @@ namespace {
 // grid d/32 CTAs x 1024 threads: lane = element of a 32-element slice, warp w sums rows w::32
 // (<= 10 independent loads in flight per thread), then warp 0 sums the 32 warp totals.
 __global__ void __launch_bounds__(1024) k_reduce(int d, int np, const float *__restrict__ partial,
-                                                 const __half *__restrict__ x,
-                                                 float *__restrict__ y32, __half *__restrict__ y16,
-                                                 __half *__restrict__ x_next,
-                                                 int *__restrict__ hist_zero) {
+                                                 const __half *x, float *__restrict__ y32,
+                                                 __half *__restrict__ y16, __half *x_next,
+                                                 int *__restrict__ hist_zero, const int8_t *__restrict__ At_next,
+                                                 long long *__restrict__ h_next, int r, uint32_t *__restrict__ err) {
     __shared__ float sm[32][33];
+    __shared__ int xm[32], xsh[32];
     griddep_launch();
     griddep_wait();
     // the FFN that read the score histogram is complete: clear it for the next layer
@@ -42,7 +43,29 @@ __global__ void __launch_bounds__(1024) k_reduce(int d, int np, const float *__r
         if (y32) y32[e] = y;
         const __half yh = __float2half_rn(y);
         if (y16) y16[e] = yh;
-        if (x_next) x_next[e] = __hadd(x[e], yh);
+        const __half xn = __hadd(x[e], yh);  // (x_next may alias x)
+        if (x_next) x_next[e] = xn;
+        if (At_next) {  // the next layer's h = A x: this chunk's exact integer part (R2)
+            bool bad = false;
+            int m, sh;
+            fp16_fixed(__half_as_ushort(xn), m, sh, bad);
+            if (bad) flag_error(err, 1u);
+            xm[lane] = m;
+            xsh[lane] = sh;
+        }
+    }
+    if (At_next) {  // (LRU engine: the next layer's select-only k_decode skips its prologue)
+        __syncthreads();
+        const int8_t *A = At_next + (int64_t)blockIdx.x * 32 * r;  // the chunk's 32 rows of A^T
+        for (int i2 = threadIdx.x; i2 < 2 * r; i2 += blockDim.x) {
+            const int i = i2 >> 1, j0 = 16 * (i2 & 1);
+            unsigned long long acc = 0;
+#pragma unroll
+            for (int j = 0; j < 16; j++)
+                acc += (unsigned long long)(long long)((int)A[(int64_t)(j0 + j) * r + i] * xm[j0 + j]) << xsh[j0 + j];
+            acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+            if ((i2 & 1) == 0 && acc) red_add_u64(h_next + (int64_t)i * kHStride, (long long)acc);
+        }
     }
 }
 
@@ -82,10 +105,11 @@ __global__ void k_set_counts(int32_t *dst, int32_t a, int32_t b, int32_t c) {
 
 cudaError_t launch_reduce(m2c_ctx *c, int n_partials, const float *partial, const __half *x,
                           float *y32, __half *y16, __half *x_next, int *hist_zero,
-                          cudaStream_t st) {
+                          cudaStream_t st, const int8_t *At_next) {
     const int d = c->desc.d_model;
     cudaError_t e = launch_k(k_reduce, dim3(d / 32), dim3(1024), 0, st, d, n_partials, partial, x,
-                             y32, y16, x_next, hist_zero);
+                             y32, y16, x_next, hist_zero, At_next, At_next ? c->dec_hb : (long long *)nullptr,
+                             c->desc.pred_rank, c->ws.err);
     c->launch_counter++;
     return e;
 }

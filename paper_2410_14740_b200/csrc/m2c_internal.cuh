@@ -169,6 +169,8 @@ struct m2c_ctx {
     uint32_t *err_host = nullptr;
     // early-fill engine: the last layer's scatter (copy stream) still reads the miss lists
     bool scat_pending = false;
+    // LRU engine: the last k_reduce also formed the next layer's h (enqueue-time state)
+    bool h_prepared = false;
     // per-call API: layer whose hit / miss lists the last m2c_cache_lookup_fill left in ws
     int ws_lists_layer = -1;
     bool fill_pending = false;        // per-call API: a miss fill still reads the ws miss lists
@@ -233,13 +235,15 @@ cudaError_t launch_ffn(m2c_ctx *c, const LayerState &L, const __half *x, const i
                        const int32_t *counts, const m2c_tier_plan &p, float *partial,
                        cudaStream_t st);
 cudaError_t launch_reduce(m2c_ctx *c, int n_partials, const float *partial, const __half *x,
-                          float *y32, __half *y16, __half *x_next, int *hist_zero, cudaStream_t st);
+                          float *y32, __half *y16, __half *x_next, int *hist_zero, cudaStream_t st,
+                          const int8_t *At_next = nullptr);  // At_next: + the next layer's h (LRU engine)
 cudaError_t launch_finalize(m2c_ctx *c, const float *y32, const __half *x, __half *y16,
                             __half *x_next, cudaStream_t st);
 // persistent decode kernel (k_decode.cu)
 cudaError_t launch_decode(m2c_ctx *c, __half *x, unsigned long long *prof, cudaStream_t st, int layer0 = 0,
                           int nl = -1, const float *pre_y = nullptr, float *post_y = nullptr,
-                          int32_t *lists_out = nullptr);  // lists_out: select-only (one layer)
+                          int32_t *lists_out = nullptr,  // lists_out: select-only (one layer)
+                          bool h_ready = false);  // select-only: h and the histogram prepared by k_reduce
 cudaError_t init_decode_attrs();
 cudaError_t decode_write_layer_table(m2c_ctx *c, void *dev_table);
 size_t decode_layer_table_bytes(int n_layers);
