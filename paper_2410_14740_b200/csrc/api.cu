@@ -202,6 +202,14 @@ static bool early_fill_on(const m2c_ctx *c) {
     return env_on && c->early_fill && c->early_mem && !c->lookahead && !c->store;
 }
 
+// the miss FFN overlapped with the fill through per-record flags (early-fill engine);
+// M2C_OVERLAP=0 disables it (A/B knob, results identical)
+static bool overlap_on(const m2c_ctx *c) {
+    static const bool env_on = !(getenv("M2C_OVERLAP") && atoi(getenv("M2C_OVERLAP")) == 0);
+    (void)c;
+    return env_on;
+}
+
 // GPU requantisation of INT misses from resident FP16 records (early-fill engine);
 // M2C_REQUANT=0 disables it (A/B knob, results identical)
 static bool requant_on(const m2c_ctx *c) {
@@ -214,7 +222,7 @@ static cudaError_t early_fill_alloc(m2c_ctx *c) {
     const m2c_tier_plan &p = c->plan;
     const int k = p.k > 0 ? p.k : 1;
     const int kt[3] = {p.k_fp16, p.k_int8, p.k_int4};
-    size_t off = a256(4 * (16 + (size_t)k)) + 3 * a256(4 * (size_t)k), st_off[3];
+    size_t off = a256(4 * (16 + (size_t)k)) + 4 * a256(4 * (size_t)k), st_off[3];
     for (int t = 0; t < 3; t++) {
         st_off[t] = off;
         off += a256((size_t)(kt[t] > 0 ? kt[t] : 1) * c->nb[t]);
@@ -226,13 +234,17 @@ static cudaError_t early_fill_alloc(m2c_ctx *c) {
     c->ident = reinterpret_cast<int32_t *>(b + a256(4 * (16 + (size_t)k)));
     c->mq_src = reinterpret_cast<int32_t *>(b + a256(4 * (16 + (size_t)k)) + a256(4 * (size_t)k));
     c->mq_job = reinterpret_cast<int32_t *>(b + a256(4 * (16 + (size_t)k)) + 2 * a256(4 * (size_t)k));
+    c->mq_ready = reinterpret_cast<int32_t *>(b + a256(4 * (16 + (size_t)k)) + 3 * a256(4 * (size_t)k));
     for (int t = 0; t < 3; t++) c->mstage[t] = b + st_off[t];
     std::vector<int32_t> id(k, 0);
     for (int t = 0, seg = 0; t < 3; seg += kt[t], t++)
         for (int m = 0; m < kt[t]; m++) id[seg + m] = m;
     if ((e = cudaMemset(c->mq, 0, 4 * (16 + (size_t)k)))) return e;
+    if ((e = cudaMemset(c->mq_ready, 0, 4 * (size_t)k))) return e;  // (no tag is 0)
     if ((e = cudaMemcpy(c->ident, id.data(), 4 * (size_t)k, cudaMemcpyHostToDevice))) return e;
     if ((e = cudaEventCreateWithFlags(&c->ev_q, cudaEventDisableTiming))) return e;
+    if ((e = cudaEventCreateWithFlags(&c->ev_rq, cudaEventDisableTiming))) return e;
+    if ((e = cudaStreamCreateWithFlags(&c->rq_stream, cudaStreamNonBlocking))) return e;
     return cudaEventCreateWithFlags(&c->ev_scat, cudaEventDisableTiming);
 }
 
@@ -319,16 +331,24 @@ static cudaError_t enqueue_layer(m2c_ctx *c, int l, __half *x) {
         // An INT8 / INT4 miss whose neuron is resident in the FP16 pool is filled by quantising
         // that record on the GPU (k_requant, the offline pack's function) instead of over PCIe
         const bool rq = requant_on(c);
-        if ((e = launch_missq(c, L, ids, p, st, rq ? c->mq_src : nullptr, decode_select_ok(c)))) return e;
+        // (mq_src always written: -1 = a host copy; the fill and the miss FFN's waits read it)
+        if ((e = launch_missq(c, L, ids, p, st, c->mq_src, decode_select_ok(c), rq))) return e;
         if ((e = mark(c, l, 9))) return e;
         if ((e = cudaEventRecord(c->ev_q, st))) return e;
         if ((e = cudaStreamWaitEvent(c->copy, c->ev_q, 0))) return e;
         if ((e = mark_copy(c, l, 0))) return e;
         const uint8_t *hsrc[3] = {L.host_rec[0], L.host_rec[1], L.host_rec[2]};
+        const bool ovl = overlap_on(c);
         if ((e = launch_copy_recs(c, hsrc, c->mstage, p, c->mq, c->mq + 16, c->ident, c->copy,
-                                  rq ? c->mq_src : nullptr)))
+                                  c->mq_src, ovl ? l : -1)))
             return e;
-        if (rq && (e = launch_requant(c, L, p, st))) return e;
+        // the requantisation on its own stream: k_lru and the hit FFN do not need it; the
+        // scatter (it may overwrite an FP16 victim the requantisation reads) and the miss FFN do
+        if (rq) {
+            if ((e = cudaStreamWaitEvent(c->rq_stream, c->ev_q, 0))) return e;
+            if ((e = launch_requant(c, L, p, c->rq_stream))) return e;
+            if ((e = cudaEventRecord(c->ev_rq, c->rq_stream))) return e;
+        }
         if ((e = mark(c, l, 10))) return e;
         if ((e = mark_copy(c, l, 1))) return e;
         if ((e = cudaEventRecord(c->ev_fill, c->copy))) return e;
@@ -341,6 +361,7 @@ static cudaError_t enqueue_layer(m2c_ctx *c, int l, __half *x) {
         if ((e = mark(c, l, 7))) return e;
         if ((e = cudaEventRecord(c->ev_lookup, st))) return e;
         if ((e = cudaStreamWaitEvent(c->copy, c->ev_lookup, 0))) return e;
+        if (rq && (e = cudaStreamWaitEvent(c->copy, c->ev_rq, 0))) return e;
         const uint8_t *ssrc[3] = {c->mstage[0], c->mstage[1], c->mstage[2]};
         uint8_t *pdst[3] = {L.pool[0], L.pool[1], L.pool[2]};
         if ((e = launch_copy_recs(c, ssrc, pdst, p, c->ws.counts, c->ident, c->ws.miss_items, c->copy)))
@@ -350,10 +371,14 @@ static cudaError_t enqueue_layer(m2c_ctx *c, int l, __half *x) {
         e = launch_ffn(c, L, x, c->ws.hit_items, c->ws.counts + 4, p, c->ws.partial, st);
         if (e) return e;
         if ((e = mark(c, l, 8))) return e;
-        if ((e = cudaStreamWaitEvent(st, c->ev_fill, 0))) return e;
+        // the miss FFN: with the overlap it starts now and takes each record as it lands
+        // (k_fill's per-record flags); else after the whole fill
+        if (!ovl && (e = cudaStreamWaitEvent(st, c->ev_fill, 0))) return e;
+        if (rq && (e = cudaStreamWaitEvent(st, c->ev_rq, 0))) return e;
         LayerState Ls = L;
         for (int t = 0; t < 3; t++) Ls.pool[t] = c->mstage[t];
-        e = launch_ffn(c, Ls, x, c->ident, c->mq + 8, p, c->ws.partial + (size_t)c->G * c->desc.d_model, st);
+        e = launch_ffn(c, Ls, x, c->ident, c->mq + 8, p, c->ws.partial + (size_t)c->G * c->desc.d_model, st,
+                       ovl ? l : -1);
         if (e) return e;
         np = 2 * c->G;
     } else {
@@ -693,6 +718,11 @@ m2c_status m2c_destroy(m2c_ctx *c) {
         cudaFree(c->early_mem);
     }
     if (c->ev_q) cudaEventDestroy(c->ev_q);
+    if (c->ev_rq) cudaEventDestroy(c->ev_rq);
+    if (c->rq_stream) {
+        cudaStreamSynchronize(c->rq_stream);
+        cudaStreamDestroy(c->rq_stream);
+    }
     if (c->ev_scat) cudaEventDestroy(c->ev_scat);
     for (void *p : c->p2p_opened) cudaIpcCloseMemHandle(p);
     if (c->p2p_tabs) cudaFree(c->p2p_tabs);

@@ -32,6 +32,8 @@
 //    s * sum (q - z) x (R5).
 //  * The per-CTA partial y goes to a [G][d] fp32 buffer reduced in a fixed order.
 #pragma once
+#include <type_traits>
+
 #include "m2c_internal.cuh"
 
 namespace m2c {
@@ -417,11 +419,17 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar, uint32_t count = 1) {
 //    entry as soon as its P units have arrived on it, then the down parts (+ tail); phase G
 //    runs on the other warps; in phase D every warp consumes the down entries in order and the
 //    producer re-issues freed space until every down entry is in.
-template <class SrcFn>
+struct NoWait {
+    __device__ __forceinline__ void operator()(int) const {}
+};
+// WaitFn wait(j): called by the lane that issues record j's copies, before them (the LRU
+// engine's miss FFN: the record is still landing in the staging area, k_fill publishes a
+// per-record flag; everything else: NoWait)
+template <class SrcFn, class WaitFn = NoWait>
 __device__ __forceinline__ void ffn_run(const FfnArgs &a, int d, int act, int n_items, int c1, int c2,
                                         SrcFn src, uint8_t *ring, const uint4 *xs, float *a_sm,
                                         FfnShared &sm, FfnPipe &pp, float *partial,
-                                        unsigned long long *stamps = nullptr) {
+                                        unsigned long long *stamps = nullptr, WaitFn wait = WaitFn()) {
     const int NW = blockDim.x >> 5;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     auto tier_of = [&](int j) { return j < c1 ? 0 : (j < c2 ? 1 : 2); };
@@ -448,10 +456,24 @@ __device__ __forceinline__ void ffn_run(const FfnArgs &a, int d, int act, int n_
                 if (j < n_items) {
                     const unsigned s = fslot(j);
                     sm.roff[s] = base + inc - sz;
-                    mbar_expect_tx(&sm.full[s], (uint32_t)sz);
-                    bulk_g2s(ring + base + inc - sz, src(j), (uint32_t)sz, &sm.full[s], pol);
+                    if constexpr (std::is_same<WaitFn, NoWait>::value) {
+                        mbar_expect_tx(&sm.full[s], (uint32_t)sz);
+                        bulk_g2s(ring + base + inc - sz, src(j), (uint32_t)sz, &sm.full[s], pol);
+                    }
                 }
                 base += __shfl_sync(0xffffffffu, inc, 31);
+            }
+            if constexpr (!std::is_same<WaitFn, NoWait>::value) {
+                // records still landing: one lane issues them in order as each is published,
+                // so the units of the early ones run while the later ones arrive
+                __syncwarp();
+                if (lane == 0)
+                    for (int j = 0; j < n_items; j++) {
+                        const unsigned s = fslot(j);
+                        wait(j);
+                        mbar_expect_tx(&sm.full[s], (uint32_t)a.nb[tier_of(j)]);
+                        bulk_g2s(ring + sm.roff[s], src(j), (uint32_t)a.nb[tier_of(j)], &sm.full[s], pol);
+                    }
             }
         }
     } else if (warp == NW - 1) {
@@ -472,6 +494,7 @@ __device__ __forceinline__ void ffn_run(const FfnArgs &a, int d, int act, int n_
                 wpos = off + sz;
                 if (lane == 0) {
                     const uint8_t *g = src(head);
+                    wait(head);
                     sm.roff[s] = off;
                     sm.span[s] = need;
                     mbar_expect_tx(&sm.full[s], (uint32_t)sz);

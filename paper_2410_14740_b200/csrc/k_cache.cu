@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(NT, 1)
 // records are scattered into their victim slots afterwards (copy stream).
 __global__ void __launch_bounds__(NT, 1)
     k_missq(LruArgs a, int32_t *__restrict__ tier_ids, int32_t *__restrict__ q,
-            int32_t *__restrict__ qsrc, int32_t *__restrict__ qjob, int F_r) {
+            int32_t *__restrict__ qsrc, int32_t *__restrict__ qjob, int F_r, int requant) {
     // q: [16] header (q[8 + t] = misses of tier t) | ids [k] (segments as tier_ids);
     // qsrc (or null): per entry the neuron's FP16-pool slot for an INT8 / INT4 miss whose FP16
     // record is resident (filled by requantisation, k_requant), else -1
@@ -248,7 +248,7 @@ __global__ void __launch_bounds__(NT, 1)
     const int pos0 = pos;
     for (int i = i0; i < i1; i++)
         if (slot_of[R[i]] < 0) {
-            const int s16 = (qsrc && tau > 0) ? a.slot_of[0][R[i]] : -1;
+            const int s16 = (qsrc && requant && tau > 0) ? a.slot_of[0][R[i]] : -1;
             if (qsrc) qsrc[seg + pos] = s16;
             nj += s16 >= 0;
             q[16 + seg + pos++] = R[i];
@@ -286,6 +286,9 @@ struct FillArgs {
     const uint8_t *stage[3];
     unsigned long long *staged;  // count of misses filled from the staging buffers
     const int32_t *skip;         // or null: entries with skip[seg + m] >= 0 are not copied
+    int32_t *ready;              // or null: ready[seg + m] = fill_tag(*step_ptr, layer) once copied
+    const int32_t *step_ptr;
+    int layer;
 };
 
 // a5: SM-driven gather of the missed records from the pinned host tier (UVA-mapped) into
@@ -322,6 +325,15 @@ __global__ void __launch_bounds__(256) k_fill(FillArgs a, const int32_t *__restr
             for (int j = 0; j < M2C_FILL_U; j++) {
                 const int64_t c = base + lane + 32 * j;
                 if (c < nv) dst[c] = v[j];
+            }
+        }
+        if (a.ready) {  // the record landed: publish it (release after the warp's stores)
+            __syncwarp();
+            if (lane == 0) {
+                __threadfence();
+                asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(a.ready + a.seg[tau] + m),
+                             "r"(fill_tag(*a.step_ptr, a.layer))
+                             : "memory");
             }
         }
     }
@@ -465,7 +477,7 @@ cudaError_t launch_stage_clear(m2c_ctx *c, const LayerState &Ln, int par, cudaSt
 }
 
 cudaError_t launch_missq(m2c_ctx *c, const LayerState &L, int32_t *tier_ids,
-                         const m2c_tier_plan &p, cudaStream_t st, int32_t *qsrc, bool sort) {
+                         const m2c_tier_plan &p, cudaStream_t st, int32_t *qsrc, bool sort, bool requant) {
     LruArgs a;
     const int cnt[3] = {p.k_fp16, p.k_int8, p.k_int4};
     const int seg[3] = {0, p.k_fp16, p.k_fp16 + p.k_int8};
@@ -476,7 +488,7 @@ cudaError_t launch_missq(m2c_ctx *c, const LayerState &L, int32_t *tier_ids,
     }
     const size_t smem = sort ? 4 * (size_t)((c->F_r + 31) / 32) : 0;
     cudaError_t e = launch_k(k_missq, dim3(3), dim3(NT), smem, st, a, tier_ids, c->mq, qsrc,
-                             qsrc ? c->mq_job : nullptr, sort ? c->F_r : 0);
+                             qsrc ? c->mq_job : nullptr, sort ? c->F_r : 0, requant ? 1 : 0);
     c->launch_counter++;
     return e;
 }
@@ -485,7 +497,7 @@ cudaError_t launch_missq(m2c_ctx *c, const LayerState &L, int32_t *tier_ids,
 // counts[8 + t] entries of each tier (k_fill without the lookahead)
 cudaError_t launch_copy_recs(m2c_ctx *c, const uint8_t *const src[3], uint8_t *const dst[3],
                              const m2c_tier_plan &p, const int32_t *counts, const int32_t *srci,
-                             const int32_t *dsti, cudaStream_t st, const int32_t *skip) {
+                             const int32_t *dsti, cudaStream_t st, const int32_t *skip, int ready_layer) {
     FillArgs a;
     const int seg[3] = {0, p.k_fp16, p.k_fp16 + p.k_int8};
     for (int t = 0; t < 3; t++) {
@@ -498,6 +510,9 @@ cudaError_t launch_copy_recs(m2c_ctx *c, const uint8_t *const src[3], uint8_t *c
     }
     a.staged = c->ws.stats + 6;
     a.skip = skip;
+    a.ready = ready_layer >= 0 ? c->mq_ready : nullptr;
+    a.step_ptr = c->ws.counts + 15;
+    a.layer = ready_layer;
     static const int fill_ctas = getenv("M2C_FILL_CTAS") ? atoi(getenv("M2C_FILL_CTAS")) : 32;
     cudaError_t e = launch_k(k_fill, dim3(fill_ctas), dim3(256), 0, st, a, counts, srci, dsti);
     c->launch_counter++;
@@ -518,6 +533,9 @@ cudaError_t launch_fill(m2c_ctx *c, const LayerState &L, const m2c_tier_plan &p,
     }
     a.staged = c->ws.stats + 6;
     a.skip = nullptr;
+    a.ready = nullptr;
+    a.step_ptr = nullptr;
+    a.layer = 0;
     static const int fill_ctas = getenv("M2C_FILL_CTAS") ? atoi(getenv("M2C_FILL_CTAS")) : 32;  // tuning knob
     cudaError_t e = launch_k(k_fill, dim3(fill_ctas), dim3(256), 0, st, a, c->ws.counts, c->ws.miss_ids,
                              c->ws.miss_items);

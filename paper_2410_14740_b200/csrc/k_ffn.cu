@@ -7,9 +7,41 @@ namespace {
 
 
 // ---- list-driven FFN (API path: m2c_sparse_ffn_forward, LRU hits / misses) --------------
+// the miss FFN of the early-fill LRU engine consumes the staging area while k_fill (copy
+// stream) is still filling it: entry e (tier segment offset included) is ready when
+// ready[e] == tag (k_fill's release store after the record's bytes) or it was requantised
+// (skip[e] >= 0: k_requant ran earlier on this stream)
+struct RecWait {
+    const int32_t *ready, *skip, *items, *step_ptr;
+    int layer, seg[3], a0[3], c1, c2;
+    uint32_t *err;
+    __device__ __forceinline__ void operator()(int j) const {
+        if (!ready) return;
+        const int t = j < c1 ? 0 : (j < c2 ? 1 : 2);
+        const int jj = j - (t == 0 ? 0 : (t == 1 ? c1 : c2));
+        const int e = seg[t] + items[seg[t] + a0[t] + jj];
+        if (skip && skip[e] >= 0) return;
+        const int tag = fill_tag(*step_ptr, layer);
+        int v;
+        asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(ready + e) : "memory");
+        if (v != tag) {
+            const unsigned long long t0 = clock64();
+            do {
+                __nanosleep(100);
+                asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(ready + e) : "memory");
+                if (clock64() - t0 > 4000000000ull) {  // ~2 s: a record that never lands
+                    flag_error(err, 4u);
+                    break;
+                }
+            } while (v != tag);
+        }
+        asm volatile("fence.proxy.async.global;" ::: "memory");  // (the TMA reads what it saw)
+    }
+};
+
 __global__ void __launch_bounds__(1024, 1)
     k_ffn(FfnArgs a, int d, int act, const __half *__restrict__ x, const int32_t *__restrict__ items,
-          const int32_t *__restrict__ counts, float *__restrict__ partial) {
+          const int32_t *__restrict__ counts, float *__restrict__ partial, RecWait w) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ FfnShared sm;
     const SmemPtrs S = carve(smem);
@@ -31,7 +63,16 @@ __global__ void __launch_bounds__(1024, 1)
         return a.pool[2] + (int64_t)items[a.seg[2] + a2 + (j - c2)] * a.nb[2];
     };
     FfnPipe pipe;
-    ffn_run(a, d, act, n_items, c1, c2, src, S.ring, S.xs, S.a, sm, pipe, partial);
+    if (w.ready) {
+        w.items = items;
+        w.c1 = c1;
+        w.c2 = c2;
+        for (int t = 0; t < 3; t++) w.seg[t] = a.seg[t];
+        w.a0[0] = a0;
+        w.a0[1] = a1;
+        w.a0[2] = a2;
+    }
+    ffn_run(a, d, act, n_items, c1, c2, src, S.ring, S.xs, S.a, sm, pipe, partial, nullptr, w);
 }
 
 }  // namespace
@@ -42,12 +83,20 @@ cudaError_t init_ffn_attrs() {
 
 cudaError_t launch_ffn(m2c_ctx *c, const LayerState &L, const __half *x, const int32_t *items,
                        const int32_t *counts, const m2c_tier_plan &p, float *partial,
-                       cudaStream_t st) {
+                       cudaStream_t st, int wait_layer) {
     const int d = c->desc.d_model;
     FfnArgs a;
     fill_args(c, L, p, a);
+    RecWait w = {};
+    if (wait_layer >= 0) {  // (the early-fill engine's miss FFN)
+        w.ready = c->mq_ready;
+        w.skip = c->mq_src;
+        w.step_ptr = c->ws.counts + 15;
+        w.layer = wait_layer;
+        w.err = c->ws.err;
+    }
     cudaError_t e = launch_k(k_ffn, dim3(c->G), dim3(d / 8), kSmemBytes, st, a, d, c->desc.act, x,
-                             items, counts, partial);
+                             items, counts, partial, w);
     c->launch_counter++;
     return e;
 }

@@ -15,11 +15,10 @@ namespace {
 // One 128-group gi of row w (matrix m) into an INT record: the warp's lanes hold 4 values
 // each; min/max by shuffles; codes, fp16 scale and u8 zero-point written at their places.
 template <int BITS>
-__device__ __forceinline__ void pack_group(const __half *w, int d, int m, int gi, uint8_t *rec, uint8_t *scales,
-                                           uint8_t *zeros) {
+__device__ __forceinline__ void pack_group_raw(const uint2 raw, int d, int m, int gi, uint8_t *rec, uint8_t *scales,
+                                               uint8_t *zeros) {
     constexpr int maxq = (1 << BITS) - 1;
     const int G = d / 128, lane = threadIdx.x & 31;
-    const uint2 raw = *reinterpret_cast<const uint2 *>(w + gi * 128 + lane * 4);
     float v[4];
     {
         __half2 a = *reinterpret_cast<const __half2 *>(&raw.x);
@@ -68,6 +67,12 @@ __device__ __forceinline__ void pack_group(const __half *w, int d, int m, int gi
         *reinterpret_cast<unsigned short *>(scales + 2 * (m * G + gi)) = s16;
         zeros[m * G + gi] = (uint8_t)z;
     }
+}
+template <int BITS>
+__device__ __forceinline__ void pack_group(const __half *w, int d, int m, int gi, uint8_t *rec, uint8_t *scales,
+                                           uint8_t *zeros) {
+    const uint2 raw = *reinterpret_cast<const uint2 *>(w + gi * 128 + (threadIdx.x & 31) * 4);
+    pack_group_raw<BITS>(raw, d, m, gi, rec, scales, zeros);
 }
 
 // One warp per 128-group; blockIdx.y = matrix (0 gate, 1 up, 2 down), blockIdx.x = neuron.
@@ -125,10 +130,23 @@ __global__ void __launch_bounds__(1024) k_requant(int d, RequantArgs a) {
         const int64_t data_bytes = i8 ? 3LL * d : 3LL * d / 2;
         uint8_t *scales = rec + data_bytes;
         uint8_t *zeros = scales + 6 * G;
-        for (int g = threadIdx.x >> 5; g < UG; g += blockDim.x >> 5) {
-            const int m = g / G, gi = g - m * G;
-            if (i8) pack_group<8>(w16 + (int64_t)m * d, d, m, gi, rec, scales, zeros);
-            else pack_group<4>(w16 + (int64_t)m * d, d, m, gi, rec, scales, zeros);
+        // every group of this warp (<= 4 at d <= 5376 with 32 warps) loaded before any is packed
+        const int NWb = blockDim.x >> 5, lane = threadIdx.x & 31;
+        for (int g0 = threadIdx.x >> 5; g0 < UG; g0 += 4 * NWb) {
+            uint2 raw[4];
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+                const int g = g0 + k * NWb;
+                if (g < UG) raw[k] = *reinterpret_cast<const uint2 *>(w16 + (int64_t)g * 128 + lane * 4);
+            }
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+                const int g = g0 + k * NWb;
+                if (g >= UG) break;
+                const int m = g / G, gi = g - m * G;
+                if (i8) pack_group_raw<8>(raw[k], d, m, gi, rec, scales, zeros);
+                else pack_group_raw<4>(raw[k], d, m, gi, rec, scales, zeros);
+            }
         }
         if (threadIdx.x == 0) {
             for (int64_t b = data_bytes + 9 * G; b < nb; b++) rec[b] = 0;  // the padding tail

@@ -149,6 +149,9 @@ struct m2c_ctx {
     int32_t *ident = nullptr;     // [k]: ident[seg_t + m] = m
     int32_t *mq_src = nullptr;    // [k]: FP16-pool slot of an INT miss filled by requantisation, or -1
     int32_t *mq_job = nullptr;    // [k]: the requantisation jobs' queue entries (per tier segment)
+    int32_t *mq_ready = nullptr;  // [k]: staging entry landed (fill_tag(step, layer)), per tier segment
+    cudaStream_t rq_stream = nullptr;  // the requantisation (off the compute chain)
+    cudaEvent_t ev_rq = nullptr;
     bool requant = true;          // early-fill engine: INT misses from resident FP16 records
     uint8_t *mstage[3] = {nullptr, nullptr, nullptr};  // [k_t][nb_t]
     void *early_mem = nullptr;
@@ -209,11 +212,12 @@ cudaError_t launch_select_global(m2c_ctx *c, const long long *keys, int n, const
                                  int32_t *tier_ids, int32_t *counts, cudaStream_t st);
 int select_blocks(int F_r);
 cudaError_t launch_missq(m2c_ctx *c, const LayerState &L, int32_t *tier_ids, const m2c_tier_plan &p,
-                         cudaStream_t st, int32_t *qsrc = nullptr, bool sort = false);
+                         cudaStream_t st, int32_t *qsrc = nullptr, bool sort = false, bool requant = false);
 cudaError_t launch_requant(m2c_ctx *c, const LayerState &L, const m2c_tier_plan &p, cudaStream_t st);
 cudaError_t launch_copy_recs(m2c_ctx *c, const uint8_t *const src[3], uint8_t *const dst[3],
                              const m2c_tier_plan &p, const int32_t *counts, const int32_t *srci,
-                             const int32_t *dsti, cudaStream_t st, const int32_t *skip = nullptr);
+                             const int32_t *dsti, cudaStream_t st, const int32_t *skip = nullptr,
+                             int ready_layer = -1);  // ready_layer >= 0: publish mq_ready per record
 cudaError_t launch_lru(m2c_ctx *c, LayerState &L, const int32_t *step_dev, const int32_t *tier_ids,
                        const m2c_tier_plan &p, int32_t *slots, uint32_t *hit_bits,
                        int32_t *miss_log, int32_t *evict_log, cudaStream_t st);
@@ -233,7 +237,7 @@ void store_stats(m2c_ctx *c, int64_t *bytes, int64_t *loads, double *io_s, doubl
 m2c_status store_write(m2c_ctx *c, const char *path, size_t layer_bytes);
 cudaError_t launch_ffn(m2c_ctx *c, const LayerState &L, const __half *x, const int32_t *items,
                        const int32_t *counts, const m2c_tier_plan &p, float *partial,
-                       cudaStream_t st);
+                       cudaStream_t st, int wait_layer = -1);  // wait_layer: the early-fill miss FFN
 cudaError_t launch_reduce(m2c_ctx *c, int n_partials, const float *partial, const __half *x,
                           float *y32, __half *y16, __half *x_next, int *hist_zero, cudaStream_t st,
                           const int8_t *At_next = nullptr);  // At_next: + the next layer's h (LRU engine)
@@ -413,6 +417,8 @@ __device__ __forceinline__ void flag_error(uint32_t *err, unsigned bit) {
     uint32_t *mirror = *reinterpret_cast<uint32_t *const *>(err + 2);
     if (mirror) *reinterpret_cast<volatile uint32_t *>(mirror) = 0x80000000u | bit;
 }
+// the per-(step, layer) value of a landed staging entry's ready flag (early-fill engine)
+__device__ __forceinline__ int fill_tag(int step, int layer) { return step * 256 + layer + 1; }
 __device__ __forceinline__ void red_add_u64(long long *p, long long v) {
     asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
