@@ -64,7 +64,9 @@ def oracle_layer(wn, plan, x, act=0):
     return ids, yhat
 
 
-def _stack(m2c, cfg, plan, L, shard=(0, 1), cc_mode=None, B_hook=None):
+def _stack(m2c, cfg, plan, L, shard=(0, 1), cc_mode=None, B_hook=None, full=None):
+    # full: the layers whose FFN weights are kept on the host for the oracle (None = all; the
+    # others keep only the predictor, enough for the tier-list check)
     ctx = m2c.M2CContext(cfg.d_model, cfg.d_ff, L, cfg.pred_rank, plan, shard=shard,
                          act=0 if cfg.act == "silu" else 1)
     cc = None
@@ -77,6 +79,8 @@ def _stack(m2c, cfg, plan, L, shard=(0, 1), cc_mode=None, B_hook=None):
         if B_hook:
             w["pred_B"] = B_hook(w["pred_B"])
         ctx.load_layer(l, w["w_gate"], w["w_up"], w["w_down_t"], w["pred_A"], w["pred_B"], cc)
+        if full is not None and l not in full:
+            w = {k: w[k] for k in ("pred_A", "pred_B")}
         ws.append(_np(w))
         del w
     return ctx, ws, cc
@@ -145,6 +149,26 @@ def test_full_s7_stack_decode_replay_against_oracle(m2c):
         ctx.decode_step(x, t + 1)
         torch.cuda.synchronize()
         _check_token(ctx, ws, plan, cfg.n_layers, y_layers={0, 13, cfg.n_layers - 1} if t == 0 else {31})
+    assert ctx.stats()["kernels_per_token"] == 1
+    ctx.close()
+
+
+def test_full_s70h_stack_decode_replay_against_oracle(m2c):
+    """The bench default (the 1-GPU point of configs[3]) at full size in the launch
+    configuration bench.py times: 40 layers of 8192 x 28672, one k_decode launch per token
+    (streaming FFN shares, 1024 threads); every layer's lists equal the oracle's on the traced
+    input, y at sampled layers within the tolerance."""
+    cfg = get_config("S70H")
+    plan = m2c.plan_of(cfg)
+    ys = {0, 20, cfg.n_layers - 1}
+    ctx, ws, _ = _stack(m2c, cfg, plan, cfg.n_layers, full=ys)
+    ctx.set_trace(True)
+    xs = token_stream(cfg, 2, device="cuda")
+    for t in range(2):
+        x = xs[t].contiguous().clone()
+        ctx.decode_step(x, t + 1)
+        torch.cuda.synchronize()
+        _check_token(ctx, ws, plan, cfg.n_layers, y_layers=ys if t == 0 else {cfg.n_layers - 1})
     assert ctx.stats()["kernels_per_token"] == 1
     ctx.close()
 
