@@ -50,8 +50,7 @@ constexpr int kBins = 4096;
 constexpr int kCap = 128;  // bucket slots per histogram bin (more: the exact fallback)
 // stamps per (layer, CTA): 0 layer start, 20 h + max, 21 hq + B slice, 22 scores, 1 P2 done, 4 after
 // Bs, 2 histogram in smem, 3 scan + needed bins, 10 share ranked, 5 P3 done, 14/15 FFN
-// internal (issue done / gate-up done), 6 FFN done, 7 after By, 16 R's A^T staged, 17 partial
-// rows summed, 18 y / x formed, 19 h contributions issued, 8 R done, 9 kernel end,
+// internal (issue done / gate-up done), 6 FFN done, 7 after By, 8 R done, 9 kernel end,
 // 12/13 prologue start / after its barrier
 constexpr int kStamps = kDecodeStamps;
 // ring offsets of the between-FFN phases (bytes)
@@ -251,8 +250,6 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
     __syncthreads();
     const int R_lo = share_lo, R_hi = share_hi, n_items = R_hi - R_lo;
     const int c1 = min(max(p.k16 - R_lo, 0), n_items), c2 = min(max(p.k16 + p.k8 - R_lo, 0), n_items);
-    const bool share_whole =
-        n_items <= kNS && (int64_t)c1 * p.nb[0] + (int64_t)(c2 - c1) * p.nb[1] + (int64_t)(n_items - c2) * p.nb[2] <= kRing;
     // (launched with programmatic stream serialization -- select-only launches of the LRU
     // engine: the set-up above overlapped the previous kernel; nothing it wrote is read above)
     griddep_wait();
@@ -483,11 +480,29 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
                     kv[u] = lane + 32 * u < c ? __ldcg(bk + lane + 32 * u) : 0ull;
                     rk[u] = 0;
                 }
+                // (512 threads, d <= 4096: the specialised loops below -- S7 +0.8% same-box;
+                // 1024 threads (S70H) keep the generic loop, measured 1.4% faster there)
+                if (MAXT == 1024) {
 #pragma unroll 1
-                for (int jj = 0; jj < c; jj++) {
-                    const unsigned long long kj = __shfl_sync(0xffffffffu, kv[jj >> 5], jj & 31);
+                    for (int jj = 0; jj < c; jj++) {
+                        const unsigned long long kj = __shfl_sync(0xffffffffu, kv[jj >> 5], jj & 31);
 #pragma unroll
-                    for (int u = 0; u < 4; u++) rk[u] += kj > kv[u];
+                        for (int u = 0; u < 4; u++) rk[u] += kj > kv[u];
+                    }
+                } else if (c <= 32) {  // (the common case: one key per lane, one compare per step)
+#pragma unroll 4
+                    for (int jj = 0; jj < c; jj++) rk[0] += __shfl_sync(0xffffffffu, kv[0], jj) > kv[0];
+                } else {  // (static register indices: kv stays out of local memory)
+#pragma unroll
+                    for (int h = 0; h < 4; h++) {
+                        const int m = min(32, c - 32 * h);
+#pragma unroll 1
+                        for (int jj = 0; jj < m; jj++) {
+                            const unsigned long long kj = __shfl_sync(0xffffffffu, kv[h], jj);
+#pragma unroll
+                            for (int u = 0; u < 4; u++) rk[u] += kj > kv[u];
+                        }
+                    }
                 }
 #pragma unroll
                 for (int u = 0; u < 4; u++) {
@@ -573,24 +588,6 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
         // barrier By; meanwhile (warp 1): layer l+1's A^T chunks of this CTA (for R) and its
         // B slice (for P2) -> smem by TMA
         const bool more = l + 1 < p.n_layers;
-#ifndef M2C_PF_PREV
-#define M2C_PF_PREV 0
-#endif
-        // (measurement knob, off) L2 prefetch of the records the PREVIOUS token selected at layer
-        // l+1 in this CTA's share (the list memory still holds them), issued by warp 1 during
-        // barrier Bx (HBM is idle until layer l+1's P4), for shares fetched whole: S7 +1.8%
-        // same-box, but the mispredicted records make the DRAM traffic 1.43x the algorithmic
-        // bytes.  Streaming shares (S70H) never prefetch: the issue stalled warp 1 ~3 us and P4
-        // did not get faster (profiles/r02_ffn_variants.txt).
-        auto pf_prev = [&] {
-            const int32_t *pl = p.lists + (int64_t)(l + 1) * (kk > 0 ? kk : 1);
-            const DecLayer &Ln = p.layers[l + 1];
-            for (int j = (threadIdx.x & 31); j < n_items; j += 32) {
-                const int q = R_lo + j, t = q < p.k16 ? 0 : (q < p.k16 + p.k8 ? 1 : 2);
-                const int id = __ldcg(pl + q);
-                if (id >= 0 && id < F_r) prefetch_l2(Ln.pool[t] + (int64_t)id * fa.nb[t], (uint32_t)fa.nb[t]);
-            }
-        };
         const int nown_c = cta < nchunk ? (nchunk - cta + G - 1) / G : 0;
         grid_sync(p.bar_flags, base + ++nbar, p.err, [&] {
             if (more && (threadIdx.x & 31) == 0) {
@@ -622,7 +619,6 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
             const size_t row = (size_t)((flag - 1u) & 1u) * P;
             const int ncc = min(nown_c, min(2, NW));  // chunks reduced concurrently
             if (more && nown_c > 0) mbar_wait(&at_bar, (uint32_t)(l & 1));  // A^T chunks staged at By
-            STAMP(16);
             for (int q0 = 0; q0 < nown_c; q0 += ncc) {
                 const int nc = min(ncc, nown_c - q0);
                 const int gw = NW / nc;  // warps per chunk
@@ -645,7 +641,6 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
                     rf[g * gw + v][lane] = acc;
                 }
                 __syncthreads();
-                STAMP(17);
                 if (g < nc && v == 0) {  // the group's first warp: y of its chunk
                     float y = 0.f;
                     for (int w = 0; w < gw; w++) y += rf[g * gw + w][lane];
@@ -695,21 +690,16 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
                     }
                 }
                 __syncthreads();
-                STAMP(18);
                 if (more) {
                     h_chunks(reinterpret_cast<const int8_t *>(S.ring + kAtOff) + (int64_t)q0 * 32 * r, nc, r,
                              xm, xsh, hnext);
                     __syncthreads();
                 }
-                STAMP(19);
             }
         }
         if (bk_in_r) bookkeeping();
         STAMP(8);
-        if (more) {
-            if (M2C_PF_PREV && share_whole) grid_sync(p.bar_flags, base + ++nbar, p.err, pf_prev);
-            else grid_sync(p.bar_flags, base + ++nbar, p.err);
-        }
+        if (more) grid_sync(p.bar_flags, base + ++nbar, p.err);
     }
     STAMP(9);
 #undef STAMP

@@ -71,8 +71,7 @@ print("P4 mean per CTA by sixths of the grid:", " ".join(f"{p4[i * G // 6:(i + 1
 for nm, (i, j) in {"gate/up": (14, 15), "down": (15, 6), "P2+Bs": (0, 4), "P3": (4, 5)}.items():
     v = np.mean([(s[:, :, j] - s[:, :, i]) / 1e3 for s in rows], axis=(0, 1))
     print(f"{nm:8s} by sixths:", " ".join(f"{v[q * G // 6:(q + 1) * G // 6].mean():.2f}" for q in range(6)))
-sub = {"P2 h+max": (0, 20), "P2 hq+B": (20, 21), "P2 dots": (21, 22), "P2 atomics": (22, 1), "P3 hist load": (4, 2), "P3 scan": (2, 3), "P3 rank": (3, 10), "P3 tail": (10, 5), "P4 issue": (5, 14), "P4 gate/up": (14, 15), "P4 down": (15, 6),
-       "R A^T wait": (7, 16), "R partials": (16, 17), "R y, x": (17, 18), "R h": (18, 19), "R tail": (19, 8)}
+sub = {"P2 h+max": (0, 20), "P2 hq+B": (20, 21), "P2 dots": (21, 22), "P2 atomics": (22, 1), "P3 hist load": (4, 2), "P3 scan": (2, 3), "P3 rank": (3, 10), "P3 tail": (10, 5), "P4 issue": (5, 14), "P4 gate/up": (14, 15), "P4 down": (15, 6)}
 for k, (i, j) in sub.items():
     v = np.mean([((s[:, :, j] - s[:, :, i]) / 1e3).mean() for s in rows])
     print(f"{k:12s} mean-CTA {v:.2f} us")
