@@ -436,6 +436,8 @@ __device__ __forceinline__ void ffn_run(const FfnArgs &a, int d, int act, int n_
     auto Dof = [&](int t) { return t == 0 ? 2 * d : (t == 1 ? d : d / 2); };
     const int total = c1 * a.nb[0] + (c2 - c1) * a.nb[1] + (n_items - c2) * a.nb[2];
     const bool whole = (n_items <= kNS && total <= kRing) || NW == 1;
+    M2C_CHECK(n_items >= 0 && n_items <= kMaxLocal && c1 >= 0 && c1 <= c2 && c2 <= n_items);
+    M2C_CHECK(!whole || total <= kRing);
     const uint64_t pol = policy_evict_first();
     const unsigned nf0 = pp.nf, ng0 = pp.ng;
     auto fslot = [&](unsigned e) { return (nf0 + e) % kNS; };
@@ -455,6 +457,7 @@ __device__ __forceinline__ void ffn_run(const FfnArgs &a, int d, int act, int n_
                 }
                 if (j < n_items) {
                     const unsigned s = fslot(j);
+                    M2C_CHECK(base + inc <= kRing && src(j) != nullptr);
                     sm.roff[s] = base + inc - sz;
                     if constexpr (std::is_same<WaitFn, NoWait>::value) {
                         mbar_expect_tx(&sm.full[s], (uint32_t)sz);
@@ -494,6 +497,7 @@ __device__ __forceinline__ void ffn_run(const FfnArgs &a, int d, int act, int n_
                 wpos = off + sz;
                 if (lane == 0) {
                     const uint8_t *g = src(head);
+                    M2C_CHECK(off + sz <= kRing && need <= kRing && g != nullptr);
                     wait(head);
                     sm.roff[s] = off;
                     sm.span[s] = need;
@@ -526,6 +530,7 @@ __device__ __forceinline__ void ffn_run(const FfnArgs &a, int d, int act, int n_
             else { j = c2 + (u - U1) / P2; q = (u - U1) - (j - c2) * P2; t = 2; Pt = P2; }
             const unsigned s = fslot(j);
             mbar_wait(&sm.full[s], fpar(j));
+            M2C_CHECK(q < Pt && Pt <= kPMax && j < n_items);
             const int D = Dof(t);
             const uint8_t *rec = ring + sm.roff[s];
             float pg, pu;

@@ -132,6 +132,7 @@ __global__ void __launch_bounds__(NT, 1)
         const int sl = sord[q];
         if ((hmask[sl >> 5] >> (sl & 31)) & 1u) continue;
         if (kpos < nm) {
+            M2C_CHECK(sl >= 0 && sl < C);
             vict[kpos] = sl;
             atomicOr(&tmask[sl >> 5], 1u << (sl & 31));
         } else {
@@ -162,10 +163,12 @@ __global__ void __launch_bounds__(NT, 1)
     }
     int tot_e;
     int epos = block_scan1(ne, &tot_e, scan_sm);
+    M2C_CHECK(tot_k >= nm && nm <= C);  // enough non-hit slots to take every miss
     for (int m = m0; m < m1; m++) {
         const int i = mpos[m];
         const int id = sR[i];
         const int sl = vict[m];
+        M2C_CHECK(i >= 0 && i < n && id >= 0 && sl >= 0 && sl < C);
         const int old = sord[m];
         if (old >= 0) {
             slot_of[old] = -1;
@@ -248,6 +251,7 @@ __global__ void __launch_bounds__(NT, 1)
     const int pos0 = pos;
     for (int i = i0; i < i1; i++)
         if (slot_of[R[i]] < 0) {
+            M2C_CHECK(pos < n && R[i] >= 0 && (F_r == 0 || R[i] < F_r));
             const int s16 = (qsrc && requant && tau > 0) ? a.slot_of[0][R[i]] : -1;
             if (qsrc) qsrc[seg + pos] = s16;
             nj += s16 >= 0;
@@ -308,6 +312,7 @@ __global__ void __launch_bounds__(256) k_fill(FillArgs a, const int32_t *__restr
         if (a.skip && a.skip[a.seg[tau] + m] >= 0) continue;  // (requantised on the GPU)
         const int id = miss_ids[a.seg[tau] + m];
         const int sl = miss_items[a.seg[tau] + m];
+        M2C_CHECK(id >= 0 && sl >= 0);
         const int64_t nv = a.nb[tau] / 16;
         const int si = a.stage_of[tau] ? a.stage_of[tau][id] : -1;  // staged by the lookahead?
         if (si >= 0 && lane == 0) atomicAdd(a.staged, 1ull);

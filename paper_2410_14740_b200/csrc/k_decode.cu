@@ -254,6 +254,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
     // engine: the set-up above overlapped the previous kernel; nothing it wrote is read above)
     griddep_wait();
     // layer 0's B slice -> smem (arrives during the prologue)
+    M2C_CHECK(nown_n * r <= kBMax && (cta < nchunk ? (nchunk - cta + G - 1) / G : 0) * 32 * r <= kBOff - kAtOff);
     if (tid == 0 && nown_n > 0) {
         mbar_expect_tx(&b_bar, (uint32_t)(nown_n * r));
         bulk_g2s_plain(S.ring + kBOff, p.layers[0].B + (int64_t)n0 * r, (uint32_t)(nown_n * r), &b_bar);
@@ -509,6 +510,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
                     const int q = ab + rk[u];
                     if (lane + 32 * u < c && q >= R_lo && q < R_hi) {
                         const int id = key_id(kv[u]);
+                        M2C_CHECK(id >= 0 && id < F_r && q < kk && q - R_lo < kMaxLocal);
                         S.loc[q - R_lo] = id;
                         lst[q] = id;
                     }
@@ -561,6 +563,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
                 int rk = 0;
                 for (int j = 0; j < m; j++) rk += cand[j] > cand[i];
                 const int id = key_id(cand[i]);
+                M2C_CHECK(id >= 0 && id < F_r && rk < n_items);
                 S.loc[rk] = id;
                 lst[R_lo + rk] = id;
             }
@@ -579,6 +582,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
             const int *loc = S.loc;
             auto src = [&](int j) -> const uint8_t * {
                 const int t = j < c1 ? 0 : (j < c2 ? 1 : 2);
+                M2C_CHECK(j >= 0 && j < n_items && loc[j] >= 0 && loc[j] < F_r);
                 return fa.pool[t] + (int64_t)loc[j] * fa.nb[t];
             };
             ffn_run(fa, d, p.act, n_items, c1, c2, src, S.ring, S.xs, S.a, sm, pipe, p.partial,

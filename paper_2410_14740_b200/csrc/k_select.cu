@@ -318,6 +318,7 @@ __global__ void __launch_bounds__(NT, 1) k_select(SelParams p) {
             const unsigned lt = (1u << lane) - 1u;
             const unsigned m = trs == 0 ? msk[0] : (trs == 1 ? msk[1] : msk[2]);
             const int pos = prefix_sh[trs] + blk_cnt[warp][trs] + __popc(m & lt);
+            M2C_CHECK(pos >= 0 && pos < (trs == 0 ? p.k16 : (trs == 1 ? p.k8 : p.k - p.k16 - p.k8)));
             p.tier_ids[seg[trs] + pos] = n;
         }
     }

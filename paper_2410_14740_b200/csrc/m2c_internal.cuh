@@ -412,6 +412,27 @@ __device__ __forceinline__ void fp16_fixed(unsigned b, int &m, int &sh, bool &ba
 // so the NEXT host call on the context returns M2C_ERR_STATE without synchronising
 // (SURVEY §8(b)).  err bits: 1 non-finite x, 4 grid-barrier timeout, 8 select count
 // mismatch, 16 p2p exchange timeout.
+// Bounds-checked build (-DM2C_CHECKS=1, tests/test_gpu_checked.py): index and capacity
+// invariants at the kernels' computed addresses trap (the launch fails) instead of corrupting
+// memory -- the stand-in for compute-sanitizer, which this GPU pool refuses.  Compiled out of
+// the product build.
+#ifndef M2C_CHECKS
+#define M2C_CHECKS 0
+#endif
+#if M2C_CHECKS
+#define M2C_CHECK(c)                                                                         \
+    do {                                                                                     \
+        if (!(c)) {                                                                          \
+            printf("m2c check failed: %s (%s:%d, block %d thread %d)\n", #c, __FILE__, __LINE__, \
+                   (int)blockIdx.x, (int)threadIdx.x);                                       \
+            __trap();                                                                        \
+        }                                                                                    \
+    } while (0)
+#else
+#define M2C_CHECK(c) \
+    do {             \
+    } while (0)
+#endif
 __device__ __forceinline__ void flag_error(uint32_t *err, unsigned bit) {
     atomicOr(err, bit);
     uint32_t *mirror = *reinterpret_cast<uint32_t *const *>(err + 2);
