@@ -329,21 +329,28 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
             if (nown_n > 0) mbar_wait(&b_bar, (uint32_t)(l & 1));  // this layer's B slice
             __syncthreads();
             STAMP(21);
-            // s_n = B_n . hq: LPN = r/16 lanes per neuron, one 16-B chunk each (consecutive
-            // lanes read consecutive smem: conflict-free), dp4a, shuffles over the LPN lanes
-            const int LPN = r / 16, npw = 32 / LPN, part = lane % LPN, sub = lane / LPN;
-            const int4 hv4 = reinterpret_cast<const int4 *>(hq)[part];
+            // s_n = B_n . hq: LPN = min(r/16, 8) lanes per neuron, CH = r/16/LPN 16-B chunks
+            // each (part + LPN c: the 8 lanes of a quarter-warp read 128 contiguous bytes of one
+            // neuron, conflict-free), dp4a, shuffles over the LPN lanes -- 4 neurons per warp
+            // pass at r = 256 (2 with 16 lanes of one chunk: twice the passes at S70H)
+            const int LPN = min(r / 16, 8), CH = r / 16 / LPN, npw = 32 / LPN, part = lane % LPN,
+                      sub = lane / LPN;
+            const int4 *hq4 = reinterpret_cast<const int4 *>(hq);
             const int8_t *Bs = reinterpret_cast<const int8_t *>(S.ring + kBOff);
             int *sc = reinterpret_cast<int *>(S.ring + kHistOff);  // [nown_n] (<= 48 KB)
             for (int i0 = warp * npw; i0 < nown_n; i0 += NW * npw) {
                 const int i = i0 + sub;
                 int acc = 0;
                 if (i < nown_n) {
-                    const int4 bv = *reinterpret_cast<const int4 *>(Bs + (int64_t)i * r + 16 * part);
-                    acc = __dp4a(bv.x, hv4.x, acc);
-                    acc = __dp4a(bv.y, hv4.y, acc);
-                    acc = __dp4a(bv.z, hv4.z, acc);
-                    acc = __dp4a(bv.w, hv4.w, acc);
+#pragma unroll 4
+                    for (int ch = 0; ch < CH; ch++) {
+                        const int4 bv = *reinterpret_cast<const int4 *>(Bs + (int64_t)i * r + 16 * (part + LPN * ch));
+                        const int4 hv4 = hq4[part + LPN * ch];
+                        acc = __dp4a(bv.x, hv4.x, acc);
+                        acc = __dp4a(bv.y, hv4.y, acc);
+                        acc = __dp4a(bv.z, hv4.z, acc);
+                        acc = __dp4a(bv.w, hv4.w, acc);
+                    }
                 }
                 for (int o = LPN / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
                 if (part == 0 && i < nown_n) sc[i] = acc;
