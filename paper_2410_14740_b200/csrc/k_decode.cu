@@ -312,8 +312,9 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
         const int shl = __ldcg(p.bin_sh + l);  // this token's histogram scale for layer l
         {
             int8_t *hq = reinterpret_cast<int8_t *>(S.ring + kRfOff);
-            for (int i = tid; i < d / 8; i += NT) S.xs[i] = __ldcg(reinterpret_cast<const uint4 *>(p.x) + i);
+            // (h first: its L2 round trip overlaps x's instead of following it)
             long long hv0 = tid < r ? __ldcg(hcur + (int64_t)tid * kHStride) : 0;
+            for (int i = tid; i < d / 8; i += NT) S.xs[i] = __ldcg(reinterpret_cast<const uint4 *>(p.x) + i);
             unsigned long long mh = (unsigned long long)(hv0 < 0 ? -hv0 : hv0);
             for (int i = tid + NT; i < r; i += NT) {
                 const long long v = __ldcg(hcur + (int64_t)i * kHStride);
