@@ -202,7 +202,7 @@ __device__ __forceinline__ void h_chunks(const int8_t *At, int nc, int r, const 
     }
 }
 
-template <int MAXT>
+template <int MAXT, bool HLDG = false>
 __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ FfnShared sm;
@@ -379,11 +379,12 @@ __global__ void __launch_bounds__(MAXT, 1) k_decode(DecArgs p) {
         // ================= P3: this CTA's share of the selection, in rank order ============
         int *hs = reinterpret_cast<int *>(S.ring + kHistOff);
         int *need = reinterpret_cast<int *>(S.ring + kNeedOff);
-        // 512 threads (d <= 4096): every thread loads its own run of 8 bins (two 16-B loads)
-        // straight into registers for the scan and keeps a copy in hs for the ranking (S7 +1.2%
-        // same-box); 1024-thread launches (S70H, S13's 640 threads) keep one TMA copy of the
-        // histogram, measured 0.6-0.9% faster there
-        constexpr bool M2C_HIST_LDG = MAXT == 512;
+        // HLDG (the instance for exactly 512 threads, S7): every thread loads its own run of 8
+        // bins (two 16-B loads) straight into registers for the scan and keeps a copy in hs for
+        // the ranking (S7 +0.8-1.2% same-box); the other instances (S70H, S13's 640 threads,
+        // T's 32: 128 bins per thread) keep one TMA copy of the histogram, measured 0.6-0.9% /
+        // ~10% faster there
+        constexpr bool M2C_HIST_LDG = HLDG;
         if (tid == 0) {
             if (!M2C_HIST_LDG) {
                 // order the ring's earlier generic accesses (and the acquired global data)
@@ -816,6 +817,8 @@ cudaError_t init_decode_attrs() {
     cudaError_t e = cudaFuncSetAttribute(k_decode<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)kSmemBytes);
     if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_decode<512, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+    if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_decode<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_sort_tiers, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * (kSortFr / 32 + 32));
@@ -900,9 +903,11 @@ cudaError_t launch_decode(m2c_ctx *c, __half *x, unsigned long long *prof, cudaS
         attr[1].val.programmaticStreamSerializationAllowed = 1;
         cfg.numAttrs = 2;
     }
-    // <= 512 threads (d <= 4096): 128 registers per thread; else 64
-    cudaError_t e = d / 8 <= 512 ? cudaLaunchKernelEx(&cfg, k_decode<512>, a)
-                                 : cudaLaunchKernelEx(&cfg, k_decode<1024>, a);
+    // <= 512 threads (d <= 4096): 128 registers per thread; else 64 (exactly 512: the instance
+    // with the register-run histogram load)
+    cudaError_t e = d / 8 == 512  ? cudaLaunchKernelEx(&cfg, k_decode<512, true>, a)
+                    : d / 8 < 512 ? cudaLaunchKernelEx(&cfg, k_decode<512>, a)
+                                  : cudaLaunchKernelEx(&cfg, k_decode<1024>, a);
     c->launch_counter++;
     return e;
 }
