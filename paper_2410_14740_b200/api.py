@@ -328,7 +328,9 @@ class M2CContext:
         check(lib().m2c_cache_state(self._h, layer, tier, None, None, C.byref(cap)))
         occ = torch.empty(max(cap.value, 1), dtype=torch.int32, device=self.device)
         last = torch.empty(max(cap.value, 1), dtype=torch.int32, device=self.device)
-        check(lib().m2c_cache_state(self._h, layer, tier, _ptr(occ), _ptr(last), C.byref(cap)))
+        # (the copies run on the compute stream: _call orders the caller's stream after them --
+        # reading the tensors unordered returned stale blocks of the caching allocator)
+        self._call(lib().m2c_cache_state, self._h, layer, tier, _ptr(occ), _ptr(last), C.byref(cap))
         return occ[:cap.value], last[:cap.value]
 
     def set_graph(self, enable: bool):
